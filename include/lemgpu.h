@@ -1,0 +1,189 @@
+/*
+ * lemgpu.h -- C-ABI of the B200-native D8 landscape-evolution step.
+ *
+ * This is the ONLY seam between host code and the sm_100a kernels.  Plain C
+ * types, caller-owned host buffers, an opaque device context.  It replaces
+ * the body of one reference execution strategy:
+ *
+ *   lem::strategy_step(Raster<double>& elev, const GridGraph&, const SimParams&,
+ *                      const StepSetup&, const Strategy&, SimWorkspace&,
+ *                      const StepInstrumentation*)        proj/include/lem/scheduler.hpp:38-41
+ *     -> dispatch switch                                   proj/src/scheduler.cpp:425-462
+ *   lem::run_simulation(Raster<double>, const RunConfig&,
+ *                       const StepCallback&)               proj/include/lem/scheduler.hpp:61-62
+ *     -> stepping loop                                     proj/src/scheduler.cpp:490-498
+ *
+ * A maintainer adds StrategyKind::kRbGpu ("rb_gpu", proj/include/lem/strategy.hpp:12-56)
+ * and routes it here; see INTEGRATION.md for the C++ shim and the ctypes
+ * binding the Python tests use.
+ *
+ * Status codes mirror the reference's exception classes
+ * (proj/include/lem/error.hpp:10-43) the way ErrorCollector::rethrow does
+ * (proj/src/scheduler.cpp:45-49):
+ *   0 ok, 1 ConfigError, 2 StructureError (cycle), 3 ConvergenceError(cell),
+ *   4 CUDA error (lem::Error), 5 other lem::Error.
+ *
+ * Threading: calls on one context are serialised on that context's CUDA
+ * stream and are not thread-safe; distinct contexts are independent.
+ */
+#ifndef LEMGPU_H
+#define LEMGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LEMGPU_ABI_VERSION 1
+#define LEMGPU_NOFLOW 0xFFFFFFFFu /* kNoFlow, proj/include/lem/raster.hpp:16 */
+
+enum {
+  LEMGPU_OK = 0,
+  LEMGPU_ECONFIG = 1,
+  LEMGPU_ESTRUCTURE = 2,
+  LEMGPU_ECONVERGENCE = 3,
+  LEMGPU_ECUDA = 4,
+  LEMGPU_EOTHER = 5
+};
+
+/* Phase slots, same order as lem::Phase (proj/include/lem/simulation.hpp:19-22). */
+enum {
+  LEMGPU_PHASE_RECEIVERS = 0,
+  LEMGPU_PHASE_DONORS = 1,
+  LEMGPU_PHASE_ORDER = 2,
+  LEMGPU_PHASE_ACCUM = 3,
+  LEMGPU_PHASE_UPLIFT = 4,
+  LEMGPU_PHASE_EROSION = 5
+};
+
+/* POD mirror of lem::SimParams (proj/include/lem/erosion.hpp:15-25) plus the
+ * neighbourhood connectivity of RunConfig (proj/include/lem/config.hpp:63). */
+typedef struct lemgpu_params {
+  double K;           /* erodibility                        (erosion.hpp:16) */
+  double m_exp;       /* drainage-area exponent             (erosion.hpp:17) */
+  double n_exp;       /* slope exponent, > 0                (erosion.hpp:18) */
+  double uplift_rate; /* interior uplift per unit time      (erosion.hpp:19) */
+  double dt;          /* implicit timestep                  (erosion.hpp:20) */
+  double epsilon;     /* Newton step-difference tolerance   (erosion.hpp:21) */
+  double dx, dy;      /* cell spacing                       (erosion.hpp:22-23) */
+  int32_t max_newton_iters; /*                              (erosion.hpp:24) */
+  int32_t connectivity;     /* 4 or 8                       (config.hpp:63) */
+} lemgpu_params;
+
+/* Per-realisation overrides for an ensemble context (paper future work,
+ * PAPER.md:749): each member runs with its own K and m. */
+typedef struct lemgpu_member {
+  double K;
+  double m_exp;
+} lemgpu_member;
+
+/* Mirror of lem::StepDiagnostics + PhaseTimings
+ * (proj/include/lem/simulation.hpp:25-40), plus device-side facts. */
+typedef struct lemgpu_diag {
+  double seconds[6];        /* per-phase device time (globaltimer), lem::Phase order */
+  uint64_t newton_iters;    /* sum of Newton iterations over eroded cells (erosion.cpp:76-77) */
+  uint32_t interior_noflow; /* interior cells with rec == kNoFlow (simulation.cpp:42-44) */
+  uint32_t nlevels;         /* TraversalPlan::nlevels() (traversal.hpp:34) */
+  uint32_t lut_misses;      /* cells whose pow(A,m) was not served by the host-libm LUT */
+  uint32_t status;          /* LEMGPU_* for this step */
+  uint32_t err_cell;        /* ConvergenceError::cell() when status == 3 */
+  uint32_t reserved;
+} lemgpu_diag;
+
+typedef struct lemgpu_ctx lemgpu_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* One DEM of width x height on CUDA device `device`.  Validates params the
+ * way SimParams::validate does (proj/src/erosion.cpp:10-17) and the grid
+ * bounds of RunConfig::validate (proj/src/config.cpp:155-173).
+ * Replaces: SimWorkspace construction (proj/include/lem/simulation.hpp:43-52). */
+int lemgpu_create(int device, uint32_t width, uint32_t height, const lemgpu_params* params,
+                  lemgpu_ctx** out);
+
+/* `members` independent realisations of width x height, batched into the
+ * same launches (stacked row-major, member-major).  per_member may be NULL
+ * (all members use params->K / params->m_exp). */
+int lemgpu_create_ensemble(int device, uint32_t width, uint32_t height, uint32_t members,
+                           const lemgpu_params* params, const lemgpu_member* per_member,
+                           lemgpu_ctx** out);
+
+void lemgpu_destroy(lemgpu_ctx* ctx);
+
+/* ---- state ------------------------------------------------------------- */
+
+/* Copy all members' elevations in / out (member-major, row-major, f64).
+ * Upload rejects non-finite values like run_simulation does
+ * (proj/src/scheduler.cpp:474-477) -> LEMGPU_ECONFIG. */
+int lemgpu_upload_elev(lemgpu_ctx* ctx, const double* host);
+int lemgpu_download_elev(lemgpu_ctx* ctx, double* host);
+
+/* Device-side lem::generate_terrain (proj/src/terrain.cpp:19-31), bit-exact;
+ * seeds[m] for member m (seeds may be NULL -> seed 42 for every member). */
+int lemgpu_generate_terrain(lemgpu_ctx* ctx, const uint64_t* seeds);
+
+/* ---- stepping ---------------------------------------------------------- */
+
+/* Run nsteps timesteps with the elevation device-resident, then synchronise.
+ * per_step (nullable) receives nsteps diagnostics.  On a failing step the
+ * call stops there and returns its status; later steps are not run.
+ * Replaces: the run_simulation loop (proj/src/scheduler.cpp:490-498). */
+int lemgpu_step(lemgpu_ctx* ctx, uint32_t nsteps, lemgpu_diag* per_step);
+
+/* Enqueue nsteps without synchronising (diagnostics stay on the device
+ * until lemgpu_sync).  For timing loops. */
+int lemgpu_step_async(lemgpu_ctx* ctx, uint32_t nsteps);
+
+/* Synchronise; copies out up to `cap` diagnostics of the steps enqueued
+ * since the last sync (oldest first) and returns the first failing status. */
+int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count);
+
+/* One lem::strategy_step on a HOST raster: upload elev, one step, download
+ * elev (the drop-in semantics of strategy_step(Raster<double>&, ...)).
+ * Replaces: proj/src/scheduler.cpp:408-464 for StrategyKind::kRbGpu. */
+int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag);
+
+/* ---- inspection (parity / debug) -------------------------------------- */
+
+/* Graph of the LAST step, in the reference's formats:
+ *   rec[N]            FlowGraph::rec            (flow_graph.hpp:23)
+ *   dnum[N]           FlowGraph::dnum           (flow_graph.hpp:25)
+ *   donor[N*conn]     FlowGraph::donor slots, kNoFlow-padded (flow_graph.hpp:24)
+ *   order[N]          TraversalPlan::order      (traversal.hpp:21)
+ *   levels[nlevels+1] TraversalPlan::levels     (traversal.hpp:22)
+ *   A[N]              AccumField::values        (accumulation.hpp:13-16)
+ * Any pointer may be NULL.  `levels` must hold N+2 entries when non-NULL. */
+int lemgpu_download_graph(lemgpu_ctx* ctx, uint32_t* rec, uint8_t* dnum, uint32_t* donor,
+                          uint32_t* order, uint32_t* levels, uint32_t* nlevels, double* A);
+
+/* Per-member statistics of the current elevation: out[4*m + {0,1,2,3}] =
+ * {mean h, max h, min h, sum h}.  Deterministic (fixed reduction order).
+ * `device_out` is a DEVICE pointer written on the context's stream. */
+int lemgpu_member_stats_device(lemgpu_ctx* ctx, double* device_out);
+
+/* ---- errors ------------------------------------------------------------ */
+const char* lemgpu_error_message(const lemgpu_ctx* ctx);
+uint32_t lemgpu_error_cell(const lemgpu_ctx* ctx);
+
+/* ---- plumbing ---------------------------------------------------------- */
+uint32_t lemgpu_abi_version(void);
+uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx);     /* members * width * height */
+void* lemgpu_stream(lemgpu_ctx* ctx);                 /* the context's cudaStream_t */
+int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
+
+/* Per-kernel device time, accumulated over the steps since the last reset
+ * (CUDA events around each launch on the context stream; enable first).
+ * ms[0] = recv_donor, ms[1] = flow (order+accum+uplift+erosion). */
+int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable);
+int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
+
+/* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */
+int lemgpu_host_register(void* ptr, size_t bytes);
+int lemgpu_host_unregister(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEMGPU_H */

@@ -1,0 +1,346 @@
+/*
+ * lem_oracle.c -- CPU restatement of the reference D8 timestep.
+ *
+ * TEST INFRASTRUCTURE ONLY: this is the parity checker for the B200 path.
+ * It is never linked into, loaded by, or called from the product library.
+ * Compile with -O2 -ffp-contract=off (the reference's own flags,
+ * CMakeLists.txt:14) so that every expression rounds exactly as the
+ * reference's does.
+ *
+ * Each function restates one reference function; citations are to the
+ * reference tree's proj/ directory.
+ */
+#include "lem_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* include/lem/erosion.hpp:16-24 -- default SimParams. */
+void lo_default_params(lo_params* p) {
+  p->K = 2e-6;
+  p->m_exp = 0.5;
+  p->n_exp = 1.0;
+  p->uplift_rate = 2e-3;
+  p->dt = 1000.0;
+  p->epsilon = 1e-6;
+  p->dx = 1.0;
+  p->dy = 1.0;
+  p->max_newton_iters = 100;
+}
+
+/* include/lem/neighborhood.hpp:17-23 -- offset_length. */
+double lo_offset_length(int dx, int dy, double sx, double sy) {
+  const double ox = dx * sx;
+  const double oy = dy * sy;
+  if (dy == 0) return fabs(ox);
+  if (dx == 0) return fabs(oy);
+  return sqrt(ox * ox + oy * oy);
+}
+
+/* src/neighborhood.cpp:9-45 -- frozen D8 / D4 stencils. */
+int lo_make_nbh(int connectivity, double dx, double dy, lo_nbh* n) {
+  static const int d8x[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+  static const int d8y[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+  static const int d4x[4] = {0, -1, 1, 0};
+  static const int d4y[4] = {-1, 0, 0, 1};
+  memset(n, 0, sizeof(*n));
+  if (connectivity != 4 && connectivity != 8) return LO_ECONFIG;
+  n->connectivity = connectivity;
+  n->dx = dx;
+  n->dy = dy;
+  for (int i = 0; i < connectivity; ++i) {
+    n->ox[i] = connectivity == 8 ? d8x[i] : d4x[i];
+    n->oy[i] = connectivity == 8 ? d8y[i] : d4y[i];
+    n->dist[i] = lo_offset_length(n->ox[i], n->oy[i], dx, dy);
+  }
+  return LO_OK;
+}
+
+/* src/terrain.cpp:12-17 -- splitmix64. */
+uint64_t lo_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* src/terrain.cpp:19-31 -- generate_terrain. */
+void lo_generate_terrain(uint32_t w, uint32_t h, uint64_t seed, double* out) {
+  const size_t n = (size_t)w * h;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t z = lo_splitmix64(seed + (uint64_t)i * 0x9E3779B97F4A7C15ull);
+    out[i] = (double)(z >> 11) * 0x1.0p-53;
+  }
+}
+
+uint64_t lo_fnv1a64(const void* data, size_t nbytes) {
+  const unsigned char* p = (const unsigned char*)data;
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < nbytes; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+static int is_perimeter(size_t c, int w, int h) {
+  const int x = (int)(c % (size_t)w), y = (int)(c / (size_t)w);
+  return x == 0 || x == w - 1 || y == 0 || y == h - 1;
+}
+
+/* include/lem/flow_graph.hpp:44-59 steepest_receiver, :74-80 compute_receivers,
+ * with include/lem/grid_graph.hpp:37-47 for_each_neighbor (off-grid skipped). */
+void lo_receivers(const double* elev, int w, int h, const lo_nbh* nbh, uint32_t* rec) {
+  const size_t n = (size_t)w * h;
+  for (size_t c = 0; c < n; ++c) {
+    if (is_perimeter(c, w, h)) {
+      rec[c] = LO_NOFLOW;
+      continue;
+    }
+    const int x = (int)(c % (size_t)w), y = (int)(c / (size_t)w);
+    double s_max = 0.0;
+    uint32_t n_max = LO_NOFLOW;
+    const double ec = elev[c];
+    for (int i = 0; i < nbh->connectivity; ++i) {
+      const int nx = x + nbh->ox[i], ny = y + nbh->oy[i];
+      if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
+      const uint32_t nb = (uint32_t)ny * (uint32_t)w + (uint32_t)nx;
+      const double s = (ec - elev[nb]) / nbh->dist[i];
+      if (s > s_max) {
+        s_max = s;
+        n_max = nb;
+      }
+    }
+    rec[c] = n_max;
+  }
+}
+
+/* include/lem/flow_graph.hpp:64-72 donors_of, :82-90 compute_donors. */
+void lo_donors(const uint32_t* rec, int w, int h, const lo_nbh* nbh, uint32_t* donor,
+               uint8_t* dnum) {
+  const size_t n = (size_t)w * h;
+  const int dmax = nbh->connectivity;
+  for (size_t c = 0; c < n; ++c) {
+    const int x = (int)(c % (size_t)w), y = (int)(c / (size_t)w);
+    uint8_t k = 0;
+    for (int i = 0; i < nbh->connectivity; ++i) {
+      const int nx = x + nbh->ox[i], ny = y + nbh->oy[i];
+      if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
+      const uint32_t nb = (uint32_t)ny * (uint32_t)w + (uint32_t)nx;
+      if (rec[nb] == (uint32_t)c) donor[(size_t)dmax * c + k++] = nb;
+    }
+    for (int i = k; i < dmax; ++i) donor[(size_t)dmax * c + i] = LO_NOFLOW;
+    dnum[c] = k;
+  }
+}
+
+/* Same kernels over tests/fixtures.hpp ExplicitGraph (CSR adjacency). */
+void lo_receivers_explicit(size_t n, const uint32_t* adj_off, const uint32_t* adj_nbr,
+                           const double* adj_dist, const uint8_t* boundary,
+                           const double* elev, uint32_t* rec) {
+  for (size_t c = 0; c < n; ++c) {
+    if (boundary[c]) {
+      rec[c] = LO_NOFLOW;
+      continue;
+    }
+    double s_max = 0.0;
+    uint32_t n_max = LO_NOFLOW;
+    for (uint32_t j = adj_off[c]; j < adj_off[c + 1]; ++j) {
+      const double s = (elev[c] - elev[adj_nbr[j]]) / adj_dist[j];
+      if (s > s_max) {
+        s_max = s;
+        n_max = adj_nbr[j];
+      }
+    }
+    rec[c] = n_max;
+  }
+}
+
+void lo_donors_explicit(size_t n, int dmax, const uint32_t* adj_off, const uint32_t* adj_nbr,
+                        const uint32_t* rec, uint32_t* donor, uint8_t* dnum) {
+  for (size_t c = 0; c < n; ++c) {
+    uint8_t k = 0;
+    for (uint32_t j = adj_off[c]; j < adj_off[c + 1]; ++j)
+      if (rec[adj_nbr[j]] == (uint32_t)c) donor[(size_t)dmax * c + k++] = adj_nbr[j];
+    for (int i = k; i < dmax; ++i) donor[(size_t)dmax * c + i] = LO_NOFLOW;
+    dnum[c] = k;
+  }
+}
+
+/* src/traversal.cpp:19-48 -- generate_queue (BFS level sets). */
+int lo_generate_queue(size_t n, const uint32_t* rec, const uint32_t* donor,
+                      const uint8_t* dnum, int dmax, uint32_t* order, uint32_t* levels,
+                      uint32_t* nlevels) {
+  size_t sz = 0;
+  uint32_t nl = 0;
+  levels[0] = 0;
+  for (size_t c = 0; c < n; ++c)
+    if (rec[c] == LO_NOFLOW) order[sz++] = (uint32_t)c;
+  levels[++nl] = (uint32_t)sz;
+  size_t lo = 0, hi = sz;
+  while (lo < hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t c = order[i];
+      const size_t base = (size_t)dmax * c;
+      for (int k = 0; k < dnum[c]; ++k) {
+        if (sz >= n) return LO_ESTRUCTURE; /* cannot happen for a consistent table */
+        order[sz++] = donor[base + k];
+      }
+    }
+    lo = hi;
+    hi = sz;
+    if (hi > lo) levels[++nl] = (uint32_t)hi;
+  }
+  *nlevels = nl;
+  if (sz != n) return LO_ESTRUCTURE;
+  return LO_OK;
+}
+
+/* include/lem/accumulation.hpp:21-28 add_donor_flow; src/accumulation.cpp:7-26
+ * accumulate_into / accumulate (uniform weight w0), order swept back to front. */
+void lo_accumulate(size_t n, const uint32_t* order, const uint32_t* donor,
+                   const uint8_t* dnum, int dmax, double w0, double* A) {
+  for (size_t c = 0; c < n; ++c) A[c] = w0;
+  for (size_t i = n; i-- > 0;) {
+    const uint32_t c = order[i];
+    const size_t base = (size_t)dmax * c;
+    double a = A[c];
+    for (int k = 0; k < dnum[c]; ++k) a += A[donor[base + k]];
+    A[c] = a;
+  }
+}
+
+/* src/erosion.cpp:52-57 -- uplift (interior only). */
+void lo_uplift(double* elev, int w, int h, double du) {
+  const size_t n = (size_t)w * h;
+  for (size_t c = 0; c < n; ++c)
+    if (!is_perimeter(c, w, h)) elev[c] += du;
+}
+
+/* src/erosion.cpp:19-34 -- newton_erode_cell. */
+double lo_newton(double h0, double hn, double F, double n_exp, double eps, int max_iters,
+                 int* iters, int* converged) {
+  double hh = h0;
+  double h_prev = h0;
+  for (int it = 1; it <= max_iters; ++it) {
+    const double diff = hh - hn;
+    const double residual = hh - h0 + F * pow(diff, n_exp);
+    const double slope = 1.0 + F * n_exp * pow(diff, n_exp - 1.0);
+    hh -= residual / slope;
+    if (hh < hn) hh = hn;
+    const double delta = hh - h_prev;
+    h_prev = hh;
+    if (fabs(delta) <= eps) {
+      *iters = it;
+      *converged = 1;
+      return hh;
+    }
+  }
+  *iters = max_iters;
+  *converged = 0;
+  return hh;
+}
+
+/* include/lem/grid_graph.hpp:53-57 -- distance_between. */
+static double distance_between(uint32_t a, uint32_t b, int w, const lo_nbh* nbh) {
+  const int dx = (int)(b % (uint32_t)w) - (int)(a % (uint32_t)w);
+  const int dy = (int)(b / (uint32_t)w) - (int)(a / (uint32_t)w);
+  return lo_offset_length(dx, dy, nbh->dx, nbh->dy);
+}
+
+/* src/erosion.cpp:36-50 erode_one_cell and :66-81 erode (levels 1..L-1). */
+int lo_erode(double* elev, int w, int h, const lo_nbh* nbh, const uint32_t* order,
+             const uint32_t* levels, uint32_t nlevels, const uint32_t* rec, const double* A,
+             const lo_params* p, uint64_t* iters, uint32_t* err_cell) {
+  (void)h;
+  uint64_t total = 0;
+  for (uint32_t l = 1; l < nlevels; ++l) {
+    for (uint32_t i = levels[l]; i < levels[l + 1]; ++i) {
+      const uint32_t c = order[i];
+      const uint32_t r = rec[c];
+      const double dist = distance_between(c, r, w, nbh);
+      const double F = p->K * p->dt * pow(A[c], p->m_exp) / pow(dist, p->n_exp);
+      int it = 0, conv = 0;
+      const double hnew =
+          lo_newton(elev[c], elev[r], F, p->n_exp, p->epsilon, p->max_newton_iters, &it, &conv);
+      if (!conv) {
+        *iters = total;
+        *err_cell = c;
+        return LO_ECONVERGENCE;
+      }
+      elev[c] = hnew;
+      total += (uint64_t)it;
+    }
+  }
+  *iters = total;
+  return LO_OK;
+}
+
+/* src/simulation.cpp:31-89 -- simulate_front + simulate_step (queue order, D8
+ * or D4 routing, uniform cell-area weights). */
+int lo_step(double* elev, int w, int h, int connectivity, const lo_params* p,
+            lo_step_out* out) {
+  lo_nbh nbh;
+  if (lo_make_nbh(connectivity, p->dx, p->dy, &nbh) != LO_OK) return LO_ECONFIG;
+  const size_t n = (size_t)w * h;
+  const int dmax = connectivity;
+  uint32_t* rec = out->rec ? out->rec : (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* donor = out->donor ? out->donor : (uint32_t*)malloc(n * dmax * sizeof(uint32_t));
+  uint8_t* dnum = out->dnum ? out->dnum : (uint8_t*)malloc(n);
+  uint32_t* order = out->order ? out->order : (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* levels = out->levels ? out->levels : (uint32_t*)malloc((n + 2) * sizeof(uint32_t));
+  double* A = out->A ? out->A : (double*)malloc(n * sizeof(double));
+  int rc = LO_OK;
+
+  lo_receivers(elev, w, h, &nbh, rec);
+  uint32_t pits = 0;
+  for (size_t c = 0; c < n; ++c)
+    if (rec[c] == LO_NOFLOW && !is_perimeter(c, w, h)) ++pits;
+  out->interior_noflow = pits;
+  lo_donors(rec, w, h, &nbh, donor, dnum);
+  rc = lo_generate_queue(n, rec, donor, dnum, dmax, order, levels, &out->nlevels);
+  if (rc == LO_OK) {
+    lo_accumulate(n, order, donor, dnum, dmax, p->dx * p->dy, A);
+    lo_uplift(elev, w, h, p->uplift_rate * p->dt);
+    out->err_cell = LO_NOFLOW;
+    rc = lo_erode(elev, w, h, &nbh, order, levels, out->nlevels, rec, A, p, &out->newton_iters,
+                  &out->err_cell);
+  }
+  if (!out->rec) free(rec);
+  if (!out->donor) free(donor);
+  if (!out->dnum) free(dnum);
+  if (!out->order) free(order);
+  if (!out->levels) free(levels);
+  if (!out->A) free(A);
+  return rc;
+}
+
+/* src/scheduler.cpp:466-500 -- run_simulation loop (rb_serial strategy). */
+int lo_run(double* elev, int w, int h, int connectivity, const lo_params* p, uint32_t steps,
+           uint64_t* newton_total, uint32_t* err_cell) {
+  const size_t n = (size_t)w * h;
+  lo_step_out o;
+  memset(&o, 0, sizeof(o));
+  o.rec = (uint32_t*)malloc(n * sizeof(uint32_t));
+  o.donor = (uint32_t*)malloc(n * connectivity * sizeof(uint32_t));
+  o.dnum = (uint8_t*)malloc(n);
+  o.order = (uint32_t*)malloc(n * sizeof(uint32_t));
+  o.levels = (uint32_t*)malloc((n + 2) * sizeof(uint32_t));
+  o.A = (double*)malloc(n * sizeof(double));
+  uint64_t total = 0;
+  int rc = LO_OK;
+  for (uint32_t s = 0; s < steps && rc == LO_OK; ++s) {
+    rc = lo_step(elev, w, h, connectivity, p, &o);
+    total += o.newton_iters;
+  }
+  *newton_total = total;
+  *err_cell = o.err_cell;
+  free(o.rec);
+  free(o.donor);
+  free(o.dnum);
+  free(o.order);
+  free(o.levels);
+  free(o.A);
+  return rc;
+}

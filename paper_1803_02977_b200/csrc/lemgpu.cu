@@ -1,0 +1,564 @@
+// lemgpu.cu -- host side of the C-ABI declared in include/lemgpu.h.
+//
+// Owns one device context per DEM (or per batch of ensemble members):
+// device buffers laid out for HBM (SoA, cell-major state + queue-position-major
+// scratch), one CUDA stream, and the launch sequence of one timestep:
+//   k_recv_donor  (regular launch, 2D tiles)
+//   k_flow        (cooperative launch, one persistent CTA set)
+// No phase ever runs on the CPU.  The host computes only what must come from
+// the host libm to be bit-identical with the reference: the stencil
+// distances (neighborhood.hpp:17-23), pow(dist, n) and the pow(A, m) table.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "lemgpu.h"
+#include "lemgpu_kernels.cuh"
+
+using namespace lemgpu;
+
+struct lemgpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  StepArgs a{};
+  lemgpu_params params{};
+  std::vector<lemgpu_member> members;
+  int flow_grid = 0;
+  // device allocations
+  double* d_kdt = nullptr;
+  double* d_mexp = nullptr;
+  double* d_lut = nullptr;
+  lemgpu_diag* d_diag = nullptr;
+  uint32_t diag_cap = 4096;
+  uint32_t pending = 0;  // steps enqueued since the last sync
+  uint32_t last_nlevels = 0;
+  bool have_graph = false;
+  uint64_t device_bytes = 0;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // 3 per pending step
+  double kernel_ms[2] = {0, 0};
+  uint32_t kernel_launches = 0;
+  // errors
+  std::string msg;
+  uint32_t err_cell = LEMGPU_NOFLOW;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int fail(lemgpu_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx)
+    ctx->msg = buf;
+  else
+    g_create_error = buf;
+  return code;
+}
+
+#define CU(ctx, call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail((ctx), LEMGPU_ECUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),    \
+                  __FILE__, __LINE__, cudaGetErrorString(e_));                                \
+  } while (0)
+
+// include/lem/neighborhood.hpp:17-23, compiled with -ffp-contract=off.
+double offset_length(int dx, int dy, double sx, double sy) {
+  const double ox = dx * sx;
+  const double oy = dy * sy;
+  if (dy == 0) return std::fabs(ox);
+  if (dx == 0) return std::fabs(oy);
+  return std::sqrt(ox * ox + oy * oy);
+}
+
+// SimParams::validate (proj/src/erosion.cpp:10-17).
+int validate(const lemgpu_params* p, std::string& why) {
+  if (!(p->dt > 0)) return why = "dt must be > 0", 1;
+  if (!(p->epsilon > 0)) return why = "epsilon must be > 0", 1;
+  if (!(p->K >= 0)) return why = "K must be >= 0", 1;
+  if (!(p->n_exp > 0)) return why = "n_exp must be > 0", 1;
+  if (!(p->dx > 0) || !(p->dy > 0)) return why = "cell spacing must be > 0", 1;
+  if (p->max_newton_iters < 1) return why = "max_newton_iters must be >= 1", 1;
+  if (p->connectivity == 6) return why = "hexagonal (6-connected) grids are not implemented", 1;
+  if (p->connectivity != 4 && p->connectivity != 8)
+    return why = "connectivity must be 4 or 8, got " + std::to_string(p->connectivity), 1;
+  return 0;
+}
+
+// True when every sum of k <= nmax copies of w is exactly k*w, i.e. w's
+// significand leaves room for log2(nmax) more bits.  Then A is a function
+// of the integer donor count and pow(A, m) can come from a host table.
+bool area_sums_exact(double w, uint64_t nmax) {
+  int e;
+  double m = std::frexp(w, &e);  // w = m * 2^e, m in [0.5,1)
+  uint64_t sig = (uint64_t)std::ldexp(m, 53);
+  int tz = 0;
+  while (tz < 53 && !(sig & 1)) {
+    sig >>= 1;
+    ++tz;
+  }
+  const int sig_bits = 53 - tz;
+  int need = 0;
+  while (need < 64 && (1ull << need) <= nmax) ++need;
+  return sig_bits + need <= 53;
+}
+
+template <typename T>
+int dmalloc(lemgpu_ctx* ctx, T** p, size_t count) {
+  const size_t bytes = count * sizeof(T);
+  CU(ctx, cudaMalloc((void**)p, bytes ? bytes : 16));
+  ctx->device_bytes += bytes;
+  return 0;
+}
+
+int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_params* p,
+                const lemgpu_member* per_member, lemgpu_ctx** out) {
+  *out = nullptr;
+  if (!p) return fail(nullptr, LEMGPU_ECONFIG, "params must not be NULL");
+  std::string why;
+  if (validate(p, why)) return fail(nullptr, LEMGPU_ECONFIG, "%s", why.c_str());
+  if (W < 3 || H < 3) return fail(nullptr, LEMGPU_ECONFIG, "raster must be at least 3x3");
+  if (M < 1) return fail(nullptr, LEMGPU_ECONFIG, "members must be >= 1");
+  const uint64_t N64 = (uint64_t)W * H * M;
+  if (N64 >= 0xFFFFFFFFull)  // config.cpp:159-161 caps the grid at 2^32-1 cells
+    return fail(nullptr, LEMGPU_ECONFIG, "grid of %llu cells exceeds 2^32-1", (unsigned long long)N64);
+
+  lemgpu_ctx* ctx = new (std::nothrow) lemgpu_ctx();
+  if (!ctx) return fail(nullptr, LEMGPU_EOTHER, "out of host memory");
+  ctx->device = device;
+  ctx->params = *p;
+  ctx->members.resize(M);
+  for (uint32_t m = 0; m < M; ++m)
+    ctx->members[m] = per_member ? per_member[m] : lemgpu_member{p->K, p->m_exp};
+  for (uint32_t m = 0; m < M; ++m) {
+    if (!(ctx->members[m].K >= 0)) {
+      delete ctx;
+      return fail(nullptr, LEMGPU_ECONFIG, "K must be >= 0 (member %u)", m);
+    }
+  }
+
+  auto bail = [&](int rc) {
+    g_create_error = ctx->msg;
+    lemgpu_destroy(ctx);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, LEMGPU_ECUDA, "cannot select CUDA device %d", device);
+  }
+  int coop = 0, nsm = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  if (!coop) {
+    delete ctx;
+    return fail(nullptr, LEMGPU_ECUDA, "device %d lacks cooperative launch", device);
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, LEMGPU_ECUDA, "cudaStreamCreate failed");
+  }
+
+  StepArgs& a = ctx->a;
+  const uint32_t N = (uint32_t)N64;
+  a.W = W;
+  a.H = H;
+  a.M = M;
+  a.N = N;
+  a.MN = W * H;
+  a.Htot = H * M;
+  a.perim = M * (2 * W + 2 * H - 4);
+  a.conn = p->connectivity;
+  a.nkind = p->n_exp == 1.0 ? 1 : p->n_exp == 2.0 ? 2 : 0;
+  a.maxit = p->max_newton_iters;
+  a.du = p->uplift_rate * p->dt;
+  a.w0 = p->dx * p->dy;  // SimParams::cell_area (erosion.hpp:26)
+  a.w0_is_one = a.w0 == 1.0;
+  a.n_exp = p->n_exp;
+  a.eps = p->epsilon;
+  a.dist_one = 0;
+  for (int k = 0; k < 8; ++k) {
+    a.off[k] = dir_oy(k) * (int)W + dir_ox(k);
+    a.dist[k] = offset_length(dir_ox(k), dir_oy(k), p->dx, p->dy);
+    if (a.dist[k] == 1.0) a.dist_one |= 1u << k;
+  }
+  a.powdist_h = std::pow(a.dist[3], p->n_exp);
+  a.powdist_v = std::pow(a.dist[1], p->n_exp);
+  a.powdist_d = std::pow(a.dist[0], p->n_exp);
+  a.lut_exact = area_sums_exact(a.w0, (uint64_t)a.MN) ? 1 : 0;
+  uint32_t lut_entries = a.MN < 65536u ? a.MN + 1 : 65537u;
+  if (const char* env = std::getenv("LEMGPU_LUT_ENTRIES")) lut_entries = (uint32_t)std::strtoul(env, nullptr, 10);
+  if (lut_entries < 2) lut_entries = 2;
+  a.lut_entries = lut_entries;
+
+  // host-libm tables (bit-identical with the reference's pow on this host)
+  std::vector<double> kdt(M), mexp(M), lut((size_t)M * lut_entries);
+  for (uint32_t m = 0; m < M; ++m) {
+    kdt[m] = ctx->members[m].K * p->dt;  // erosion.cpp:38: K * dt first
+    mexp[m] = ctx->members[m].m_exp;
+    double* row = lut.data() + (size_t)m * lut_entries;
+    for (uint32_t i = 0; i < lut_entries; ++i) row[i] = std::pow((double)i * a.w0, mexp[m]);
+  }
+
+  int rc;
+  if ((rc = dmalloc(ctx, &ctx->d_kdt, M)) || (rc = dmalloc(ctx, &ctx->d_mexp, M)) ||
+      (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &a.h, N)) ||
+      (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
+      (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) ||
+      (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
+      (rc = dmalloc(ctx, &a.Aq, N)) || (rc = dmalloc(ctx, &a.hq, N)) ||
+      (rc = dmalloc(ctx, &a.levels, (size_t)N + 2)) ||
+      (rc = dmalloc(ctx, &a.tstat, (size_t)N / kExTile + 2)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
+      (rc = dmalloc(ctx, &ctx->d_diag, ctx->diag_cap)))
+    return bail(rc);
+  a.kdt = ctx->d_kdt;
+  a.mexp = ctx->d_mexp;
+  a.lut = ctx->d_lut;
+#define CUB(call)                          \
+  do {                                     \
+    if ((call) != cudaSuccess) {           \
+      fail(ctx, LEMGPU_ECUDA, "%s", #call); \
+      return bail(LEMGPU_ECUDA);           \
+    }                                      \
+  } while (0)
+  CUB(cudaMemcpy(ctx->d_kdt, kdt.data(), M * sizeof(double), cudaMemcpyHostToDevice));
+  CUB(cudaMemcpy(ctx->d_mexp, mexp.data(), M * sizeof(double), cudaMemcpyHostToDevice));
+  CUB(cudaMemcpy(ctx->d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUB(cudaMemset(a.h, 0, (size_t)N * sizeof(double)));
+  CUB(cudaMemset(a.rcode, 0, (size_t)N + 16));
+  CUB(cudaMemset(a.dmask, 0, (size_t)N + 16));
+  CUB(cudaMemset(a.tstat, 0, ((size_t)N / kExTile + 2) * 8));
+  Ctl c0{};
+  c0.epoch = 1;
+  c0.err_cell = LEMGPU_NOFLOW;
+  c0.t_k1_begin = ~0ull;
+  c0.t_k1_end = 0;
+  CUB(cudaMemcpy(a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
+
+  // one persistent CTA set: every CTA must be co-resident (cooperative launch)
+  int per_sm = 0;
+  const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
+  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kTPB, 0));
+  if (per_sm < 1) {
+    fail(ctx, LEMGPU_ECUDA, "k_flow cannot be resident");
+    return bail(LEMGPU_ECUDA);
+  }
+  ctx->flow_grid = per_sm * nsm;
+  if (const char* env = std::getenv("LEMGPU_FLOW_CTAS_PER_SM")) {
+    const int want = std::atoi(env);
+    if (want >= 1 && want <= per_sm) ctx->flow_grid = want * nsm;
+  }
+  *out = ctx;
+  return LEMGPU_OK;
+#undef CUB
+}
+
+int enqueue_step(lemgpu_ctx* ctx) {
+  StepArgs a = ctx->a;
+  if (ctx->pending >= ctx->diag_cap) return fail(ctx, LEMGPU_EOTHER, "too many steps pending");
+  a.diag = ctx->d_diag + ctx->pending;
+  cudaEvent_t* ev = nullptr;
+  if (ctx->timing) {
+    while (ctx->ev.size() < 3 * (size_t)(ctx->pending + 1)) {
+      cudaEvent_t e;
+      CU(ctx, cudaEventCreate(&e));
+      ctx->ev.push_back(e);
+    }
+    ev = &ctx->ev[3 * ctx->pending];
+    CU(ctx, cudaEventRecord(ev[0], ctx->stream));
+  }
+  const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+  if (a.conn == 8)
+    k_recv_donor<8><<<g1, kTPB, 0, ctx->stream>>>(a);
+  else
+    k_recv_donor<4><<<g1, kTPB, 0, ctx->stream>>>(a);
+  CU(ctx, cudaGetLastError());
+  if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
+  void* args[] = {&a};
+  const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
+  CU(ctx, cudaLaunchCooperativeKernel(fk, dim3(ctx->flow_grid), dim3(kTPB), args, 0, ctx->stream));
+  if (ev) CU(ctx, cudaEventRecord(ev[2], ctx->stream));
+  ++ctx->pending;
+  ctx->have_graph = true;
+  return LEMGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t lemgpu_abi_version(void) { return LEMGPU_ABI_VERSION; }
+
+int lemgpu_create(int device, uint32_t width, uint32_t height, const lemgpu_params* params,
+                  lemgpu_ctx** out) {
+  return create_impl(device, width, height, 1, params, nullptr, out);
+}
+
+int lemgpu_create_ensemble(int device, uint32_t width, uint32_t height, uint32_t members,
+                           const lemgpu_params* params, const lemgpu_member* per_member,
+                           lemgpu_ctx** out) {
+  return create_impl(device, width, height, members, params, per_member, out);
+}
+
+void lemgpu_destroy(lemgpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  StepArgs& a = ctx->a;
+  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, a.h,   a.rcode,  a.dmask, a.order,
+                  a.ppos,     a.fc,        a.cdir,     a.Aq,  a.hq,     a.levels, a.tstat,
+                  a.ctl,      ctx->d_diag};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* lemgpu_error_message(const lemgpu_ctx* ctx) {
+  return ctx ? ctx->msg.c_str() : g_create_error.c_str();
+}
+uint32_t lemgpu_error_cell(const lemgpu_ctx* ctx) { return ctx ? ctx->err_cell : LEMGPU_NOFLOW; }
+uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx) { return ctx ? ctx->a.N : 0; }
+void* lemgpu_stream(lemgpu_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes) {
+  if (!ctx || !bytes) return LEMGPU_ECONFIG;
+  *bytes = ctx->device_bytes;
+  return LEMGPU_OK;
+}
+
+int lemgpu_upload_elev(lemgpu_ctx* ctx, const double* host) {
+  if (!ctx || !host) return fail(ctx, LEMGPU_ECONFIG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const StepArgs& a = ctx->a;
+  CU(ctx, cudaMemcpyAsync(a.h, host, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  // reject non-finite input (scheduler.cpp:474-477); reuse fc[N] as scratch
+  uint32_t* bad = a.fc + a.N;
+  CU(ctx, cudaMemsetAsync(bad, 0xFF, sizeof(uint32_t), ctx->stream));
+  k_check_finite<<<1184, kTPB, 0, ctx->stream>>>(a.h, a.N, bad);
+  uint32_t first = 0;
+  CU(ctx, cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (first != LEMGPU_NOFLOW)
+    return fail(ctx, LEMGPU_ECONFIG, "input terrain has a non-finite value at cell %u", first);
+  ctx->have_graph = false;
+  return LEMGPU_OK;
+}
+
+int lemgpu_download_elev(lemgpu_ctx* ctx, double* host) {
+  if (!ctx || !host) return fail(ctx, LEMGPU_ECONFIG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaMemcpyAsync(host, ctx->a.h, (size_t)ctx->a.N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return LEMGPU_OK;
+}
+
+int lemgpu_generate_terrain(lemgpu_ctx* ctx, const uint64_t* seeds) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const StepArgs& a = ctx->a;
+  std::vector<unsigned long long> s(a.M, 42ull);
+  if (seeds)
+    for (uint32_t m = 0; m < a.M; ++m) s[m] = seeds[m];
+  unsigned long long* d_seeds = nullptr;
+  CU(ctx, cudaMalloc(&d_seeds, a.M * sizeof(unsigned long long)));
+  CU(ctx, cudaMemcpy(d_seeds, s.data(), a.M * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  k_terrain<<<2368, kTPB, 0, ctx->stream>>>(a.h, a.N, a.MN, d_seeds);
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_seeds);
+  ctx->have_graph = false;
+  return LEMGPU_OK;
+}
+
+int lemgpu_step_async(lemgpu_ctx* ctx, uint32_t nsteps) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  for (uint32_t s = 0; s < nsteps; ++s) {
+    if (ctx->pending >= ctx->diag_cap) {
+      uint32_t cnt = 0;
+      const int rc = lemgpu_sync(ctx, nullptr, 0, &cnt);
+      if (rc) return rc;
+    }
+    const int rc = enqueue_step(ctx);
+    if (rc) return rc;
+  }
+  return LEMGPU_OK;
+}
+
+int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  const uint32_t n = ctx->pending;
+  std::vector<lemgpu_diag> d(n);
+  if (n) CU(ctx, cudaMemcpy(d.data(), ctx->d_diag, n * sizeof(lemgpu_diag), cudaMemcpyDeviceToHost));
+  if (ctx->timing && n) {
+    for (uint32_t s = 0; s < n; ++s) {
+      float t1 = 0, t2 = 0;
+      cudaEventElapsedTime(&t1, ctx->ev[3 * s], ctx->ev[3 * s + 1]);
+      cudaEventElapsedTime(&t2, ctx->ev[3 * s + 1], ctx->ev[3 * s + 2]);
+      ctx->kernel_ms[0] += t1;
+      ctx->kernel_ms[1] += t2;
+    }
+    ctx->kernel_launches += n;
+  }
+  ctx->pending = 0;
+  int status = LEMGPU_OK;
+  for (uint32_t s = 0; s < n; ++s) {
+    if (d[s].status != 0) {
+      status = d[s].status == 0xFFFFFFFFu ? LEMGPU_EOTHER : (int)d[s].status;
+      ctx->err_cell = d[s].err_cell;
+      if (status == LEMGPU_ECONVERGENCE)
+        fail(ctx, status, "Newton iteration did not converge at cell %u after %d iterations",
+             d[s].err_cell, ctx->params.max_newton_iters);
+      else if (status == LEMGPU_ESTRUCTURE)
+        fail(ctx, status, "receiver graph has a cycle: only %u of %u cells reachable from sources",
+             d[s].err_cell, ctx->a.N);
+      else
+        fail(ctx, status, "step %u failed with status %u", s, d[s].status);
+      // clear the sticky device flag so the context can be reused
+      Ctl c0{};
+      CU(ctx, cudaMemcpy(&c0, ctx->a.ctl, sizeof c0, cudaMemcpyDeviceToHost));
+      c0.err_flag = 0;
+      c0.err_cell = LEMGPU_NOFLOW;
+      c0.t_k1_begin = ~0ull;
+      c0.t_k1_end = 0;
+      CU(ctx, cudaMemcpy(ctx->a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
+      break;
+    }
+    ctx->last_nlevels = d[s].nlevels;
+  }
+  if (out)
+    for (uint32_t s = 0; s < n && s < cap; ++s) out[s] = d[s];
+  if (count) *count = n;
+  return status;
+}
+
+int lemgpu_step(lemgpu_ctx* ctx, uint32_t nsteps, lemgpu_diag* per_step) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  uint32_t done = 0;
+  while (done < nsteps) {
+    const uint32_t chunk = (nsteps - done) < ctx->diag_cap ? (nsteps - done) : ctx->diag_cap;
+    if (ctx->pending) {
+      const int rc0 = lemgpu_sync(ctx, nullptr, 0, nullptr);
+      if (rc0) return rc0;
+    }
+    int rc = lemgpu_step_async(ctx, chunk);
+    if (rc) return rc;
+    uint32_t cnt = 0;
+    rc = lemgpu_sync(ctx, per_step ? per_step + done : nullptr, chunk, &cnt);
+    if (rc) return rc;
+    done += chunk;
+  }
+  return LEMGPU_OK;
+}
+
+int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag) {
+  if (!ctx || !elev_inout) return fail(ctx, LEMGPU_ECONFIG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const StepArgs& a = ctx->a;
+  CU(ctx, cudaMemcpyAsync(a.h, elev_inout, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  int rc = lemgpu_step_async(ctx, 1);
+  if (rc) return rc;
+  CU(ctx, cudaMemcpyAsync(elev_inout, a.h, (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  lemgpu_diag d{};
+  uint32_t cnt = 0;
+  rc = lemgpu_sync(ctx, &d, 1, &cnt);
+  if (diag) *diag = d;
+  return rc;
+}
+
+int lemgpu_download_graph(lemgpu_ctx* ctx, uint32_t* rec, uint8_t* dnum, uint32_t* donor,
+                          uint32_t* order, uint32_t* levels, uint32_t* nlevels, double* A) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  if (!ctx->have_graph) return fail(ctx, LEMGPU_ECONFIG, "no step has run since the last upload");
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  const StepArgs& a = ctx->a;
+  const size_t N = a.N;
+  uint32_t* d_rec = nullptr;
+  uint8_t* d_dnum = nullptr;
+  uint32_t* d_donor = nullptr;
+  double* d_A = nullptr;
+  if (rec) CU(ctx, cudaMalloc(&d_rec, N * 4));
+  if (dnum) CU(ctx, cudaMalloc(&d_dnum, N));
+  if (donor) CU(ctx, cudaMalloc(&d_donor, N * a.conn * 4));
+  if (A) CU(ctx, cudaMalloc(&d_A, N * 8));
+  if (rec || dnum || donor) k_export_graph<<<2368, kTPB, 0, ctx->stream>>>(a, d_rec, d_dnum, d_donor);
+  if (A) k_export_accum<<<2368, kTPB, 0, ctx->stream>>>(a, d_A);
+  CU(ctx, cudaGetLastError());
+  if (rec) CU(ctx, cudaMemcpyAsync(rec, d_rec, N * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (dnum) CU(ctx, cudaMemcpyAsync(dnum, d_dnum, N, cudaMemcpyDeviceToHost, ctx->stream));
+  if (donor) CU(ctx, cudaMemcpyAsync(donor, d_donor, N * a.conn * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (A) CU(ctx, cudaMemcpyAsync(A, d_A, N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (order) CU(ctx, cudaMemcpyAsync(order, a.order, N * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (levels) CU(ctx, cudaMemcpyAsync(levels, a.levels, ((size_t)ctx->last_nlevels + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (nlevels) *nlevels = ctx->last_nlevels;
+  cudaFree(d_rec);
+  cudaFree(d_dnum);
+  cudaFree(d_donor);
+  cudaFree(d_A);
+  return LEMGPU_OK;
+}
+
+int lemgpu_member_stats_device(lemgpu_ctx* ctx, double* device_out) {
+  if (!ctx || !device_out) return fail(ctx, LEMGPU_ECONFIG, "null argument");
+  CU(ctx, cudaSetDevice(ctx->device));
+  const StepArgs& a = ctx->a;
+  const uint32_t chunks = 64;
+  // partials live in the accumulation scratch (Aq), which is per-step scratch
+  double* part = a.Aq;
+  if ((size_t)a.M * chunks * 3 > a.N) return fail(ctx, LEMGPU_ECONFIG, "members too small for stats scratch");
+  k_stats_partial<<<dim3(chunks, a.M), kTPB, 0, ctx->stream>>>(a.h, a.MN, chunks, part);
+  k_stats_final<<<(a.M + 127) / 128, 128, 0, ctx->stream>>>(part, a.M, chunks, a.MN, device_out);
+  CU(ctx, cudaGetLastError());
+  ctx->have_graph = false;  // Aq was clobbered
+  return LEMGPU_OK;
+}
+
+int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  ctx->timing = enable != 0;
+  ctx->kernel_ms[0] = ctx->kernel_ms[1] = 0;
+  ctx->kernel_launches = 0;
+  return LEMGPU_OK;
+}
+
+int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches) {
+  if (!ctx || !ms) return LEMGPU_ECONFIG;
+  ms[0] = ctx->kernel_ms[0];
+  ms[1] = ctx->kernel_ms[1];
+  if (launches) *launches = ctx->kernel_launches;
+  return LEMGPU_OK;
+}
+
+int lemgpu_host_register(void* ptr, size_t bytes) {
+  return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? LEMGPU_OK : LEMGPU_ECUDA;
+}
+int lemgpu_host_unregister(void* ptr) {
+  return cudaHostUnregister(ptr) == cudaSuccess ? LEMGPU_OK : LEMGPU_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+"""Parity of the sm_100a path (through the C-ABI) with the pinned CPU oracle.
+
+Bar: rec, dnum, donor slots, order, levels, A bit-exact; h
+bit-exact for n = 1; h within 1e-9 relative for n != 1; newton_iters and
+interior_noflow exact."""
+import json
+
+import numpy as np
+import pytest
+
+import paper_1803_02977_b200 as lem
+from _oracle import NOFLOW, Oracle, RefLib, fnv1a64, make_params
+
+pytestmark = pytest.mark.gpu
+
+ARRAYS = ("rec", "dnum", "donor", "order", "levels", "A")
+
+
+def sim_params(**kw):
+    return lem.SimParams(**kw)
+
+
+def device_ctx(w, h, conn=8, **kw):
+    return lem.DeviceContext(w, h, sim_params(**kw), conn)
+
+
+def compare_step(ctx, oracle_out, h_gpu, h_orc, exact_h=True, tag=""):
+    g = ctx.download_graph(donor=True)
+    for k in ARRAYS:
+        assert np.array_equal(g[k], oracle_out[k]), f"{tag}: {k} differs"
+    assert g["nlevels"] == oracle_out["nlevels"], tag
+    if exact_h:
+        bad = np.nonzero(h_gpu.view(np.uint64).ravel() != h_orc.view(np.uint64).ravel())[0]
+        assert bad.size == 0, f"{tag}: h differs at {bad[:5]} gpu={h_gpu.ravel()[bad[:3]]} cpu={h_orc.ravel()[bad[:3]]}"
+    else:
+        rel = np.abs(h_gpu - h_orc) / np.maximum(np.abs(h_orc), 1e-300)
+        assert rel.max() <= 1e-9, f"{tag}: max rel {rel.max()}"
+
+
+@pytest.mark.parametrize("path", sorted((__import__("pathlib").Path(__file__).parent / "golden").glob("small_*.npz")),
+                         ids=lambda p: p.stem)
+def test_small_golden(path):
+    g = np.load(path)
+    kw = json.loads(str(g["params"]))
+    w, h, conn = int(g["w"]), int(g["h"]), int(g["conn"])
+    ctx = device_ctx(w, h, conn, **kw)
+    ctx.upload(g["h0"])
+    d = ctx.step(1)[0]
+    out = ctx.download()
+    gr = ctx.download_graph(donor=True)
+    for k in ARRAYS:
+        assert np.array_equal(gr[k], g[k]), k
+    exact = kw.get("n_exp", 1.0) == 1.0
+    if exact:
+        assert np.array_equal(out.view(np.uint64), g["h1"].view(np.uint64))
+    else:
+        assert np.max(np.abs(out - g["h1"]) / np.abs(g["h1"])) <= 1e-9
+    assert d.newton_iters == int(g["newton_iters"]) or not exact
+    assert d.interior_noflow == int(g["interior_noflow"])
+    assert d.lut_misses == 0 or "m_exp" in kw or "dx" in kw
+
+
+@pytest.mark.parametrize("w,h,seed,conn,kw", [
+    (64, 64, 1, 8, {}),
+    (100, 77, 2, 8, {}),
+    (3, 3, 3, 8, {}),
+    (5, 200, 4, 8, {}),
+    (257, 129, 5, 8, {}),
+    (131, 70, 6, 4, {}),
+    (90, 61, 7, 8, {"dx": 0.5, "dy": 2.0}),
+    (120, 80, 8, 8, {"m_exp": 0.35, "K": 5e-6}),
+    (80, 80, 9, 8, {"K": 0.0}),
+    (1024, 33, 10, 8, {}),
+])
+def test_multistep_vs_oracle(oracle, w, h, seed, conn, kw):
+    p = make_params(**kw)
+    ctx = device_ctx(w, h, conn, **kw)
+    e = oracle.terrain(w, h, seed)
+    ctx.upload(e)
+    for s in range(8):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, conn=conn, params=p)
+        hg = ctx.download()
+        compare_step(ctx, o, hg, e, tag=f"{w}x{h} step {s}")
+        assert d.newton_iters == o["newton_iters"]
+        assert d.interior_noflow == o["interior_noflow"]
+        assert d.nlevels == o["nlevels"]
+
+
+def test_terrain_generation_bit_exact(oracle):
+    for (w, h, seed) in [(1000, 1000, 42), (37, 11, 7), (5, 5, 0)]:
+        assert np.array_equal(lem.generate_terrain(w, h, seed), oracle.terrain(w, h, seed))
+
+
+def test_anchor_1000(golden_dir):
+    a = json.loads((golden_dir / "anchors.json").read_text())["1000"]
+    ctx = device_ctx(1000, 1000)
+    ctx.generate_terrain([42])
+    assert fnv1a64(ctx.download()) == a["terrain"]
+    d1 = ctx.step(1)[0]
+    g = ctx.download_graph()
+    st = a["step1"]
+    assert fnv1a64(g["rec"]) == st["rec"]
+    assert fnv1a64(g["dnum"]) == st["dnum"]
+    assert fnv1a64(g["order"]) == st["order"]
+    assert fnv1a64(g["A"]) == st["A"]
+    assert g["levels"].tolist() == st["levels"]
+    assert fnv1a64(ctx.download()) == st["h"]
+    assert d1.newton_iters == st["newton_iters"] and d1.interior_noflow == st["interior_noflow"]
+    ds = ctx.step(119)
+    s120 = a["step120"]
+    assert fnv1a64(ctx.download()) == s120["h"]
+    assert d1.newton_iters + sum(d.newton_iters for d in ds) == s120["newton_total"]
+    assert all(d.lut_misses == 0 for d in ds)
+
+
+def test_anchor_10000(golden_dir):
+    anchors = json.loads((golden_dir / "anchors.json").read_text())
+    if "10000" not in anchors:
+        pytest.skip("10000^2 anchors not generated")
+    a = anchors["10000"]
+    ctx = device_ctx(10000, 10000)
+    ctx.generate_terrain([42])
+    assert fnv1a64(ctx.download()) == a["terrain"]
+    d1 = ctx.step(1)[0]
+    g = ctx.download_graph()
+    st = a["step1"]
+    for k in ("rec", "dnum", "order", "A"):
+        assert fnv1a64(g[k]) == st[k], k
+    assert g["levels"].tolist() == st["levels"]
+    assert fnv1a64(ctx.download()) == st["h"]
+    assert d1.newton_iters == st["newton_iters"] and d1.interior_noflow == st["interior_noflow"]
+    if "step120" in a:
+        ds = ctx.step(119)
+        assert fnv1a64(ctx.download()) == a["step120"]["h"]
+        assert d1.newton_iters + sum(d.newton_iters for d in ds) == a["step120"]["newton_total"]
+
+
+def test_10000_properties():
+    """Size-independent checks at the headline size."""
+    n = 10000
+    ctx = device_ctx(n, n)
+    ctx.generate_terrain([7])
+    h0 = ctx.download()
+    ctx.step(1)
+    h1 = ctx.download()
+    g = ctx.download_graph()
+    N = n * n
+    rec, order, levels, A = g["rec"], g["order"], g["levels"], g["A"]
+    # order is a permutation of all cells
+    seen = np.zeros(N, np.uint8)
+    seen[order] = 1
+    assert seen.all()
+    # level-0 is exactly the NoFlow cells, ascending (traversal.cpp:27-29)
+    l0 = order[: levels[1]]
+    assert np.array_equal(l0, np.nonzero(rec == NOFLOW)[0].astype(np.uint32))
+    # every cell sits one level below its receiver
+    lvl = np.empty(N, np.int32)
+    for l in range(g["nlevels"]):
+        lvl[order[levels[l]:levels[l + 1]]] = l
+    has = rec != NOFLOW
+    assert (lvl[has] == lvl[rec[has]] + 1).all()
+    # exact mass conservation (acceptance.cpp:113-129)
+    assert A[~has].sum() == float(N)
+    # perimeter fixed, interior never below its receiver
+    hh0, hh1 = h0.reshape(n, n), h1.reshape(n, n)
+    assert np.array_equal(hh0[0], hh1[0]) and np.array_equal(hh0[:, 0], hh1[:, 0])
+    flat = h1.ravel()
+    assert (flat[has] >= flat[rec[has]]).all()
+
+
+def test_10000_step_vs_reference_cpu():
+    """One full 10000^2 step against the unmodified reference on this host."""
+    if not RefLib.available():
+        pytest.skip("oracle/_ref/liblemref.so not present")
+    ref = RefLib.get()
+    n = 10000
+    e = ref.terrain(n, n, 42)
+    ctx = device_ctx(n, n)
+    ctx.upload(e)
+    d = ctx.step(1)[0]
+    hg = ctx.download()
+    rc, newton, _ = ref.run(e, 1, strategy="rb_private_queues", workers=ref.max_threads())
+    assert rc == 0
+    assert np.array_equal(hg.view(np.uint64), e.view(np.uint64))
+    assert d.newton_iters == newton
+
+
+def test_ensemble_members_match_independent_runs(oracle):
+    w, h, M = 67, 45, 5
+    members = [(1e-6 * (1 + i % 8), 0.35 + 0.05 * i) for i in range(M)]
+    seeds = [1000 + i for i in range(M)]
+    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M, per_member=members)
+    ctx.generate_terrain(seeds)
+    refs = [oracle.terrain(w, h, s) for s in seeds]
+    for step in range(6):
+        ds = ctx.step(1)
+        tot = 0
+        for i in range(M):
+            o = oracle.step(refs[i], params=make_params(K=members[i][0], m_exp=members[i][1]))
+            tot += o["newton_iters"]
+        hg = ctx.download()
+        for i in range(M):
+            assert np.array_equal(hg[i].view(np.uint64), refs[i].view(np.uint64)), (step, i)
+        assert ds[0].newton_iters == tot
+
+
+def test_member_stats():
+    import torch
+
+    w, h, M = 200, 150, 3
+    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M)
+    ctx.generate_terrain([1, 2, 3])
+    ctx.step(3)
+    out = torch.empty(4 * M, dtype=torch.float64, device="cuda")
+    ctx.member_stats_device(out.data_ptr())
+    torch.cuda.synchronize()
+    hh = ctx.download().reshape(M, -1)
+    s = out.cpu().numpy().reshape(M, 4)
+    assert np.allclose(s[:, 0], hh.mean(1), rtol=1e-12)
+    assert (s[:, 1] == hh.max(1)).all() and (s[:, 2] == hh.min(1)).all()
+
+
+def test_n2_tolerance_and_drift(oracle):
+    w = h = 200
+    p = make_params(n_exp=2.0)
+    ctx = device_ctx(w, h, n_exp=2.0)
+    e = oracle.terrain(w, h, 42)
+    ctx.upload(e)
+    d = ctx.step(1)[0]
+    o = oracle.step(e, params=p)
+    hg = ctx.download()
+    compare_step(ctx, o, hg, e, exact_h=False, tag="n=2 step 1")
+    assert abs(d.newton_iters - o["newton_iters"]) <= max(10, o["newton_iters"] // 10000)
+    ctx.step(119)
+    oracle.run(e, 119, params=p)
+    rel = np.abs(ctx.download() - e) / np.abs(e)
+    assert rel.max() <= 1e-6  # reported drift after 120 steps; per-step bound is 1e-9
+
+
+def test_convergence_error_surfaces_cell():
+    ctx = device_ctx(40, 40, max_newton_iters=1)
+    ctx.generate_terrain([5])
+    with pytest.raises(lem.ConvergenceError) as ei:
+        ctx.step(1)
+    c = ei.value.cell()
+    assert 0 < c < 1600 and "did not converge" in str(ei.value)
+    # the context stays usable after the error is reported
+    ctx2 = device_ctx(40, 40)
+    ctx2.generate_terrain([5])
+    ctx2.step(2)
+
+
+def test_nonfinite_input_rejected():
+    ctx = device_ctx(16, 16)
+    e = np.zeros((16, 16))
+    e[3, 4] = np.nan
+    with pytest.raises(lem.ConfigError, match="non-finite value at cell 52"):
+        ctx.upload(e)
+
+
+def test_strategy_step_and_run_simulation_dropin(oracle):
+    w, h = 48, 40
+    e = oracle.terrain(w, h, 11)
+    g = lem.GridGraph(w, h)
+    ws = lem.SimWorkspace()
+    mine = e.copy()
+    for _ in range(4):
+        d = lem.strategy_step(mine, g, lem.SimParams(), lem.StepSetup(), lem.Strategy(), ws)
+        o = oracle.step(e)
+        assert np.array_equal(mine.view(np.uint64), e.view(np.uint64))
+        assert d.newton_iters == o["newton_iters"]
+    cfg = lem.RunConfig(width=w, height=h, seed=11, timesteps=10)
+    res = lem.run_simulation(cfg)
+    e2 = oracle.terrain(w, h, 11)
+    rc, newton, _ = oracle.run(e2, 10)
+    assert np.array_equal(res.elevation.view(np.uint64), e2.view(np.uint64))
+    assert res.newton_iters == newton
+    seen = []
+    lem.run_simulation(oracle.terrain(w, h, 11), cfg, on_step=lambda s, r, d: seen.append((s, float(r.sum()))))
+    assert [s for s, _ in seen] == list(range(1, 11))

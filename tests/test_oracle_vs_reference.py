@@ -1,0 +1,79 @@
+"""Pins the C oracle against outputs of the REAL reference: the committed
+golden fixtures (tests/golden/, made by tests/golden/make_golden.py from
+oracle/_ref/liblemref.so) and, when the reference library is present, live
+side-by-side runs on random inputs."""
+import json
+
+import numpy as np
+import pytest
+
+from _oracle import RefLib, fnv1a64, make_params
+
+ARRAYS = ("rec", "dnum", "donor", "order", "levels", "A")
+
+
+def _small_cases(golden_dir):
+    return sorted(golden_dir.glob("small_*.npz"))
+
+
+def test_small_golden_fixtures(oracle, golden_dir):
+    cases = _small_cases(golden_dir)
+    assert len(cases) >= 8
+    for path in cases:
+        g = np.load(path)
+        kw = json.loads(str(g["params"]))
+        e = g["h0"].copy()
+        s = oracle.step(e, conn=int(g["conn"]), params=make_params(**kw))
+        assert s["status"] == 0, path.name
+        for k in ARRAYS:
+            assert np.array_equal(s[k], g[k]), (path.name, k)
+        assert np.array_equal(e.view(np.uint64), g["h1"].view(np.uint64)), path.name
+        assert s["newton_iters"] == int(g["newton_iters"]) and s["interior_noflow"] == int(g["interior_noflow"])
+
+
+def test_anchor_1000_step1(oracle, golden_dir):
+    a = json.loads((golden_dir / "anchors.json").read_text())["1000"]
+    e = oracle.terrain(1000, 1000, 42)
+    assert fnv1a64(e) == a["terrain"]
+    s = oracle.step(e)
+    st = a["step1"]
+    assert fnv1a64(s["rec"]) == st["rec"]
+    assert fnv1a64(s["dnum"]) == st["dnum"]
+    assert fnv1a64(s["order"]) == st["order"]
+    assert fnv1a64(s["A"]) == st["A"]
+    assert fnv1a64(e) == st["h"]
+    assert s["levels"].tolist() == st["levels"]
+    assert s["interior_noflow"] == st["interior_noflow"] and s["newton_iters"] == st["newton_iters"]
+
+
+@pytest.mark.slow
+def test_anchor_1000_step120(oracle, golden_dir):
+    a = json.loads((golden_dir / "anchors.json").read_text())["1000"]["step120"]
+    e = oracle.terrain(1000, 1000, 42)
+    rc, newton, _ = oracle.run(e, 120)
+    assert rc == 0
+    assert fnv1a64(e) == a["h"] and newton == a["newton_total"]
+
+
+@pytest.mark.skipif(not RefLib.available(), reason="oracle/_ref not built (no /root/reference here)")
+@pytest.mark.parametrize("w,h,seed,conn,kw", [
+    (23, 19, 101, 8, {}),
+    (31, 7, 102, 4, {}),
+    (40, 33, 103, 8, {"dx": 0.25, "dy": 3.0, "m_exp": 0.7}),
+    (26, 26, 104, 8, {"n_exp": 1.5}),
+    (26, 26, 105, 8, {"n_exp": 0.7, "K": 1e-4}),
+])
+def test_live_vs_reference(oracle, w, h, seed, conn, kw):
+    ref = RefLib.get()
+    p = make_params(**kw)
+    e_o = oracle.terrain(w, h, seed)
+    e_r = ref.terrain(w, h, seed)
+    assert np.array_equal(e_o, e_r)
+    for _ in range(5):
+        so = oracle.step(e_o, conn=conn, params=p)
+        sr = ref.step(e_r, conn=conn, params=p)
+        assert so["status"] == sr["status"] == 0
+        for k in ARRAYS:
+            assert np.array_equal(so[k], sr[k]), k
+        assert np.array_equal(e_o.view(np.uint64), e_r.view(np.uint64))
+        assert so["newton_iters"] == sr["newton_iters"]
