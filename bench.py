@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 D8 landscape-evolution step (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+                    [--workload dem10000|ens64|dem1000|dem4000n2]
+
+A "step" is one timestep (receivers, donors, level order, accumulation,
+uplift + erosion) over the whole workload.  Default workload (N=1): the
+10000x10000 random-noise DEM of BASELINE.json configs[1].  For N>1 every rank
+advances its own 10000^2 realisation ("replicas only": one DEM does not
+shard) and the per-step ensemble statistics are all-reduced over
+NCCL -- weak scaling.  ``--workload ens64`` is configs[4]: 64 x 2000^2
+members sharded over the ranks (strong scaling).
+
+Rank 0 prints one JSON line.  ``value`` is device-resident throughput
+(inputs in HBM), ``e2e`` is the same metric through the C-ABI's
+strategy_step entry (lemgpu_step_host) with pinned host buffers copied in and
+out every step.  ``--impl reference`` times the unmodified reference CPU
+implementation (oracle/_ref/liblemref.so) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "cell-steps/s, 10000² DEM, 1 GPU; ensemble cell-steps/s at 1/2/4/8 B200"
+UNIT = "cell-steps/s"
+PAPER_P100 = 1e8 * 120 / 70.0  # RB+GPU 10000^2 x 120 steps in 70 s on one P100
+# Algorithmic bytes per cell-step: receivers 12 + donors 5 | order 9 + accum 21 + uplift/erosion 40
+B_RECV_DONOR = 17
+B_FLOW = 70
+B_STEP = 87
+WORKLOADS = {
+    "dem10000": dict(w=10000, h=10000, members=1, n_exp=1.0,
+                     desc="10000x10000 random-noise DEM, D8, m=0.5 n=1, fixed-perimeter base level, seed 42 (configs[1])"),
+    "dem1000": dict(w=1000, h=1000, members=1, n_exp=1.0, desc="1000x1000 random-noise DEM, D8, n=1 (configs[0]; L2-resident)"),
+    "dem4000n2": dict(w=4000, h=4000, members=1, n_exp=2.0, desc="4000x4000 random-noise DEM, D8, n=2 Newton (configs[2])"),
+    "ens64": dict(w=2000, h=2000, members=64, n_exp=1.0,
+                  desc="ensemble of 64 x 2000^2 DEMs, seeds 1000+i, K_i=1e-6(1+i%8), m_i=0.35+0.05*floor(i/8) (configs[4])"),
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            j = json.loads(p.read_text())
+            return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, device_index: int, period=0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.N = None
+            self.err = str(e)
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.N.nvmlDeviceGetClockInfo(self.h, self.N.NVML_CLOCK_SM))
+                r = self.N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.N is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.N is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def member_table(workload, rank, world):
+    """Member ids / seeds / (K, m) owned by this rank."""
+    wl = WORKLOADS[workload]
+    if wl["members"] == 1:
+        # replicas only: one realisation per rank
+        return [rank], [42 + rank], [(2e-6, 0.5)]
+    M = wl["members"]
+    ids = [i for i in range(M) if i * world // M == rank] if M >= world else [rank % M]
+    seeds = [1000 + i for i in ids]
+    km = [(1e-6 * (1 + i % 8), 0.35 + 0.05 * (i // 8)) for i in ids]
+    return ids, seeds, km
+
+
+def traffic_from_profiles(workload):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    for p in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
+        try:
+            j = json.loads(p.read_text())
+        except Exception:
+            continue
+        if j.get("workload") == workload:
+            return j.get("kernels", {}), p.name
+    return {}, None
+
+
+def cpu_baseline_reference(workload, budget_s=30.0):
+    """The unmodified reference on this host's cores: lem::strategy_step with
+    rb_private_queues (its fastest strategy), all OpenMP threads, a bounded
+    number of steps of the same workload."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from _oracle import RefLib, make_params  # test-infrastructure checker
+
+    wl = WORKLOADS[workload]
+    w, h = wl["w"], wl["h"]
+    if not RefLib.available():
+        return None
+    ref = RefLib.get()
+    threads = ref.max_threads()
+    p = make_params(n_exp=wl["n_exp"])
+    # bounded sample: ~budget_s of CPU work, at least 2 timed steps after 1 warm-up
+    est = 3e-8 * w * h * 16 / max(threads, 1)  # ~3 s per 10000^2 step on 16 cores
+    n = int(max(2, min(10, budget_s // max(est, 1e-3))))
+    samples, _ = ref.bench(w, h, n, warmup=1, strategy="rb_private_queues", workers=threads, params=p)
+    per_step = float(np.median(samples))
+    cells = w * h
+    return {"value": cells / per_step, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{len(samples)} lem::strategy_step(rb_private_queues, {threads} threads) timesteps of the "
+                      f"{w}x{h} seed-42 DEM, median wall time {per_step:.3f} s/step (oracle/_ref, -O2 -ffp-contract=off)"}
+
+
+def run_reference_arm(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    sys.path.insert(0, str(ROOT / "tests"))
+    from _oracle import RefLib, make_params
+
+    wl = WORKLOADS[args.workload]
+    w, h = wl["w"], wl["h"]
+    cfg = {"workload": wl["desc"], "grid": [w, h], "members": wl["members"], "impl": "reference CPU (rb_private_queues)"}
+    if not RefLib.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblemref.so not built"}))
+        return 0
+    ref = RefLib.get()
+    threads = ref.max_threads()
+    p = make_params(n_exp=wl["n_exp"])
+    members = wl["members"]
+    # one "step" = one timestep of the whole workload; for the ensemble, a
+    # bounded sample (one member) scaled to the member count.
+    t0 = time.time()
+    wsecs, _ = ref.bench(w, h, 1, warmup=0, strategy="rb_private_queues", workers=threads, params=p)
+    est = float(wsecs[0]) * members
+    budget = 180.0
+    k = args.steps
+    warm = max(0, min(args.warmup - 1, int((budget / 4) // max(est, 1e-3))))
+    k_run = int(max(1, min(k, (budget - (time.time() - t0)) // max(est, 1e-3) - warm)))
+    secs, _ = ref.bench(w, h, k_run, warmup=warm, strategy="rb_private_queues", workers=threads, params=p)
+    per_step = float(np.mean(secs)) * members
+    value = w * h * members / per_step
+    sample = (f"{k_run} timed + {warm + 1} warm-up lem::strategy_step(rb_private_queues, {threads} threads) on "
+              f"{w}x{h}" + (f" (one member, scaled x{members})" if members > 1 else "") +
+              (f"; steps capped from {k} to fit the time budget" if k_run < k else ""))
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": k_run, "warmup": warm + 1,
+           "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM, lem::generate_terrain)", "config": cfg,
+           "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--workload", default="dem10000", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_02977_b200 as lem
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = WORKLOADS[args.workload]
+    w, h = wl["w"], wl["h"]
+    ids, seeds, km = member_table(args.workload, rank, world)
+    M = len(ids)
+    params = lem.SimParams(n_exp=wl["n_exp"])
+    ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M,
+                            per_member=km if (wl["members"] > 1) else None)
+    ctx.generate_terrain(seeds)
+    cells = w * h * M
+    ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    ens = world > 1 or wl["members"] > 1
+    stats = torch.zeros(4 * max(M, 1), dtype=torch.float64, device=f"cuda:{local}")
+    gstats = torch.zeros(4, dtype=torch.float64, device=f"cuda:{local}")
+
+    def one_step():
+        ctx.step_async(1)
+        if ens:
+            # per-member statistics epilogue + NCCL reduction
+            ctx.member_stats_device(stats.data_ptr())
+            if world > 1:
+                with torch.cuda.stream(ext):
+                    gstats.copy_(stats.view(M, 4).sum(0))
+                    dist.all_reduce(gstats)
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        one_step()
+    ctx.sync()
+    ctx.kernel_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    try:
+        nvml_index = torch.cuda._get_nvml_device_index(local)
+    except Exception:
+        nvml_index = local
+    with ClockSampler(nvml_index) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(ext)
+        for _ in range(args.steps):
+            one_step()
+        end.record(ext)
+        diags = ctx.sync()  # raises on any failing step
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    kt = ctx.kernel_times()
+    ctx.kernel_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_cells = cells * world if wl["members"] == 1 else w * h * wl["members"]
+    value = total_cells * args.steps / (ms / 1e3)
+
+    # ---- end to end through the C-ABI strategy_step entry, pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        host = np.empty(cells, np.float64)
+        reg = lem._abi.lib().lemgpu_host_register(host.ctypes.data, host.nbytes) == 0
+        lem._abi.lib().lemgpu_download_elev(ctx.handle, host.ctypes.data)
+        ctx.step_host(host)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.step_host(host)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        if reg:
+            lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
+        e2e = {"value": total_cells * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": cells * 8,
+               "d2h_bytes_per_step": cells * 8, "steps": args.e2e_steps,
+               "path": "lemgpu_step_host (strategy_step on a host raster: H2D, step, D2H per call)",
+               "pinned": bool(reg)}
+
+    peak, peak_src = load_peaks()
+    n_l = max(kt["launches"], 1)
+    k1_ms, fl_ms = kt["recv_donor"] / n_l, kt["flow"] / n_l
+    dom = "k_flow" if fl_ms >= k1_ms else "k_recv_donor"
+    dom_ms = max(fl_ms, k1_ms)
+    dom_bytes = (B_FLOW if dom == "k_flow" else B_RECV_DONOR) * cells
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic_tbl, traffic_src = traffic_from_profiles(args.workload)
+    traffic = traffic_tbl.get(dom, {}).get("dram_bytes_per_launch") if traffic_tbl else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_cell": B_FLOW if dom == "k_flow" else B_RECV_DONOR,
+                "kernel_ms": {"k_recv_donor": k1_ms, "k_flow": fl_ms},
+                "step": {"alg_bytes_per_cell": B_STEP, "achieved": value / world * B_STEP / 1e9 if wl["members"] == 1
+                         else value / world * B_STEP / 1e9, "frac": (value / world) * B_STEP / 1e9 / peak},
+                "traffic_source": traffic_src}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_reference(args.workload)
+        except Exception as e:  # report, never fail the bench
+            cpu = {"value": None, "error": str(e)}
+    launches = 2 * args.steps + (2 * args.steps if ens else 0)
+    last = diags[-1] if diags else None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if wl["members"] == 1 else "strong",
+        "vs_baseline": value / PAPER_P100 if (args.workload == "dem10000" and world == 1) else None,
+        "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM generated on device, bit-exact lem::generate_terrain)",
+        "config": {"workload": wl["desc"] + (" -- one independent replica per GPU, per-step NCCL stats all-reduce"
+                                             if (world > 1 and wl["members"] == 1) else ""),
+                   "grid": [w, h], "members_per_gpu": M, "params": "K=2e-6 m=0.5 n=%g u=2e-3 dt=1000 eps=1e-6" % wl["n_exp"],
+                   "parallelism": f"replicas{world}" if wl["members"] == 1 else f"members/{world}",
+                   "l2": f"inputs larger than L2: {ctx.device_bytes() / 1e9:.1f} GB device state per GPU vs 126 MB L2, no flush",
+                   "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",
+                   "nlevels_last_step": last.nlevels if last else None,
+                   "phase_ms_last_step": ({k: round(v * 1e3, 4) for k, v in zip(
+                       ("receivers+donors", "donors", "order", "accum", "uplift", "accum+uplift+erosion"), last.seconds)}
+                       if last else None),
+                   "newton_iters_last_step": last.newton_iters if last else None},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -179,6 +179,10 @@ int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
 int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable);
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
 
+/* Debug: globaltimer stamps (ns) taken by k_flow at each grid barrier of the
+ * last step (start, level 0, each expansion level, order done, sweeps done). */
+int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t* count);
+
 /* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */
 int lemgpu_host_register(void* ptr, size_t bytes);
 int lemgpu_host_unregister(void* ptr);

@@ -11,6 +11,7 @@
 // Nothing here is part of the product path.
 #include <cstdint>
 #include <cstring>
+#include <chrono>
 #include <exception>
 #include <string>
 
@@ -149,6 +150,40 @@ int lr_run(int w, int h, int connectivity, const LrParams* p, const char* strate
         if (newton) *newton = res.newton_iters;
       },
       err_cell);
+}
+
+// Timed CPU baseline: `warmup` untimed then `steps` timed lem::strategy_step
+// calls of one strategy on a persistent workspace (the run_simulation loop
+// body, scheduler.cpp:490-498).  seconds[i] = wall time of timed step i,
+// including the per-step FlowGraph::resize the phase timers miss.
+int lr_bench(int w, int h, int connectivity, const LrParams* p, const char* strategy,
+             std::uint32_t workers, std::uint64_t seed, std::uint32_t warmup, std::uint32_t steps,
+             double* seconds, std::uint64_t* newton) {
+  return guarded(
+      [&] {
+        auto kind = lem::strategy_from_string(strategy);
+        if (!kind) throw lem::ConfigError(std::string("unknown strategy ") + strategy);
+        lem::Raster<double> r = lem::generate_terrain(w, h, seed);
+        const lem::Neighborhood nbh = lem::Neighborhood::make(connectivity, p->dx, p->dy);
+        const lem::GridGraph g(w, h, nbh);
+        const lem::SimParams sp = to_params(p);
+        lem::StepSetup setup;
+        setup.order = lem::uses_stack_order(*kind) ? lem::OrderKind::kStack : lem::OrderKind::kQueue;
+        const lem::Strategy st{*kind, workers};
+        lem::SimWorkspace ws;
+        std::uint64_t it = 0;
+        for (std::uint32_t s = 0; s < warmup + steps; ++s) {
+          const auto t0 = std::chrono::steady_clock::now();
+          lem::StepDiagnostics d = lem::strategy_step(r, g, sp, setup, st, ws);
+          const auto t1 = std::chrono::steady_clock::now();
+          if (s >= warmup) {
+            seconds[s - warmup] = std::chrono::duration<double>(t1 - t0).count();
+            it += d.newton_iters;
+          }
+        }
+        if (newton) *newton = it;
+      },
+      nullptr);
 }
 
 }  // extern "C"

@@ -195,6 +195,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     a.dist[k] = offset_length(dir_ox(k), dir_oy(k), p->dx, p->dy);
     if (a.dist[k] == 1.0) a.dist_one |= 1u << k;
   }
+  a.unit_card = (a.dist[1] == 1.0 && a.dist[3] == 1.0) ? 1 : 0;
+  a.rinv_diag = 1.0 / a.dist[0];
   a.powdist_h = std::pow(a.dist[3], p->n_exp);
   a.powdist_v = std::pow(a.dist[1], p->n_exp);
   a.powdist_d = std::pow(a.dist[0], p->n_exp);
@@ -218,7 +220,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
       (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &a.h, N)) ||
       (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
       (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) ||
-      (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
+      (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) ||
+      (rc = dmalloc(ctx, &a.cbound, ((size_t)N / kChunkRoots + 2) * kCBS)) ||
       (rc = dmalloc(ctx, &a.Aq, N)) || (rc = dmalloc(ctx, &a.hq, N)) ||
       (rc = dmalloc(ctx, &a.levels, (size_t)N + 2)) ||
       (rc = dmalloc(ctx, &a.tstat, (size_t)N / kExTile + 2)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
@@ -251,7 +254,9 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   // one persistent CTA set: every CTA must be co-resident (cooperative launch)
   int per_sm = 0;
   const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
-  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kTPB, 0));
+  for (const void* f : {(const void*)k_flow<0>, (const void*)k_flow<1>, (const void*)k_flow<2>})
+    CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmemBytes));
+  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kTPB, kFlowSmemBytes));
   if (per_sm < 1) {
     fail(ctx, LEMGPU_ECUDA, "k_flow cannot be resident");
     return bail(LEMGPU_ECUDA);
@@ -289,7 +294,7 @@ int enqueue_step(lemgpu_ctx* ctx) {
   if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
   void* args[] = {&a};
   const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
-  CU(ctx, cudaLaunchCooperativeKernel(fk, dim3(ctx->flow_grid), dim3(kTPB), args, 0, ctx->stream));
+  CU(ctx, cudaLaunchCooperativeKernel(fk, dim3(ctx->flow_grid), dim3(kTPB), args, kFlowSmemBytes, ctx->stream));
   if (ev) CU(ctx, cudaEventRecord(ev[2], ctx->stream));
   ++ctx->pending;
   ctx->have_graph = true;
@@ -319,7 +324,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
   void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, a.h,   a.rcode,  a.dmask, a.order,
-                  a.ppos,     a.fc,        a.cdir,     a.Aq,  a.hq,     a.levels, a.tstat,
+                  a.ppos,     a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.tstat,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -551,6 +556,18 @@ int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches) {
   ms[0] = ctx->kernel_ms[0];
   ms[1] = ctx->kernel_ms[1];
   if (launches) *launches = ctx->kernel_launches;
+  return LEMGPU_OK;
+}
+
+int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t* count) {
+  if (!ctx || !ns) return LEMGPU_ECONFIG;
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  Ctl c{};
+  CU(ctx, cudaMemcpy(&c, ctx->a.ctl, sizeof c, cudaMemcpyDeviceToHost));
+  const uint32_t n = c.ntl < cap ? c.ntl : cap;
+  for (uint32_t i = 0; i < n; ++i) ns[i] = c.tl[i];
+  if (count) *count = n;
   return LEMGPU_OK;
 }
 

@@ -33,8 +33,8 @@ constexpr int kBY = 32;
 // k_flow scan tiles.
 constexpr int kL0IPT = 16;                 // level-0 cells per thread (one uint4 of rcodes)
 constexpr int kL0Tile = kTPB * kL0IPT;     // 4096 cells
-constexpr int kExIPT = 4;                  // frontier items per thread
-constexpr int kExTile = kTPB * kExIPT;     // 1024 frontier cells
+constexpr int kExIPT = 8;                  // frontier items per thread
+constexpr int kExTile = kTPB * kExIPT;     // 2048 frontier cells
 
 // Frozen D8 stencil (src/neighborhood.cpp:12): k -> (ox, oy).  The
 // opposite direction of k is 7-k.  D4 is the cardinal subsequence
@@ -54,7 +54,13 @@ struct Ctl {
   uint32_t level_total[2];  // children produced by the level just expanded
   uint32_t pad;
   unsigned long long t_k1_begin, t_k1_end;  // globaltimer span of k_recv_donor
+  uint32_t ntl, pad2;
+  unsigned long long tl[96];  // debug timeline of the last k_flow (globaltimer at each barrier)
 };
+#define LG_TL(lead, ctl)                                             \
+  do {                                                               \
+    if ((lead) && (ctl)->ntl < 96) (ctl)->tl[(ctl)->ntl++] = globaltimer(); \
+  } while (0)
 
 struct StepArgs {
   // geometry (stacked members: rows [m*H, (m+1)*H) belong to member m)
@@ -70,6 +76,8 @@ struct StepArgs {
   int w0_is_one;
   uint32_t lut_entries;
   uint32_t dist_one;  // bit k set when dist[k] == 1.0 (division is the identity)
+  int unit_card;      // dx == dy == 1: cardinal slopes are the drops themselves
+  double rinv_diag;   // RN(1 / dist_diag), used only to pre-decide far-from-tie comparisons
   int off[8];         // linear offset of direction k (oy*W + ox)
   double dist[8];     // offset_length of direction k (neighborhood.hpp:17-23)
   double powdist_h, powdist_v, powdist_d;  // host-libm pow(dist, n): horizontal, vertical, diagonal
@@ -84,7 +92,7 @@ struct StepArgs {
   uint32_t* order;
   uint32_t* ppos;
   uint32_t* fc;
-  uint8_t* cdir;
+  uint32_t* cbound;   // per source chunk: first position at each level
   double* Aq;
   double* hq;
   uint32_t* levels;
@@ -94,6 +102,18 @@ struct StepArgs {
 };
 
 // ---------------------------------------------------------------- helpers
+
+// IEEE round-to-nearest arithmetic usable on host and device (the host side
+// is compiled with -ffp-contract=off, so plain operators do not fuse).
+#ifdef __CUDA_ARCH__
+#define LG_SUB(x, y) __dsub_rn((x), (y))
+#define LG_MUL(x, y) __dmul_rn((x), (y))
+#define LG_DIV(x, y) __ddiv_rn((x), (y))
+#else
+#define LG_SUB(x, y) ((x) - (y))
+#define LG_MUL(x, y) ((x) * (y))
+#define LG_DIV(x, y) ((x) / (y))
+#endif
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -184,64 +204,146 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* tstat, uint32_t
 
 // ------------------------------------------------------- receivers/donors
 
+// Stencil slots are addressed relative to the centre (1,1) of a 3x3 window.
+// steepest_receiver (flow_graph.hpp:44-59): s_k = (ec - en_k) / dist_k, strict
+// '>' against s_max = 0, so the FIRST maximum in stencil order wins.
+//
+// Fast path for unit cardinal spacing (dx == dy == 1, the reference default):
+// cardinal slopes are the drops themselves (x / 1.0 is exact) and the only
+// rounding-sensitive quantity is the diagonal quotient RN(d / sqrt2).  RN is
+// monotone, so the best diagonal is the one with the largest drop dd and the
+// class comparison RN(dd/c) vs dc is decided by one multiplication by RN(1/c)
+// unless the two are within 2^-40 relative (then the true IEEE division is
+// taken).  Diagonal ties are resolved exactly: only drops within 2^-50 of dd
+// can round to the same quotient, and those are divided for real.  The
+// result is the reference's argmax bit for bit, with ~0 divisions per cell.
+// The reference loop itself (with the exact skips: ec - en <= 0 can never
+// beat s_max >= 0, and x / 1.0 == x).  Used directly for general spacing /
+// D4, and as the exact slow path of the D8 fast path below.
+template <int CONN>
+__host__ __device__ __forceinline__ uint8_t receiver_code_ref(const double (&d)[8], const StepArgs& a) {
+  double smax = 0.0;
+  uint8_t code = kNoFlowCode;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (!dir_in(CONN, k)) continue;
+    if (d[k] > 0.0) {
+      const double s = ((a.dist_one >> k) & 1u) ? d[k] : LG_DIV(d[k], a.dist[k]);
+      if (s > smax) {
+        smax = s;
+        code = (uint8_t)k;
+      }
+    }
+  }
+  return code;
+}
+
+template <int CONN>
+__host__ __device__ __forceinline__ uint8_t receiver_code(const double (&d)[8], const StepArgs& a) {
+  if (CONN == 8 && a.unit_card) {
+    const double dc = fmax(fmax(d[1], d[3]), fmax(d[4], d[6]));
+    const double dd = fmax(fmax(d[0], d[2]), fmax(d[5], d[7]));
+    const bool cpos = dc > 0.0, dpos = dd > 0.0;
+    if (!cpos && !dpos) return kNoFlowCode;
+    bool card_ok = cpos, diag_ok = dpos;
+    if (cpos && dpos) {
+      // RN(dd / c) vs dc, decided by RN(dd * RN(1/c)) unless within 2^-40
+      const double approx = LG_MUL(dd, a.rinv_diag);
+      if (dd < 0x1p-1000 || dc < 0x1p-1000 || fabs(LG_SUB(approx, dc)) <= LG_MUL(dc, 0x1p-40))
+        return receiver_code_ref<CONN>(d, a);
+      diag_ok = approx > dc;
+      card_ok = !diag_ok;
+    }
+    uint32_t mask = 0;
+    if (card_ok) {
+      mask = (d[1] == dc ? 0x02u : 0u) | (d[3] == dc ? 0x08u : 0u) | (d[4] == dc ? 0x10u : 0u) |
+             (d[6] == dc ? 0x40u : 0u);
+    } else {
+      // a second diagonal within 2^-50 of dd may round to the same quotient
+      const double near = LG_MUL(dd, 1.0 - 0x1p-50);
+      const bool amb = (d[0] > near && d[0] != dd) || (d[2] > near && d[2] != dd) ||
+                       (d[5] > near && d[5] != dd) || (d[7] > near && d[7] != dd);
+      if (amb) return receiver_code_ref<CONN>(d, a);
+      mask = (d[0] == dd ? 0x01u : 0u) | (d[2] == dd ? 0x04u : 0u) | (d[5] == dd ? 0x20u : 0u) |
+             (d[7] == dd ? 0x80u : 0u);
+    }
+#ifdef __CUDA_ARCH__
+    return (uint8_t)(__ffs(mask) - 1);
+#else
+    return (uint8_t)__builtin_ctz(mask);
+#endif
+  }
+  return receiver_code_ref<CONN>(d, a);
+}
+
 // One CTA: a kBY x kBX tile of cells.  h is staged with a 2-cell halo, the
 // receiver code with a 1-cell halo, so the donor mask of every tile cell is
 // computed from receivers evaluated in the same CTA -- one HBM read of h,
 // one byte written per output array, no atomics (pull-based donors).
+// Warp-per-row loops keep all row arithmetic warp-uniform.
 template <int CONN>
 __global__ void __launch_bounds__(kTPB) k_recv_donor(StepArgs a) {
   __shared__ double sh[kBY + 4][kBX + 4];
-  __shared__ uint8_t rc[kBY + 2][kBX + 2 + 2];
+  __shared__ uint8_t rc[kBY + 2][kBX + 4];
   if (ld_volatile_u32(&a.ctl->err_flag)) return;
   if (threadIdx.x == 0) atomicMin(&a.ctl->t_k1_begin, globaltimer());
-  const long long x0 = (long long)blockIdx.x * kBX, y0 = (long long)blockIdx.y * kBY;
-  const long long W = a.W, Ht = a.Htot;
-
-  for (int i = threadIdx.x; i < (kBY + 4) * (kBX + 4); i += kTPB) {
-    const int r = i / (kBX + 4), cc = i - r * (kBX + 4);
-    const long long gy = y0 - 2 + r, gx = x0 - 2 + cc;
-    double v = 0.0;
-    if (gy >= 0 && gy < Ht && gx >= 0 && gx < W) v = __ldg(a.h + gy * W + gx);
-    sh[r][cc] = v;
-  }
-  __syncthreads();
-
-  // steepest_receiver (flow_graph.hpp:44-59): s = (ec - en) / dist, strict
-  // '>' against s_max starting at 0, first maximum in stencil order wins.
-  // Neighbours with ec - en <= 0 give s <= 0 and can never win, so their
-  // division is skipped; division by a unit distance is the identity.
-  for (int i = threadIdx.x; i < (kBY + 2) * (kBX + 2); i += kTPB) {
-    const int r = i / (kBX + 2), cc = i - r * (kBX + 2);
-    const long long gy = y0 - 1 + r, gx = x0 - 1 + cc;
-    uint8_t code = kNoFlowCode;
-    if (gy >= 0 && gy < Ht && gx > 0 && gx < W - 1) {
-      const uint32_t yl = (uint32_t)(gy % a.H);
-      if (yl > 0 && yl < a.H - 1) {
-        const double ec = sh[r + 1][cc + 1];
-        double smax = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (!dir_in(CONN, k)) continue;
-          const double d = __dsub_rn(ec, sh[r + 1 + dir_oy(k)][cc + 1 + dir_ox(k)]);
-          if (d > 0.0) {
-            const double s = ((a.dist_one >> k) & 1u) ? d : __ddiv_rn(d, a.dist[k]);
-            if (s > smax) {
-              smax = s;
-              code = (uint8_t)k;
-            }
-          }
-        }
-      }
-    }
-    rc[r][cc] = code;
-  }
-  __syncthreads();
-
-  // donors_of (flow_graph.hpp:64-72): neighbour n in direction k donates to
-  // c iff rec[n] == c, i.e. n's code is the opposite direction 7-k.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+  const uint32_t W = a.W, Ht = a.Htot;
+
+  // ---- stage h: rows y0-2 .. y0+kBY+1, columns x0-2 .. x0+kBX+1
+  for (int r = warp; r < kBY + 4; r += kNW) {
+    const int gy = (int)y0 - 2 + r;
+    const bool rowok = gy >= 0 && (uint32_t)gy < Ht;
+    const double* row = a.h + (size_t)(rowok ? gy : 0) * W;
+#pragma unroll
+    for (int j = 0; j < kBX / 32; ++j) {
+      const uint32_t gx = x0 + lane + 32 * j;
+      sh[r][2 + lane + 32 * j] = (rowok && gx < W) ? __ldg(row + gx) : 0.0;
+    }
+    if (lane < 4) {
+      const int cc = lane < 2 ? lane : kBX + lane;  // 0,1 | kBX+2,kBX+3
+      const int gx = (int)x0 - 2 + cc;
+      sh[r][cc] = (rowok && gx >= 0 && (uint32_t)gx < W) ? __ldg(row + gx) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  // ---- receiver codes: rows y0-1 .. y0+kBY, columns x0-1 .. x0+kBX
+  for (int r = warp; r < kBY + 2; r += kNW) {
+    const int gy = (int)y0 - 1 + r;
+    bool rowint = false;
+    if (gy >= 0 && (uint32_t)gy < Ht) {
+      const uint32_t yl = (uint32_t)gy % a.H;
+      rowint = yl > 0 && yl < a.H - 1;
+    }
+    for (int j = 0; j <= kBX / 32; ++j) {
+      int cc;  // column within rc (rc column c <-> sh column c+1 <-> gx = x0-1+c)
+      if (j < kBX / 32) {
+        cc = 1 + lane + 32 * j;
+      } else {
+        if (lane >= 2) break;
+        cc = lane == 0 ? 0 : kBX + 1;
+      }
+      const int gx = (int)x0 - 1 + cc;
+      uint8_t code = kNoFlowCode;
+      if (rowint && gx > 0 && gx < (int)W - 1) {
+        const double ec = sh[r + 1][cc + 1];
+        double d[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          d[k] = dir_in(CONN, k) ? __dsub_rn(ec, sh[r + 1 + dir_oy(k)][cc + 1 + dir_ox(k)]) : 0.0;
+        code = receiver_code<CONN>(d, a);
+      }
+      rc[r][cc] = code;
+    }
+  }
+  __syncthreads();
+
+  // ---- donors_of (flow_graph.hpp:64-72): neighbour n in direction k donates
+  // to c iff rec[n] == c, i.e. n's code is the opposite direction 7-k.
   for (int r = warp; r < kBY; r += kNW) {
-    const long long gy = y0 + r;
+    const uint32_t gy = y0 + r;
     if (gy >= Ht) break;
     const int cc0 = lane * 4;
     uint32_t pc = 0, pm = 0;
@@ -257,8 +359,8 @@ __global__ void __launch_bounds__(kTPB) k_recv_donor(StepArgs a) {
       pm |= m << (8 * j);
       pc |= (uint32_t)rc[r + 1][cc + 1] << (8 * j);
     }
-    const long long gx = x0 + cc0;
-    const long long base = gy * W + gx;
+    const uint32_t gx = x0 + cc0;
+    const size_t base = (size_t)gy * W + gx;
     if (gx + 3 < W && (W & 3) == 0) {
       *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
       *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
@@ -275,17 +377,62 @@ __global__ void __launch_bounds__(kTPB) k_recv_donor(StepArgs a) {
 }
 
 // ------------------------------------------------------------ flow kernel
+//
+// Phase A (order): level 0 by a single-pass compaction of rcode == kNoFlow,
+// then one frontier expansion per level -- decoupled look-back scan of
+// popcount(dmask) -> first-child positions fc[] and the children themselves.
+// One grid barrier per level (the only inherently level-synchronous part).
+//
+// Phase B (accumulation + uplift + erosion) exploits the single-receiver
+// structure the way the paper's RB+PQ strategy does (scheduler.cpp:269-392):
+// the sources (level 0) are cut into chunks of kChunkRoots consecutive
+// sources; a chunk's upstream forest occupies ONE contiguous position range
+// per level (children of consecutive parents are consecutive), so its
+// per-level ranges follow from fc[] alone and chunks are fully independent.
+// Each CTA takes whole chunks: the forest is staged in shared memory,
+// accumulated deepest-level-first and eroded downstream->upstream with CTA
+// barriers only -- no grid barrier, and every cell's h is read and written
+// once, with the spatial locality of the source order.  Chunks too large for
+// shared memory run the same sweeps on position-major global scratch, and
+// plans deeper than kChunkMaxLevels use grid-wide level sweeps instead.
+// All three schedules evaluate the identical per-cell arithmetic in a
+// dependency-respecting order, so h is bit-identical among them.
 
-struct FlowSmem {
+constexpr int kChunkRoots = 128;
+constexpr int kChunkCap = 2048;
+constexpr int kChunkMaxLevels = 32;
+constexpr int kCBS = kChunkMaxLevels + 1;  // chunk-boundary entries per chunk
+
+struct ExpandSmem {
   uint32_t scan[kNW + 1];
   uint32_t bcast;
   uint32_t ord[kExTile];
+};
+
+struct ChunkSmem {
+  double h[kChunkCap];
+  double A[kChunkCap];
+  uint32_t c[kChunkCap];
+  uint16_t cs[kChunkCap];
+  uint16_t par[kChunkCap];
+  uint8_t cn[kChunkCap];
+  uint32_t lo[kCBS + 1];
+  uint32_t base[kCBS + 1];
+  uint32_t nl, total;
+};
+
+struct FlowSmem {
+  union {
+    ExpandSmem ex;
+    ChunkSmem ch;
+  };
   unsigned long long red[kNW];
   uint32_t red32[kNW];
 };
+constexpr size_t kFlowSmemBytes = sizeof(FlowSmem);
 
 // Level 0 (traversal.cpp:27-29): every cell with rec == kNoFlow, ascending.
-__device__ __forceinline__ void tile_level0(const StepArgs& a, FlowSmem& sm, uint32_t t,
+__device__ __forceinline__ void tile_level0(const StepArgs& a, ExpandSmem& sm, uint32_t t,
                                             uint32_t ntiles, uint32_t epoch) {
   const uint32_t cell0 = t * (uint32_t)kL0Tile + threadIdx.x * kL0IPT;
   uint32_t w[4] = {0, 0, 0, 0};
@@ -330,10 +477,9 @@ __device__ __forceinline__ void tile_level0(const StepArgs& a, FlowSmem& sm, uin
 
 // Expand frontier [lo, hi) into the next level (traversal.cpp:35-44): for
 // each frontier cell in order, its donors in stencil (= bit) order.  The
-// exclusive scan of popcount(dmask) over the frontier is the first-child
-// position fc[pos]; children also record their parent position (ppos) and
-// the direction parent->child (cdir) for the erosion sweep.
-__device__ __forceinline__ void tile_expand(const StepArgs& a, FlowSmem& sm, uint32_t t,
+// exclusive scan of popcount(dmask) over the frontier gives the first-child
+// position fc[pos].
+__device__ __forceinline__ void tile_expand(const StepArgs& a, ExpandSmem& sm, uint32_t t,
                                             uint32_t ntiles, uint32_t lo, uint32_t hi,
                                             uint32_t epoch, int par) {
   const uint32_t tb = lo + t * (uint32_t)kExTile;
@@ -359,6 +505,7 @@ __device__ __forceinline__ void tile_expand(const StepArgs& a, FlowSmem& sm, uin
   __syncthreads();
   const uint32_t pre = sm.bcast;
   uint32_t out = hi + pre + excl;
+  const long long W = a.W;
 #pragma unroll
   for (int j = 0; j < kExIPT; ++j) {
     const uint32_t pos = tb + threadIdx.x * kExIPT + j;
@@ -368,10 +515,7 @@ __device__ __forceinline__ void tile_expand(const StepArgs& a, FlowSmem& sm, uin
       while (mm) {
         const int k = __ffs(mm) - 1;
         mm &= mm - 1;
-        a.order[out] = (uint32_t)((long long)c[j] + dir_ox(k) + (long long)dir_oy(k) * a.W);
-        a.ppos[out] = pos;
-        a.cdir[out] = (uint8_t)k;
-        ++out;
+        a.order[out++] = (uint32_t)((long long)c[j] + dir_ox(k) + dir_oy(k) * W);
       }
     }
   }
@@ -441,17 +585,20 @@ __device__ __forceinline__ double newton_gen(double h0, double hn, double F, dou
   return h;
 }
 
+__device__ __forceinline__ bool is_interior(const StepArgs& a, uint32_t c) {
+  const uint32_t y = c / a.W, x = c - y * a.W, yl = y % a.H;
+  return x > 0 && x < a.W - 1 && yl > 0 && yl < a.H - 1;
+}
+
+// erode_one_cell (erosion.cpp:36-50) for cell c with receiver rc: uplifted
+// start h0, already-updated receiver elevation hn, drainage area A.
 template <int NK>
-__device__ __forceinline__ void erode_pos(const StepArgs& a, uint32_t pos, unsigned long long& iters,
-                                          uint32_t& misses) {
-  const uint32_t c = a.order[pos];
-  const uint32_t p = a.ppos[pos];
-  const int k = a.cdir[pos];           // parent -> child; child -> receiver is 7-k
-  const double A = a.Aq[pos];
-  const double hn = a.hq[p];           // receiver, already updated this step
-  const double h0 = __dadd_rn(a.h[c], a.du);  // uplift (erosion.cpp:52-57), one rounding
+__device__ __forceinline__ double erode_cell(const StepArgs& a, uint32_t c, uint32_t rc, double h0,
+                                             double hn, double A, unsigned long long& iters,
+                                             uint32_t& misses, bool& ok) {
   const uint32_t mem = a.M > 1 ? c / a.MN : 0u;
-  // F = K*dt*pow(A,m)/pow(dist,n) (erosion.cpp:38-39): (K*dt) first.
+  // F = K*dt*pow(A,m)/pow(dist,n) (erosion.cpp:38-39): (K*dt) first; pow(A,m)
+  // from the host-libm table when A is an exact multiple of the cell area.
   double powA;
   const double q = a.w0_is_one ? A : __ddiv_rn(A, a.w0);
   if (a.lut_exact && q < (double)a.lut_entries && q == floor(q)) {
@@ -460,30 +607,181 @@ __device__ __forceinline__ void erode_pos(const StepArgs& a, uint32_t pos, unsig
     powA = pow(A, __ldg(a.mexp + mem));
     ++misses;
   }
-  // pow(dist(c, rec[c]), n): opposite directions share a distance class.
-  const double pd = (k == 1 || k == 6) ? a.powdist_v : (k == 3 || k == 4) ? a.powdist_h : a.powdist_d;
+  // pow(dist(c, rec[c]), n) by offset class (grid_graph.hpp:53-57)
+  const int off = (int)(c - rc);
+  const double pd = (off == 1 || off == -1) ? a.powdist_h
+                    : (off == (int)a.W || off == -(int)a.W) ? a.powdist_v : a.powdist_d;
   const double F = __ddiv_rn(__dmul_rn(__ldg(a.kdt + mem), powA), pd);
   int it;
-  bool ok;
   double hnew;
   if (NK == 1)
     hnew = newton_n1(h0, hn, F, a.eps, a.maxit, it, ok);
   else
     hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, it, ok);
   if (ok) {
-    a.h[c] = hnew;
-    a.hq[pos] = hnew;
     iters += (unsigned long long)it;
   } else {
     atomicMin(&a.ctl->err_cell, c);
     atomicMax(&a.ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
   }
+  return hnew;
+}
+
+// One chunk in shared memory.  Local index i enumerates the chunk's forest
+// level by level (base[l] .. base[l+1]); parents/children are local indices.
+template <int NK>
+__device__ __forceinline__ void chunk_smem(const StepArgs& a, ChunkSmem& s, unsigned long long& iters,
+                                           uint32_t& misses) {
+  const uint32_t T = s.total, nl = s.nl, tid = threadIdx.x;
+  // load, stage 1: cell and child range of every position (independent
+  // loads, 4 in flight per thread)
+  {
+    uint32_t l = 0;
+    for (uint32_t i0 = tid; i0 < T; i0 += 4 * kTPB) {
+      uint32_t pos[4], lv[4], c[4], f0[4], f1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * kTPB;
+        if (i < T) {
+          while (s.base[l + 1] <= i) ++l;
+          lv[u] = l;
+          pos[u] = s.lo[l] + (i - s.base[l]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u * kTPB < T) {
+          c[u] = a.order[pos[u]];
+          f0[u] = a.fc[pos[u]];
+          f1[u] = a.fc[pos[u] + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * kTPB;
+        if (i < T) {
+          s.c[i] = c[u];
+          s.cn[i] = (uint8_t)(f1[u] - f0[u]);
+          s.cs[i] = (uint16_t)(f1[u] > f0[u] ? s.base[lv[u] + 1] + (f0[u] - s.lo[lv[u] + 1]) : 0u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // load, stage 2: uplifted h (erosion.cpp:52-57: interior cells only)
+  for (uint32_t i0 = tid; i0 < T; i0 += 4 * kTPB) {
+    double hv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kTPB;
+      if (i < T) hv[u] = a.h[s.c[i]];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kTPB;
+      if (i < T) s.h[i] = (i >= s.base[1] || is_interior(a, s.c[i])) ? __dadd_rn(hv[u], a.du) : hv[u];
+    }
+  }
+  for (uint32_t i = tid; i < T; i += kTPB) {
+    const uint32_t n = s.cn[i], c0 = s.cs[i];
+    for (uint32_t j = 0; j < n; ++j) s.par[c0 + j] = (uint16_t)i;
+  }
+  // accumulation, deepest level first (accumulation.hpp:21-28: fixed slot order)
+  for (int l = (int)nl - 1; l >= 0; --l) {
+    for (uint32_t i = s.base[l] + tid; i < s.base[l + 1]; i += kTPB) {
+      double acc = a.w0;
+      const uint32_t n = s.cn[i], c0 = s.cs[i];
+      for (uint32_t j = 0; j < n; ++j) acc = __dadd_rn(acc, s.A[c0 + j]);
+      s.A[i] = acc;
+    }
+    __syncthreads();
+  }
+  // drainage area out, position-major (AccumField::values, via the order)
+  {
+    uint32_t l = 0;
+    for (uint32_t i = tid; i < T; i += kTPB) {
+      while (s.base[l + 1] <= i) ++l;
+      a.Aq[s.lo[l] + (i - s.base[l])] = s.A[i];
+    }
+  }
+  // erosion, downstream -> upstream (erosion.cpp:66-81); level 0 never eroded
+  for (uint32_t l = 1; l < nl; ++l) {
+    for (uint32_t i = s.base[l] + tid; i < s.base[l + 1]; i += kTPB) {
+      const uint32_t p = s.par[i];
+      bool ok;
+      const double hnew = erode_cell<NK>(a, s.c[i], s.c[p], s.h[i], s.h[p], s.A[i], iters, misses, ok);
+      if (ok) s.h[i] = hnew;
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = tid; i < T; i += kTPB) {
+    const uint32_t c = s.c[i];
+    if (i >= s.base[1] || is_interior(a, c)) a.h[c] = s.h[i];
+  }
+  __syncthreads();
+}
+
+// The same sweeps on position-major global scratch (hq, Aq, ppos), for a
+// chunk that does not fit in shared memory (GRID = false: CTA barriers) or
+// for the whole plan at once when it is deeper than kChunkMaxLevels (GRID =
+// true: per-level ranges are the global levels, grid barriers).
+template <int NK, bool GRID>
+__device__ void sweep_global(const StepArgs& a, cg::grid_group& grid, const uint32_t* lo,
+                             const uint32_t* hi, uint32_t nl, unsigned long long& iters,
+                             uint32_t& misses) {
+  const uint32_t start = GRID ? blockIdx.x * kTPB + threadIdx.x : threadIdx.x;
+  const uint32_t stride = GRID ? gridDim.x * kTPB : kTPB;
+  auto sync = [&]() {
+    if (GRID)
+      grid.sync();
+    else
+      __syncthreads();
+  };
+  for (uint32_t l = 0; l < nl; ++l) {
+    for (uint32_t pos = lo[l] + start; pos < hi[l]; pos += stride) {
+      const uint32_t c = a.order[pos];
+      double hv = a.h[c];
+      if (l > 0 || is_interior(a, c)) hv = __dadd_rn(hv, a.du);
+      a.hq[pos] = hv;
+      if (l + 1 < nl)
+        for (uint32_t j = a.fc[pos], j1 = a.fc[pos + 1]; j < j1; ++j) a.ppos[j] = pos;
+    }
+  }
+  sync();
+  for (int l = (int)nl - 1; l >= 0; --l) {
+    for (uint32_t pos = lo[l] + start; pos < hi[l]; pos += stride) {
+      double acc = a.w0;
+      if ((uint32_t)l + 1 < nl)
+        for (uint32_t j = a.fc[pos], j1 = a.fc[pos + 1]; j < j1; ++j) acc = __dadd_rn(acc, a.Aq[j]);
+      a.Aq[pos] = acc;
+    }
+    sync();
+  }
+  for (uint32_t l = 1; l < nl; ++l) {
+    for (uint32_t pos = lo[l] + start; pos < hi[l]; pos += stride) {
+      const uint32_t p = a.ppos[pos];
+      bool ok;
+      const double hnew =
+          erode_cell<NK>(a, a.order[pos], a.order[p], a.hq[pos], a.hq[p], a.Aq[pos], iters, misses, ok);
+      if (ok) a.hq[pos] = hnew;
+    }
+    sync();
+    if (GRID && ld_volatile_u32(&a.ctl->err_flag)) break;
+  }
+  for (uint32_t l = 0; l < nl; ++l) {
+    for (uint32_t pos = lo[l] + start; pos < hi[l]; pos += stride) {
+      const uint32_t c = a.order[pos];
+      if (l > 0 || is_interior(a, c)) a.h[c] = a.hq[pos];
+    }
+  }
+  sync();
 }
 
 template <int NK>
-__global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
+__global__ void __launch_bounds__(kTPB, 3) k_flow(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ FlowSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FlowSmem& sm = *reinterpret_cast<FlowSmem*>(smem_raw);
   const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   const bool lead = (b == 0 && tid == 0);
   Ctl* ctl = a.ctl;
@@ -495,7 +793,7 @@ __global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
   uint32_t E0 = ld_volatile_u32(&ctl->epoch);
   const unsigned long long t_begin = globaltimer();
   if ((unsigned long long)E0 + a.N + 4ull >= (1ull << 30)) {
-    // Epoch space nearly exhausted: clear all status words and restart.
+    // look-back epoch space nearly exhausted: clear all status words, restart
     const uint32_t ntst = a.N / kExTile + 2;
     for (uint32_t i = b * kTPB + tid; i < ntst; i += G * kTPB) a.tstat[i] = 0ull;
     E0 = 1;
@@ -507,22 +805,36 @@ __global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
     a.diag->status = 0;
     a.diag->err_cell = LEMGPU_NOFLOW;
     a.fc[a.N] = a.N;
+    ctl->ntl = 0;
+    ctl->tl[ctl->ntl++] = t_begin;
   }
 
-  // ---- level 0
+  // ---- Phase A: breadth-first level order
   const uint32_t nt0 = (a.N + kL0Tile - 1) / kL0Tile;
-  for (uint32_t t = b; t < nt0; t += G) tile_level0(a, sm, t, nt0, E0);
+  for (uint32_t t = b; t < nt0; t += G) tile_level0(a, sm.ex, t, nt0, E0);
   grid.sync();
+  LG_TL(lead, ctl);
 
-  // ---- breadth-first expansion, one grid barrier per level
   uint32_t lo = 0, hi = ld_volatile_u32(&ctl->level_total[0]);
+  const uint32_t n0 = hi;
+  const uint32_t nch = (n0 + kChunkRoots - 1) / kChunkRoots;
+  for (uint32_t k = b * kTPB + tid; k <= nch; k += G * kTPB) a.cbound[(size_t)k * kCBS] = min(k * kChunkRoots, n0);
   uint32_t l = 0;
   while (true) {
     const uint32_t F = hi - lo;
     const uint32_t nt = (F + kExTile - 1) / kExTile;
-    for (uint32_t t = b; t < nt; t += G) tile_expand(a, sm, t, nt, lo, hi, E0 + 1 + l, (l + 1) & 1);
+    for (uint32_t t = b; t < nt; t += G) tile_expand(a, sm.ex, t, nt, lo, hi, E0 + 1 + l, (l + 1) & 1);
     grid.sync();
+    LG_TL(lead, ctl);
     const uint32_t total = ld_volatile_u32(&ctl->level_total[(l + 1) & 1]);
+    // chunk boundaries one level down: P_{l+1}(k) = fc[P_l(k)] (the end of a
+    // level maps to the end of the next; fc there belongs to the next sweep)
+    if (l + 1 <= (uint32_t)kChunkMaxLevels) {
+      for (uint32_t k = b * kTPB + tid; k <= nch; k += G * kTPB) {
+        const uint32_t p = a.cbound[(size_t)k * kCBS + l];
+        a.cbound[(size_t)k * kCBS + l + 1] = p >= hi ? hi + total : a.fc[p];
+      }
+    }
     if (total == 0) break;
     if (lead) a.levels[l + 2] = hi + total;
     lo = hi;
@@ -530,52 +842,61 @@ __global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
     ++l;
   }
   const uint32_t nlev = l + 1;
+  grid.sync();
+  LG_TL(lead, ctl);
   const unsigned long long t_order = globaltimer();
-  bool failed = false;
-  if (hi != a.N) {  // cells unreachable from the sources: a receiver cycle (traversal.cpp:46)
+  unsigned long long iters = 0;
+  uint32_t misses = 0;
+  const bool failed = hi != a.N;  // cells unreachable from the sources: a cycle (traversal.cpp:46)
+  if (failed) {
     if (lead) {
       ctl->err_flag = LEMGPU_ESTRUCTURE;
       ctl->err_cell = hi;  // cells placed
     }
-    failed = true;
-  }
-
-  // ---- accumulation, deepest level first (accumulation.cpp:7-17); the
-  // level-0 pass also applies uplift to the level-0 pits (erosion.cpp:52-57).
-  unsigned long long t_accum = t_order;
-  if (!failed) {
-    for (int L = (int)nlev - 1; L >= 0; --L) {
-      const uint32_t s = a.levels[L], e = a.levels[L + 1];
-      for (uint32_t pos = s + b * kTPB + tid; pos < e; pos += G * kTPB) {
-        double acc = a.w0;
-        const uint32_t j0 = a.fc[pos], j1 = a.fc[pos + 1];
-        for (uint32_t j = j0; j < j1; ++j) acc = __dadd_rn(acc, a.Aq[j]);
-        a.Aq[pos] = acc;
-        if (L == 0) {
-          const uint32_t c = a.order[pos];
-          const uint32_t x = c % a.W, yl = (c / a.W) % a.H;
-          double hv = a.h[c];
-          if (x > 0 && x < a.W - 1 && yl > 0 && yl < a.H - 1) {
-            hv = __dadd_rn(hv, a.du);
-            a.h[c] = hv;
-          }
-          a.hq[pos] = hv;
-        }
+  } else if (nlev <= (uint32_t)kChunkMaxLevels) {
+    // ---- Phase B: independent source chunks, one CTA each
+    ChunkSmem& s = sm.ch;
+    for (uint32_t k = b; k < nch; k += G) {
+      if (tid <= nlev) {
+        const uint32_t x = a.cbound[(size_t)k * kCBS + tid];
+        const uint32_t y = a.cbound[(size_t)(k + 1) * kCBS + tid];
+        s.lo[tid] = x;
+        s.base[tid] = y - x;  // level sizes, turned into a prefix below
       }
-      grid.sync();
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t acc = 0, d = 0;
+        for (uint32_t q = 0; q < nlev; ++q) {
+          const uint32_t n = s.base[q];
+          s.base[q] = acc;
+          acc += n;
+          if (n) d = q + 1;
+        }
+        for (uint32_t q = nlev; q <= (uint32_t)kCBS; ++q) s.base[q] = acc;
+        s.nl = d;
+        s.total = acc;
+      }
+      __syncthreads();
+      if (s.total <= (uint32_t)kChunkCap) {
+        chunk_smem<NK>(a, s, iters, misses);
+      } else {
+        // copy the chunk's per-level ranges out of the union first
+        uint32_t rlo[kCBS], rhi[kCBS];
+        const uint32_t nl = s.nl;
+        for (uint32_t q = 0; q < nl; ++q) {
+          rlo[q] = s.lo[q];
+          rhi[q] = s.lo[q] + (s.base[q + 1] - s.base[q]);
+        }
+        __syncthreads();
+        sweep_global<NK, false>(a, grid, rlo, rhi, nl, iters, misses);
+      }
     }
-    t_accum = globaltimer();
-
-    // ---- erosion, levels 1..L-1 downstream -> upstream (erosion.cpp:66-81)
-    unsigned long long iters = 0;
-    uint32_t misses = 0;
-    for (uint32_t L = 1; L < nlev; ++L) {
-      const uint32_t s = a.levels[L], e = a.levels[L + 1];
-      for (uint32_t pos = s + b * kTPB + tid; pos < e; pos += G * kTPB) erode_pos<NK>(a, pos, iters, misses);
-      grid.sync();
-      if (ld_volatile_u32(&ctl->err_flag)) break;
-    }
-    // deterministic integer reduction of the per-thread counters
+  } else {
+    // ---- deep plan: grid-wide level sweeps
+    sweep_global<NK, true>(a, grid, a.levels, a.levels + 1, nlev, iters, misses);
+  }
+  // deterministic integer reduction of the per-thread counters
+  {
     const int lane = tid & 31, warp = tid >> 5;
     for (int o = 16; o; o >>= 1) {
       iters += __shfl_down_sync(0xffffffffu, iters, o);
@@ -587,17 +908,18 @@ __global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
     }
     __syncthreads();
     if (tid == 0) {
-      unsigned long long s = 0;
+      unsigned long long sum = 0;
       uint32_t mm = 0;
       for (int w = 0; w < kNW; ++w) {
-        s += sm.red[w];
+        sum += sm.red[w];
         mm += sm.red32[w];
       }
-      if (s) atomicAdd(reinterpret_cast<unsigned long long*>(&a.diag->newton_iters), s);
+      if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(&a.diag->newton_iters), sum);
       if (mm) atomicAdd(&a.diag->lut_misses, mm);
     }
   }
   grid.sync();
+  LG_TL(lead, ctl);
   if (lead) {
     const unsigned long long t_end = globaltimer();
     const uint32_t st = ctl->err_flag;
@@ -605,13 +927,14 @@ __global__ void __launch_bounds__(kTPB) k_flow(StepArgs a) {
     d->seconds[LEMGPU_PHASE_RECEIVERS] = (double)(ctl->t_k1_end - ctl->t_k1_begin) * 1e-9;
     d->seconds[LEMGPU_PHASE_DONORS] = 0.0;  // fused into k_recv_donor
     d->seconds[LEMGPU_PHASE_ORDER] = (double)(t_order - t_begin) * 1e-9;
-    d->seconds[LEMGPU_PHASE_ACCUM] = (double)(t_accum - t_order) * 1e-9;
-    d->seconds[LEMGPU_PHASE_UPLIFT] = 0.0;  // fused into the accumulation / erosion sweeps
-    d->seconds[LEMGPU_PHASE_EROSION] = (double)(t_end - t_accum) * 1e-9;
+    d->seconds[LEMGPU_PHASE_ACCUM] = 0.0;   // fused with uplift + erosion per source chunk
+    d->seconds[LEMGPU_PHASE_UPLIFT] = 0.0;
+    d->seconds[LEMGPU_PHASE_EROSION] = (double)(t_end - t_order) * 1e-9;
     d->nlevels = nlev;
     d->interior_noflow = a.levels[1] - a.perim;
     d->status = st;
     d->err_cell = st ? ctl->err_cell : LEMGPU_NOFLOW;
+    d->reserved = nch;
     ctl->epoch = E0 + 2 + l;
     ctl->t_k1_begin = ~0ull;
     ctl->t_k1_end = 0ull;

@@ -357,6 +357,14 @@ class DeviceContext:
         self._check(self._L.lemgpu_kernel_times(self._h, ms, C.byref(n)))
         return {"recv_donor": ms[0], "flow": ms[1], "launches": n.value}
 
+    def debug_timeline(self):
+        """k_flow barrier timestamps of the last step, as ms offsets from its start."""
+        buf = (C.c_uint64 * 96)()
+        n = C.c_uint32(0)
+        self._check(self._L.lemgpu_debug_timeline(self._h, buf, 96, C.byref(n)))
+        t = [buf[i] for i in range(n.value)]
+        return [(x - t[0]) * 1e-6 for x in t]
+
     def device_bytes(self) -> int:
         b = C.c_uint64(0)
         self._check(self._L.lemgpu_device_bytes(self._h, C.byref(b)))

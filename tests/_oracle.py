@@ -149,6 +149,8 @@ class RefLib:
             C.POINTER(C.c_uint32), C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.lr_run.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32, C.c_uint32,
                              C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
+        L.lr_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32, C.c_uint64,
+                               C.c_uint32, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64)]
         self.L = L
 
     @classmethod
@@ -189,6 +191,17 @@ class RefLib:
         if rc not in (0, 3):
             raise RuntimeError(self.L.lr_last_error().decode())
         return rc, nt.value, ec.value
+
+    def bench(self, w, h, steps, warmup=0, strategy="rb_private_queues", workers=None, seed=42, conn=8, params=None):
+        """Per-step wall seconds of lem::strategy_step on a persistent workspace."""
+        p = params or make_params()
+        secs = np.zeros(max(1, steps), np.float64)
+        nt = C.c_uint64(0)
+        rc = self.L.lr_bench(w, h, conn, C.byref(p), strategy.encode(), workers or self.max_threads(), seed, warmup,
+                             steps, secs.ctypes.data, C.byref(nt))
+        if rc != 0:
+            raise RuntimeError(self.L.lr_last_error().decode())
+        return secs[:steps], nt.value
 
     def max_threads(self) -> int:
         return int(self.L.lr_max_threads())
