@@ -173,14 +173,17 @@ uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx);     /* members * width * heigh
 void* lemgpu_stream(lemgpu_ctx* ctx);                 /* the context's cudaStream_t */
 int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
 
-/* Per-kernel device time, accumulated over the steps since the last reset
- * (CUDA events around each launch on the context stream; enable first).
- * ms[0] = recv_donor, ms[1] = flow (order+accum+uplift+erosion). */
+/* Device time accumulated over the steps synced since timing was enabled:
+ * ms[0] = whole step (CUDA events around each graph launch on the context
+ * stream), ms[1] = k_recv_donor, ms[2] = level order (k_level0 + k_expand),
+ * ms[3] = accumulation + uplift + erosion (k_chunks / k_deep_*); the phase
+ * split comes from %globaltimer stamps taken on the device.  `ms` holds 4. */
 int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable);
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
 
-/* Debug: globaltimer stamps (ns) taken by k_flow at each grid barrier of the
- * last step (start, level 0, each expansion level, order done, sweeps done). */
+/* Debug: %globaltimer stamps (ns) of the last completed step: k_recv_donor
+ * begin/end, then the end of k_level0, of every k_expand level and of the
+ * accumulation/erosion sweeps. */
 int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t* count);
 
 /* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */

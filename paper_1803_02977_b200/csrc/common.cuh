@@ -1,0 +1,242 @@
+// common.cuh -- shared definitions of the sm_100a D8 landscape-evolution step.
+//
+// One timestep is a CUDA graph of these kernels:
+//
+//   k_recv_donor        receivers + donor bitmask, smem-staged stencil   (k_recv_donor.cuh)
+//   k_l0_count/_write   level 0 of the BFS order: stream compaction       (k_order.cuh)
+//   WHILE { k_expand }  one frontier expansion per level                  (k_order.cuh)
+//   k_chunks            accumulation + uplift + erosion per source chunk  (k_physics.cuh)
+//   k_deep_*            the same sweeps level by level for deep plans     (k_physics.cuh)
+//   k_finalize          per-step diagnostics                              (k_physics.cuh)
+//
+// The number of levels is data dependent; it is discovered on the device and
+// drives graph WHILE nodes (cudaGraphSetConditional), so a step is one
+// cudaGraphLaunch with no host round trip.
+//
+// Arithmetic is FP64 and never contracted: compiled with --fmad=false and
+// every rounding-relevant operation is an explicit __d*_rn intrinsic, so the
+// results are bit-identical to the reference built with -ffp-contract=off
+// (proj/CMakeLists.txt:14).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lemgpu.h"
+
+namespace lemgpu {
+
+constexpr int kTPB = 256;           // threads per CTA (all kernels)
+constexpr int kNW = kTPB / 32;      // warps per CTA
+constexpr uint8_t kNoFlowCode = 8;  // rcode value for kNoFlow
+
+// k_recv_donor tile (output cells): halo of 2 for h, 1 for the receiver codes.
+constexpr int kBX = 128;
+constexpr int kBY = 32;
+// scan tiles
+constexpr int kL0IPT = 16;              // level-0 cells per thread (one uint4 of rcodes)
+constexpr int kL0Tile = kTPB * kL0IPT;  // 4096 cells
+constexpr int kExIPT = 4;               // frontier items per thread
+constexpr int kExTile = kTPB * kExIPT;  // 1024 frontier cells
+// source chunks of the physics sweeps
+constexpr int kChunkRoots = 32;       // level-0 sources per chunk (one warp each)
+constexpr int kChunkCap = 512;        // cells per chunk held in shared memory
+constexpr int kChunkTPB = 128;        // k_chunks CTA: 4 warps, 4 chunks in flight
+constexpr int kChunkMaxLevels = 24;   // shallow (chunked) plans: nlevels <= this
+constexpr int kCBS = kChunkMaxLevels + 1;
+
+enum : uint32_t { kModeShallow = 0, kModeDeep = 1, kModeFailed = 2 };
+
+// Frozen D8 stencil (src/neighborhood.cpp:12): k -> (ox, oy).  The opposite
+// direction of k is 7-k.  D4 is the cardinal subsequence {1,3,4,6}
+// (neighborhood.cpp:20-29), kept at its D8 slot so stencil order and the
+// opposite-direction rule are shared.
+__host__ __device__ constexpr int dir_ox(int k) {
+  return (k == 0 || k == 3 || k == 5) ? -1 : (k == 1 || k == 6) ? 0 : 1;
+}
+__host__ __device__ constexpr int dir_oy(int k) { return k < 3 ? -1 : k < 5 ? 0 : 1; }
+// Branch-free runtime form: linear offset of direction k in a raster of width W.
+__device__ __forceinline__ int dir_off(uint32_t k, int W) {
+  const int ox = (int)((0x9224u >> (2 * k)) & 3u) - 1;
+  const int oy = (int)((0xA940u >> (2 * k)) & 3u) - 1;
+  return ox + oy * W;
+}
+__host__ __device__ constexpr bool dir_in(int conn, int k) {
+  return conn == 8 || k == 1 || k == 3 || k == 4 || k == 6;
+}
+
+// IEEE round-to-nearest arithmetic usable on host and device (host code is
+// compiled with -ffp-contract=off, so plain operators do not fuse).
+#ifdef __CUDA_ARCH__
+#define LG_ADD(x, y) __dadd_rn((x), (y))
+#define LG_SUB(x, y) __dsub_rn((x), (y))
+#define LG_MUL(x, y) __dmul_rn((x), (y))
+#define LG_DIV(x, y) __ddiv_rn((x), (y))
+#else
+#define LG_ADD(x, y) ((x) + (y))
+#define LG_SUB(x, y) ((x) - (y))
+#define LG_MUL(x, y) ((x) * (y))
+#define LG_DIV(x, y) ((x) / (y))
+#endif
+
+// Device control block (one per context).
+struct Ctl {
+  // persistent
+  uint32_t err_flag;  // sticky LEMGPU_* of the first failing step
+  uint32_t err_cell;  // failing cell (any failing cell is acceptable)
+  uint32_t err_slot;  // diagnostics slot of the step that failed
+  uint32_t slot;      // diagnostics slot of the running step
+  uint32_t cond[4];   // loop conditions when the step runs eagerly (no graph)
+  // per step (reset by k_finalize)
+  uint32_t lvl;          // level being expanded
+  uint32_t done;         // finished CTAs of the running kernel
+  uint32_t n0, nch, nlev, mode;
+  uint32_t dlvl;  // level of the deep sweeps
+  uint32_t misses;
+  unsigned long long newton;
+  unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
+  uint32_t ntl, nltl;
+  unsigned long long tl[96];   // debug timeline of the running step (finisher stamps)
+  unsigned long long ltl[98];  // ... and of the last completed step
+};
+
+struct StepArgs {
+  // geometry (stacked members: rows [m*H, (m+1)*H) belong to member m)
+  uint32_t W, H, M;
+  uint32_t N;     // W*H*M  (< 2^32, RunConfig::validate, config.cpp:159-161)
+  uint32_t MN;    // W*H
+  uint32_t Htot;  // H*M
+  uint32_t perim;  // perimeter cells over all members
+  int conn;
+  int maxit;
+  int nkind;      // 1: n == 1, 2: n == 2, 0: general n
+  int lut_exact;  // A is always an exact integer multiple of w0
+  int w0_is_one;
+  uint32_t lut_entries;
+  uint32_t dist_one;  // bit k set when dist[k] == 1.0 (division is the identity)
+  int unit_card;      // dx == dy == 1: cardinal slopes are the drops themselves
+  double rinv_diag;   // RN(1 / dist_diag): pre-decides far-from-tie comparisons only
+  double dist[8];     // offset_length of direction k (neighborhood.hpp:17-23)
+  double powdist_h, powdist_v, powdist_d;  // host-libm pow(dist, n) per offset class
+  double du, w0, n_exp, eps;
+  const double* kdt;   // per member K*dt
+  const double* mexp;  // per member m
+  const double* ftab;  // per member and offset class: F(a) = (K*dt * pow(a*w0, m)) / pow(dist, n), host libm
+  // state / scratch
+  double* h;
+  uint8_t* rcode;
+  uint8_t* dmask;
+  uint32_t* order;
+  uint32_t* ppos;
+  uint32_t* fc;
+  uint32_t* cbound;  // [level][chunk]: first position of a source chunk at each level
+  uint32_t cb_stride;
+  double* Aq;
+  double* hq;
+  uint32_t* levels;
+  uint8_t* pdm;       // donor mask of the cell at each queue position
+  uint32_t* part;     // level-0 per-segment NoFlow counts
+  uint32_t* bins;     // 3 x scan_grid per-segment child counts (rotating)
+  uint32_t scan_grid;  // CTAs of the scan kernels (segments per level)
+  int eager;          // 1: no graph; loop conditions go through ctl->cond
+  int use_tma;        // k_recv_donor stages h with one TMA box per tile
+  Ctl* ctl;
+  lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
+  cudaGraphConditionalHandle h_expand, h_dacc, h_deros;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+__device__ __forceinline__ void timeline(Ctl* ctl) {
+  const uint32_t i = ctl->ntl;
+  if (i < 96) {
+    ctl->tl[i] = globaltimer();
+    ctl->ntl = i + 1;
+  }
+}
+
+// True in every thread of exactly one CTA: the last CTA of the grid to get
+// here (all others have finished their work and fenced it).  The caller's
+// finisher code then sees every CTA's global writes.  Resets the counter.
+__device__ __forceinline__ bool last_block_done(Ctl* ctl) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t prev = atomicAdd(&ctl->done, 1u);
+    s_last = (prev == nb - 1) ? 1u : 0u;
+    if (s_last) {
+      ctl->done = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+// Exclusive block scan of one u32 per thread; *total gets the block sum.
+// scratch: kNW+1 u32 of shared memory; contains the barriers it needs.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kNW ? scratch[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < kNW; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kNW) scratch[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t warp_excl = warp ? scratch[warp - 1] : 0u;
+  *total = scratch[kNW - 1];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+// Loop condition of the step graph (0: level expansion, 1: deep
+// accumulation, 2: deep erosion): a graph conditional when the step is a
+// CUDA graph, a control-block word when it runs eagerly (profiling).
+__device__ __forceinline__ void set_cond(const StepArgs& a, int which, unsigned v) {
+  if (a.eager) {
+    a.ctl->cond[which] = v;
+  } else {
+    const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : a.h_deros;
+    cudaGraphSetConditional(h, v);
+  }
+}
+
+__device__ __forceinline__ bool is_interior(const StepArgs& a, uint32_t c) {
+  const uint32_t y = c / a.W, x = c - y * a.W, yl = y % a.H;
+  return x > 0 && x < a.W - 1 && yl > 0 && yl < a.H - 1;
+}
+
+}  // namespace lemgpu

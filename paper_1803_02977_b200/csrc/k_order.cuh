@@ -1,0 +1,332 @@
+// k_order.cuh -- the breadth-first level order (phase 3), the paper's key
+// restructuring.
+//
+//   generate_queue   proj/src/traversal.cpp:19-48
+//
+// Level 0 is the ascending list of cells with rec == kNoFlow (traversal.cpp:
+// 27-29); level l+1 is, for each level-l cell in order, its donors in slot
+// (= stencil = bit) order (traversal.cpp:35-44).  Every level is a stream
+// compaction over a static partition of its position range into one segment
+// per CTA (reduce-then-scan, no serial look-back chain):
+//
+//   * the per-segment item counts of level l are accumulated into bins by
+//     the kernel that WRITES level l (warp-aggregated integer atomics), so each
+//     level needs a single kernel: CTA b sums the bins of segments < b for its
+//     base, then scans its segment tile by tile (warp shuffles + smem, carry
+//     between tiles) and writes the children and fc[pos], the queue position
+//     of the first child;
+//   * each queue entry carries its cell's donor mask (pdm, written when the
+//     entry is created), so counting and expanding a level read it coalesced
+//     instead of gathering dmask by cell index.
+//
+// The level loop is a graph WHILE node; the last CTA of each level clears its
+// condition when the next level is empty.
+#pragma once
+
+#include "common.cuh"
+
+namespace lemgpu {
+
+constexpr int kKidCap = 8 * kExTile;  // children of one expansion tile, staged in smem (any fan-out)
+
+struct ScanSmem {
+  uint32_t scan[kNW + 1];
+  uint32_t base;
+  uint32_t ord[kExTile];
+  uint8_t dm[kExTile];
+  uint32_t kids[kKidCap];
+};
+
+// Sum of v over the first `upto` entries of bins[] (one CTA, all threads);
+// also the sum of all `nb` entries.
+__device__ __forceinline__ void bins_prefix(const uint32_t* bins, uint32_t upto, uint32_t nb,
+                                            uint32_t* scratch, uint32_t& pre, uint32_t& total) {
+  uint32_t p = 0, t = 0;
+  for (uint32_t i = threadIdx.x; i < nb; i += kTPB) {
+    const uint32_t v = bins[i];
+    t += v;
+    if (i < upto) p += v;
+  }
+  p = __reduce_add_sync(0xffffffffu, p);
+  t = __reduce_add_sync(0xffffffffu, t);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t sp[kNW], st[kNW];
+  if (lane == 0) {
+    sp[warp] = p;
+    st[warp] = t;
+  }
+  __syncthreads();
+  p = 0;
+  t = 0;
+#pragma unroll
+  for (int w = 0; w < kNW; ++w) {
+    p += sp[w];
+    t += st[w];
+  }
+  pre = p;
+  total = t;
+  __syncthreads();
+  (void)scratch;
+}
+
+// Add v to bins[bin] with one atomic per distinct bin of the warp.
+__device__ __forceinline__ void bin_add(uint32_t* bins, uint32_t bin, uint32_t v, bool active) {
+  const uint32_t key = active ? bin : 0xFFFFFFFFu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const uint32_t sum = __reduce_add_sync(peers, v);
+  if (active && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1) && sum) atomicAdd(bins + bin, sum);
+}
+
+// Second pass over the queue positions [p0, p1) just written by this CTA:
+// each entry's donor mask (coalesced pdm store, gathered dmask with several
+// loads in flight per thread) and the per-segment child counts of the next
+// sweep (segments of Sn positions starting at `base`).
+template <bool KIDS>
+__device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* kids, uint32_t p0, uint32_t p1,
+                                             uint32_t base, uint32_t Sn, uint32_t* bins) {
+  uint32_t cur_bin = 0xFFFFFFFFu, cur_end = 0, sum = 0;
+  for (uint32_t pb = p0 + threadIdx.x; pb < p1; pb += 4 * kTPB) {
+    uint32_t cm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t p = pb + u * kTPB;
+      if (p < p1) {
+        uint32_t child;
+        if (KIDS) {
+          child = kids[p - p0];
+          a.order[p] = child;
+        } else {
+          child = a.order[p];
+        }
+        cm[u] = __ldg(a.dmask + child);
+      } else {
+        cm[u] = 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t p = pb + u * kTPB;
+      if (p < p1) {
+        a.pdm[p] = (uint8_t)cm[u];
+        if (p >= cur_end) {
+          if (sum) atomicAdd(bins + cur_bin, sum);
+          cur_bin = (p - base) / Sn;
+          cur_end = base + (cur_bin + 1) * Sn;
+          sum = 0;
+        }
+        sum += __popc(cm[u]);
+      }
+    }
+  }
+  bin_add(bins, cur_bin, sum, cur_bin != 0xFFFFFFFFu);
+}
+
+// segment size of a level of n items over G CTAs
+__device__ __forceinline__ uint32_t seg_size(uint32_t n, uint32_t G) { return n ? (n + G - 1) / G : 1u; }
+
+// --------------------------------------------------------------- level 0
+// pass 1: NoFlow count per segment of the cell range
+__global__ void __launch_bounds__(kTPB) k_l0_count(StepArgs a) {
+  Ctl* ctl = a.ctl;
+  if (ld_volatile_u32(&ctl->err_flag)) return;  // sticky failure of an earlier step (uniform)
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t S = ((a.N + G - 1) / G + 15u) & ~15u;
+  const uint32_t s0 = b * S, s1 = min(a.N, s0 + S);
+  uint32_t cnt = 0;
+  for (uint32_t c = s0 + threadIdx.x * 16; c < s1; c += kTPB * 16) {
+    if (c + 16 <= s1) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.rcode + c));
+      cnt += (__popc(__vcmpeq4(v.x, 0x08080808u)) + __popc(__vcmpeq4(v.y, 0x08080808u)) +
+              __popc(__vcmpeq4(v.z, 0x08080808u)) + __popc(__vcmpeq4(v.w, 0x08080808u))) >> 3;
+    } else {
+      for (uint32_t j = c; j < s1; ++j) cnt += a.rcode[j] == kNoFlowCode;
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  __shared__ uint32_t sw[kNW];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kNW; ++w) t += sw[w];
+    a.part[b] = t;
+  }
+  for (uint32_t i = b * kTPB + threadIdx.x; i < G; i += G * kTPB) a.bins[i] = 0;  // bins of level 0
+}
+
+// pass 2: write level 0 (ascending cells), its donor masks and the bins of
+// its child counts
+__global__ void __launch_bounds__(kTPB) k_l0_write(StepArgs a) {
+  __shared__ ScanSmem sm;
+  Ctl* ctl = a.ctl;
+  if (ld_volatile_u32(&ctl->err_flag)) return;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t S = ((a.N + G - 1) / G + 15u) & ~15u;
+  const uint32_t s0 = b * S, s1 = min(a.N, s0 + S);
+  uint32_t pre, n0;
+  bins_prefix(a.part, b, G, sm.scan, pre, n0);
+  const uint32_t Sb = seg_size(n0, G);  // level-0 segment size for k_expand(0)
+  for (uint32_t i = b * kTPB + threadIdx.x; i < G; i += G * kTPB) a.bins[G + i] = 0;  // bins of level 1
+  uint32_t carry = pre;
+  for (uint32_t t0 = s0; t0 < s1; t0 += kL0Tile) {
+    const uint32_t c0 = t0 + threadIdx.x * kL0IPT;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (c0 + kL0IPT <= s1) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.rcode + c0));
+      w[0] = v.x;
+      w[1] = v.y;
+      w[2] = v.z;
+      w[3] = v.w;
+    } else {
+      for (uint32_t j = 0; j < (uint32_t)kL0IPT; ++j)
+        if (c0 + j < s1) w[j >> 2] |= (uint32_t)a.rcode[c0 + j] << (8 * (j & 3));
+    }
+    uint32_t eq[4], cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      eq[q] = __vcmpeq4(w[q], 0x08080808u);
+      cnt += __popc(eq[q]) >> 3;
+    }
+    uint32_t tot;
+    const uint32_t first = carry;
+    uint32_t out = carry + block_excl_scan(cnt, &tot, sm.scan);
+    carry += tot;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t e = eq[q];
+      while (e) {
+        const int bit = __ffs(e) - 1;
+        e &= ~(0xFFu << (bit & ~7));
+        a.order[out++] = c0 + q * 4 + (bit >> 3);
+      }
+    }
+    __syncthreads();  // this tile's queue entries are visible to the whole CTA
+    pdm_and_bins<false>(a, nullptr, first, first + tot, 0u, Sb, a.bins);
+  }
+  if (last_block_done(ctl) && threadIdx.x == 0) {
+    a.levels[0] = 0;
+    a.levels[1] = n0;
+    a.fc[a.N] = a.N;
+    ctl->n0 = n0;
+    ctl->nch = (n0 + kChunkRoots - 1) / kChunkRoots;
+    ctl->lvl = 0;
+    timeline(ctl);
+  }
+}
+
+// --------------------------------------------------------- level l -> l+1
+// One level of the while loop.  Also derives the per-chunk position ranges
+// of this level from fc[] of the previous one: a chunk of consecutive sources
+// owns ONE contiguous range per level, P_l(k) = fc[P_{l-1}(k)] (the end of a
+// level maps to the end of the next).
+__global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
+  __shared__ ScanSmem sm;
+  Ctl* ctl = a.ctl;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t l = ld_volatile_u32(&ctl->lvl);
+  const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
+  const uint32_t lo = a.levels[l], hi = a.levels[l + 1];
+  uint32_t total = 0;
+  if (!err) {
+    const uint32_t* bins_in = a.bins + (size_t)(l % 3) * G;
+    uint32_t* bins_out = a.bins + (size_t)((l + 1) % 3) * G;
+    uint32_t* bins_clr = a.bins + (size_t)((l + 2) % 3) * G;
+    for (uint32_t i = b * kTPB + threadIdx.x; i < G; i += G * kTPB) bins_clr[i] = 0;
+    if (l <= (uint32_t)kChunkMaxLevels) {
+      const uint32_t nch = ctl->nch;
+      uint32_t* cb = a.cbound + (size_t)l * a.cb_stride;
+      const uint32_t* cbp = a.cbound + (size_t)(l ? l - 1 : 0) * a.cb_stride;
+      for (uint32_t k = b * kTPB + threadIdx.x; k <= nch; k += G * kTPB) {
+        uint32_t v;
+        if (l == 0) {
+          v = min(k * (uint32_t)kChunkRoots, hi);
+        } else {
+          const uint32_t p = cbp[k];
+          v = p >= lo ? hi : a.fc[p];
+        }
+        cb[k] = v;
+      }
+    }
+    uint32_t pre;
+    bins_prefix(bins_in, b, G, sm.scan, pre, total);
+    const uint32_t S = seg_size(hi - lo, G);
+    const uint32_t Sn = seg_size(total, G);  // segment size of the next level
+    const uint32_t s0 = lo + min(b * S, hi - lo), s1 = lo + min((b + 1) * S, hi - lo);
+    uint32_t carry = hi + pre;
+    const uint32_t W = a.W;
+    for (uint32_t tb = s0; tb < s1; tb += kExTile) {
+      // coalesced staging of the tile's cells and donor masks
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) {
+        const uint32_t p = tb + j * kTPB + threadIdx.x;
+        const bool in = p < s1;
+        sm.ord[j * kTPB + threadIdx.x] = in ? a.order[p] : 0u;
+        sm.dm[j * kTPB + threadIdx.x] = in ? a.pdm[p] : (uint8_t)0;
+      }
+      __syncthreads();
+      uint32_t c[kExIPT], m[kExIPT], cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) {
+        c[j] = sm.ord[threadIdx.x * kExIPT + j];
+        m[j] = sm.dm[threadIdx.x * kExIPT + j];
+        cnt += __popc(m[j]);
+      }
+      uint32_t tot;
+      uint32_t out = carry + block_excl_scan(cnt, &tot, sm.scan);
+      carry += tot;
+      const uint32_t first = carry - tot;
+      uint32_t fcv[kExIPT];
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) {
+        fcv[j] = out;
+        uint32_t mm = m[j];
+        while (mm) {
+          const uint32_t k = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const uint32_t child = (uint32_t)((int)c[j] + dir_off(k, (int)W));
+          sm.kids[out - first] = child;
+          ++out;
+        }
+      }
+      __syncthreads();  // sm.ord reused to transpose fc for coalesced stores
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) sm.ord[threadIdx.x * kExIPT + j] = fcv[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) {
+        const uint32_t p = tb + j * kTPB + threadIdx.x;
+        if (p < s1) a.fc[p] = sm.ord[j * kTPB + threadIdx.x];
+      }
+      pdm_and_bins<true>(a, sm.kids, first, first + tot, hi, Sn, bins_out);
+      __syncthreads();
+    }
+  }
+  if (last_block_done(ctl) && threadIdx.x == 0) {
+    if (total > 0) {
+      a.levels[l + 2] = hi + total;
+      ctl->lvl = l + 1;
+      set_cond(a, 0, 1);
+    } else {
+      // plan complete: nlevels = l + 1 (traversal.cpp:45); cycle check (:46)
+      ctl->nlev = l + 1;
+      uint32_t mode = l + 1 <= (uint32_t)kChunkMaxLevels ? kModeShallow : kModeDeep;
+      if (!err && hi != a.N) {
+        ctl->err_flag = LEMGPU_ESTRUCTURE;
+        ctl->err_cell = hi;  // cells placed
+        ctl->err_slot = ctl->slot;
+        mode = kModeFailed;
+      }
+      if (err) mode = kModeFailed;
+      ctl->mode = mode;
+      if (mode == kModeDeep) {
+        ctl->dlvl = l;  // deepest level first
+        set_cond(a, 1, 1);
+      }
+      ctl->t_order_end = globaltimer();
+      set_cond(a, 0, 0);
+    }
+    timeline(ctl);
+  }
+}
+
+}  // namespace lemgpu

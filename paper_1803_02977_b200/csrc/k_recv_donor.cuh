@@ -1,0 +1,273 @@
+// k_recv_donor.cuh -- receivers (phase 1) + donors (phase 2) in one stencil pass.
+//
+//   steepest_receiver  proj/include/lem/flow_graph.hpp:44-59
+//   donors_of          proj/include/lem/flow_graph.hpp:64-72
+//
+// One CTA owns a kBY x kBX tile.  h is staged in shared memory with a 2-cell
+// halo (one coalesced HBM read of h), receiver codes are computed for the
+// tile plus a 1-cell ring, and the donor bitmask of every tile cell is then
+// a pull over the neighbours' codes (no atomics).  Outputs: rcode (the D8
+// direction 0..7 of the receiver, 8 = kNoFlow) and dmask (bit k set when the
+// neighbour in direction k drains into the cell), one byte each.
+#pragma once
+
+#include "common.cuh"
+
+namespace lemgpu {
+
+// The reference loop itself, with its exact skips: ec - en <= 0 never beats
+// s_max >= 0 and x / 1.0 == x.  Used for general spacing / D4 and as the exact
+// slow path of the D8 fast path.
+template <int CONN>
+__host__ __device__ __forceinline__ uint8_t receiver_code_ref(const double (&d)[8], const StepArgs& a) {
+  double smax = 0.0;
+  uint8_t code = kNoFlowCode;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (!dir_in(CONN, k)) continue;
+    if (d[k] > 0.0) {
+      const double s = ((a.dist_one >> k) & 1u) ? d[k] : LG_DIV(d[k], a.dist[k]);
+      if (s > smax) {
+        smax = s;
+        code = (uint8_t)k;
+      }
+    }
+  }
+  return code;
+}
+
+__host__ __device__ __forceinline__ double dmax2(double x, double y) { return y > x ? y : x; }
+
+// D8, unit cardinal spacing (the reference default): division-free argmax.
+// t_k = d_k for cardinals (exact: x / 1.0 == x) and t_k = RN(d_k * RN(1/c))
+// for diagonals, within 2^-51 relative of the true slope RN(d_k / c).  If a
+// single direction lies within 2^-48 of max t it is the unique argmax of the
+// true slopes; several cardinal candidates are exact and the first maximum
+// wins; anything else (near ties involving a diagonal, subnormal drops) takes
+// the reference loop.  Verified against the loop on 2M adversarial vectors
+// (tests/native/test_receiver_code.cu).
+template <int CONN>
+__host__ __device__ __forceinline__ uint8_t receiver_code(const double (&d)[8], const StepArgs& a) {
+  if (CONN == 8 && a.unit_card) {
+    double t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool diag = (k == 0 || k == 2 || k == 5 || k == 7);
+      t[k] = diag ? LG_MUL(d[k], a.rinv_diag) : d[k];
+    }
+    const double tmax = dmax2(dmax2(dmax2(t[0], t[1]), dmax2(t[2], t[3])),
+                              dmax2(dmax2(t[4], t[5]), dmax2(t[6], t[7])));
+    // t_k > 0 <=> d_k > 0 (RN(x * 0.707..) of a positive x never rounds to 0),
+    // so tmax <= 0 means no downhill neighbour; tiny positive maxima take the
+    // reference loop
+    if (!(tmax > 0x1p-1000)) return tmax > 0.0 ? receiver_code_ref<CONN>(d, a) : kNoFlowCode;
+    const double thr = LG_MUL(tmax, 1.0 - 0x1p-48);
+    uint32_t cand = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cand |= (t[k] >= thr ? 1u : 0u) << k;
+    if ((cand & (cand - 1)) == 0) {  // a single candidate
+#ifdef __CUDA_ARCH__
+      return (uint8_t)(__ffs(cand) - 1);
+#else
+      return (uint8_t)__builtin_ctz(cand);
+#endif
+    }
+    if ((cand & 0xA5u) == 0) {  // only cardinals (exact values): first maximum
+      uint32_t eq = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) eq |= ((cand >> k) & 1u) && t[k] == tmax ? (1u << k) : 0u;
+#ifdef __CUDA_ARCH__
+      return (uint8_t)(__ffs(eq) - 1);
+#else
+      return (uint8_t)__builtin_ctz(eq);
+#endif
+    }
+    return receiver_code_ref<CONN>(d, a);
+  }
+  return receiver_code_ref<CONN>(d, a);
+}
+
+// ---- TMA (cp.async.bulk.tensor) staging of the h tile, mbarrier completion
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// exact per-byte equality mask: 0x01 in every byte of x that is zero
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+  const uint32_t t = ((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x;
+  return (~t & 0x80808080u) >> 7;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
+  __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
+  __shared__ __align__(4) uint8_t rc[kBY + 2][kBX + 4];
+  __shared__ uint8_t rowint[kBY + 2];
+  __shared__ __align__(8) uint64_t bar;
+  if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+  const uint32_t W = a.W, Ht = a.Htot;
+  if (tid == 0) {
+    atomicMin(&a.ctl->t_k1_begin, globaltimer());
+    if (a.use_tma) {
+      // one TMA box = the whole halo tile; out-of-range cells arrive as 0
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (uint32_t)sizeof(sh));
+      tma_load_2d(&sh[0][0], &hmap, (int)x0 - 2, (int)y0 - 2, &bar);
+    }
+  }
+
+  // ---- stage h: rows y0-2 .. y0+kBY+1, columns x0-2 .. x0+kBX+1
+  if (!a.use_tma) for (int r = warp; r < kBY + 4; r += kNW) {
+    const int gy = (int)y0 - 2 + r;
+    const bool rowok = gy >= 0 && (uint32_t)gy < Ht;
+    const double* row = a.h + (size_t)(rowok ? gy : 0) * W;
+#pragma unroll
+    for (int j = 0; j < kBX / 32; ++j) {
+      const uint32_t gx = x0 + lane + 32 * j;
+      sh[r][2 + lane + 32 * j] = (rowok && gx < W) ? __ldg(row + gx) : 0.0;
+    }
+    if (lane < 4) {
+      const int cc = lane < 2 ? lane : kBX + lane;  // 0,1 | kBX+2,kBX+3
+      const int gx = (int)x0 - 2 + cc;
+      sh[r][cc] = (rowok && gx >= 0 && (uint32_t)gx < W) ? __ldg(row + gx) : 0.0;
+    }
+  }
+  if (tid < kBY + 2) {  // rc row r <-> gy = y0 - 1 + r: does it hold interior cells?
+    const int gy = (int)y0 - 1 + tid;
+    uint8_t ok = 0;
+    if (gy >= 0 && (uint32_t)gy < Ht) {
+      const uint32_t yl = (uint32_t)gy % a.H;
+      ok = yl > 0 && yl < a.H - 1;
+    }
+    rowint[tid] = ok;
+  }
+  __syncthreads();
+  if (a.use_tma) mbar_wait(&bar, 0);
+
+  // ---- receiver codes for rc rows 0..kBY+1 (gy = y0-1+r), rc columns
+  // c = 0..kBX+1 (gx = x0-1+c).  Columns 1..kBX: one thread per column and
+  // half of the rows, sliding a 3x3 register window down the column (three
+  // shared loads per cell); the two ring columns are done separately.
+  {
+    const int c = 1 + (tid & (kBX - 1));
+    const int rbeg = (tid < kBX) ? 0 : (kBY + 2) / 2;
+    const int rend = (tid < kBX) ? (kBY + 2) / 2 : kBY + 2;
+    const int gx = (int)x0 - 1 + c;
+    const bool colint = gx > 0 && gx < (int)W - 1;
+    // window rows: w0 = sh row r, w1 = r+1, w2 = r+2 (sh col c..c+2)
+    double w0[3], w1[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      w0[q] = sh[rbeg][c + q];
+      w1[q] = sh[rbeg + 1][c + q];
+    }
+    for (int r = rbeg; r < rend; ++r) {
+      double w2[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) w2[q] = sh[r + 2][c + q];
+      uint8_t code = kNoFlowCode;
+      if (colint && rowint[r]) {
+        const double ec = w1[1];
+        double d[8];
+        d[0] = LG_SUB(ec, w0[0]);
+        d[1] = LG_SUB(ec, w0[1]);
+        d[2] = LG_SUB(ec, w0[2]);
+        d[3] = LG_SUB(ec, w1[0]);
+        d[4] = LG_SUB(ec, w1[2]);
+        d[5] = LG_SUB(ec, w2[0]);
+        d[6] = LG_SUB(ec, w2[1]);
+        d[7] = LG_SUB(ec, w2[2]);
+        if (CONN == 4) d[0] = d[2] = d[5] = d[7] = 0.0;
+        code = receiver_code<CONN>(d, a);
+      }
+      rc[r][c] = code;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        w0[q] = w1[q];
+        w1[q] = w2[q];
+      }
+    }
+  }
+  if (tid < 2 * (kBY + 2)) {  // ring columns c = 0 and c = kBX+1
+    const int r = tid >> 1, c = (tid & 1) ? kBX + 1 : 0;
+    const int gx = (int)x0 - 1 + c;
+    uint8_t code = kNoFlowCode;
+    if (rowint[r] && gx > 0 && gx < (int)W - 1) {
+      const double ec = sh[r + 1][c + 1];
+      double d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d[k] = dir_in(CONN, k) ? LG_SUB(ec, sh[r + 1 + dir_oy(k)][c + 1 + dir_ox(k)]) : 0.0;
+      code = receiver_code<CONN>(d, a);
+    }
+    rc[r][c] = code;
+  }
+  __syncthreads();
+
+  // ---- donors_of: neighbour in direction k donates iff its code is 7-k.
+  // Four cells per thread in SWAR form: for each direction, the four
+  // neighbour codes are one byte window of a shared row.
+  for (int r = warp; r < kBY; r += kNW) {
+    const uint32_t gy = y0 + r;
+    if (gy >= Ht) break;
+    const int c4 = lane * 4;  // tile columns c4..c4+3 <-> rc columns c4+1..c4+4
+    uint32_t lo[3], hi[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      lo[q] = *reinterpret_cast<const uint32_t*>(&rc[r + q][c4]);
+      hi[q] = *reinterpret_cast<const uint32_t*>(&rc[r + q][c4 + 4]);
+    }
+    uint32_t pm = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (!dir_in(CONN, k)) continue;
+      const int q = 1 + dir_oy(k);
+      const uint32_t sel = dir_ox(k) < 0 ? 0x3210u : dir_ox(k) == 0 ? 0x4321u : 0x5432u;
+      const uint32_t win = __byte_perm(lo[q], hi[q], sel);
+      pm |= zero_bytes(win ^ (0x01010101u * (uint32_t)(7 - k))) << k;
+    }
+    const uint32_t pc = __byte_perm(lo[1], hi[1], 0x4321u);
+    const uint32_t gx = x0 + c4;
+    const size_t base = (size_t)gy * W + gx;
+    if (gx + 3 < W && (W & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
+      *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
+    } else {
+      for (int j = 0; j < 4; ++j)
+        if (gx + j < W) {
+          a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
+          a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
+        }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());
+}
+
+}  // namespace lemgpu

@@ -1,0 +1,101 @@
+// k_util.cuh -- non-hot-path kernels: terrain generation, input check,
+// graph/accumulation export for parity, per-member statistics.
+#pragma once
+
+#include "common.cuh"
+
+namespace lemgpu {
+
+
+// lem::generate_terrain (terrain.cpp:12-31), per member seed.
+__global__ void k_terrain(double* h, uint32_t N, uint32_t MN, const unsigned long long* seeds) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const uint32_t m = i / MN, li = i - m * MN;
+    unsigned long long z = seeds[m] + (unsigned long long)li * 0x9E3779B97F4A7C15ull;
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    h[i] = __dmul_rn((double)(z >> 11), 0x1.0p-53);
+  }
+}
+
+// First non-finite cell (run_simulation's input check, scheduler.cpp:474-477).
+__global__ void k_check_finite(const double* h, uint32_t N, uint32_t* first_bad) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+    if (!isfinite(h[i])) atomicMin(first_bad, i);
+}
+
+// FlowGraph export in the reference layout (flow_graph.hpp:19-38).
+__global__ void k_export_graph(StepArgs a, uint32_t* rec, uint8_t* dnum, uint32_t* donor) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {
+    const uint8_t code = a.rcode[c];
+    if (rec) rec[c] = code == kNoFlowCode ? LEMGPU_NOFLOW : (uint32_t)((long long)c + dir_ox(code) + (long long)dir_oy(code) * a.W);
+    const uint32_t m = a.dmask[c];
+    if (dnum) dnum[c] = (uint8_t)__popc(m);
+    if (donor) {
+      uint32_t* slot = donor + (size_t)c * a.conn;
+      int j = 0;
+      for (int k = 0; k < 8; ++k)
+        if ((m >> k) & 1u) slot[j++] = (uint32_t)((long long)c + dir_ox(k) + (long long)dir_oy(k) * a.W);
+      for (; j < a.conn; ++j) slot[j] = LEMGPU_NOFLOW;
+    }
+  }
+}
+
+__global__ void k_export_accum(StepArgs a, double* A) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < a.N; p += gridDim.x * blockDim.x)
+    A[a.order[p]] = a.Aq[p];
+}
+
+// Per-member {sum, max, min} partials over fixed chunks (deterministic).
+__global__ void k_stats_partial(const double* h, uint32_t MN, uint32_t chunks, double* part) {
+  const uint32_t m = blockIdx.y, ch = blockIdx.x;
+  const uint32_t per = (MN + chunks - 1) / chunks;
+  const uint32_t s = ch * per, e = min(MN, s + per);
+  const double* hm = h + (size_t)m * MN;
+  double sum = 0.0, mx = -INFINITY, mn = INFINITY;
+  for (uint32_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+    const double v = hm[i];
+    sum = __dadd_rn(sum, v);
+    mx = fmax(mx, v);
+    mn = fmin(mn, v);
+  }
+  __shared__ double ss[kTPB], sx[kTPB], sn[kTPB];
+  ss[threadIdx.x] = sum;
+  sx[threadIdx.x] = mx;
+  sn[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = kTPB / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      ss[threadIdx.x] = __dadd_rn(ss[threadIdx.x], ss[threadIdx.x + o]);
+      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + o]);
+      sn[threadIdx.x] = fmin(sn[threadIdx.x], sn[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = part + ((size_t)m * chunks + ch) * 3;
+    o[0] = ss[0];
+    o[1] = sx[0];
+    o[2] = sn[0];
+  }
+}
+
+__global__ void k_stats_final(const double* part, uint32_t M, uint32_t chunks, uint32_t MN, double* out) {
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
+    double sum = 0.0, mx = -INFINITY, mn = INFINITY;
+    for (uint32_t ch = 0; ch < chunks; ++ch) {
+      const double* p = part + ((size_t)m * chunks + ch) * 3;
+      sum = __dadd_rn(sum, p[0]);
+      mx = fmax(mx, p[1]);
+      mn = fmin(mn, p[2]);
+    }
+    out[4 * m + 0] = __ddiv_rn(sum, (double)MN);
+    out[4 * m + 1] = mx;
+    out[4 * m + 2] = mn;
+    out[4 * m + 3] = sum;
+  }
+}
+
+}  // namespace lemgpu

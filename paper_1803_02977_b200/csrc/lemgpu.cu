@@ -1,10 +1,10 @@
 // lemgpu.cu -- host side of the C-ABI declared in include/lemgpu.h.
 //
 // Owns one device context per DEM (or per batch of ensemble members):
-// device buffers laid out for HBM (SoA, cell-major state + queue-position-major
-// scratch), one CUDA stream, and the launch sequence of one timestep:
-//   k_recv_donor  (regular launch, 2D tiles)
-//   k_flow        (cooperative launch, one persistent CTA set)
+// device buffers laid out for HBM (SoA: cell-major state, queue-position-major
+// scratch), one CUDA stream, and ONE instantiated CUDA graph per context that
+// is a whole timestep (see common.cuh): the level loops are graph WHILE nodes
+// driven from the device, so a step is a single cudaGraphLaunch.
 // No phase ever runs on the CPU.  The host computes only what must come from
 // the host libm to be bit-identical with the reference: the stencil
 // distances (neighborhood.hpp:17-23), pow(dist, n) and the pow(A, m) table.
@@ -14,13 +14,18 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "lemgpu.h"
-#include "lemgpu_kernels.cuh"
+#include "common.cuh"
+#include "k_order.cuh"
+#include "k_physics.cuh"
+#include "k_recv_donor.cuh"
+#include "k_util.cuh"
 
 using namespace lemgpu;
 
@@ -30,7 +35,10 @@ struct lemgpu_ctx {
   StepArgs a{};
   lemgpu_params params{};
   std::vector<lemgpu_member> members;
-  int flow_grid = 0;
+  int scan_grid = 0, chunk_grid = 0, deep_grid = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CUtensorMap hmap{};  // TMA descriptor of h (k_recv_donor staging)
   // device allocations
   double* d_kdt = nullptr;
   double* d_mexp = nullptr;
@@ -41,10 +49,10 @@ struct lemgpu_ctx {
   uint32_t last_nlevels = 0;
   bool have_graph = false;
   uint64_t device_bytes = 0;
-  // timing
+  // timing: CUDA events around each graph launch + device phase stamps
   bool timing = false;
-  std::vector<cudaEvent_t> ev;  // 3 per pending step
-  double kernel_ms[2] = {0, 0};
+  std::vector<cudaEvent_t> ev;  // 2 per pending step
+  double kernel_ms[4] = {0, 0, 0, 0};  // step, recv_donor, order, accumulation+uplift+erosion
   uint32_t kernel_launches = 0;
   // errors
   std::string msg;
@@ -125,6 +133,72 @@ int dmalloc(lemgpu_ctx* ctx, T** p, size_t count) {
   return 0;
 }
 
+// One timestep as a CUDA graph (see common.cuh).  StepArgs is captured by
+// value in every kernel node; everything that changes from step to step lives
+// in the device control block.
+int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void* fn, dim3 grid,
+               dim3 block, size_t smem, bool with_map = false) {
+  cudaKernelNodeParams kp{};
+  void* args[] = {&ctx->a, &ctx->hmap};
+  (void)with_map;
+  kp.func = const_cast<void*>(fn);
+  kp.gridDim = grid;
+  kp.blockDim = block;
+  kp.sharedMemBytes = (unsigned)smem;
+  kp.kernelParams = args;
+  cudaGraphNode_t n;
+  CU(ctx, cudaGraphAddKernelNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+  *prev = n;
+  return 0;
+}
+
+int add_while(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, cudaGraphConditionalHandle h,
+              const void* fn, dim3 grid, size_t smem) {
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t n;
+  CU(ctx, cudaGraphAddNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaGraphNode_t inner = nullptr;
+  const int rc = add_kernel(ctx, body, &inner, fn, grid, dim3(kTPB), smem);
+  if (rc) return rc;
+  *prev = n;
+  return 0;
+}
+
+int build_graph(lemgpu_ctx* ctx) {
+  StepArgs& a = ctx->a;
+  cudaGraph_t g;
+  CU(ctx, cudaGraphCreate(&g, 0));
+  ctx->graph = g;
+  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
+  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
+  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
+  const int nk = a.nkind;
+  const void* fk1 = a.conn == 8 ? (const void*)k_recv_donor<8> : (const void*)k_recv_donor<4>;
+  const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
+  const void* fde = nk == 1 ? (const void*)k_deep_erode<1> : nk == 2 ? (const void*)k_deep_erode<2> : (const void*)k_deep_erode<0>;
+  cudaGraphNode_t prev = nullptr;
+  int rc;
+  const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+  if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, true)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_count, dim3(ctx->scan_grid), dim3(kTPB), 0)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0)) ||
+      (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(ctx->scan_grid), 0)) ||
+      (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0)) ||
+      (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0)) ||
+      (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0)))
+    return rc;
+  CU(ctx, cudaGraphInstantiate(&ctx->exec, g, 0));
+  return 0;
+}
+
 int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_params* p,
                 const lemgpu_member* per_member, lemgpu_ctx** out) {
   *out = nullptr;
@@ -191,7 +265,6 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.eps = p->epsilon;
   a.dist_one = 0;
   for (int k = 0; k < 8; ++k) {
-    a.off[k] = dir_oy(k) * (int)W + dir_ox(k);
     a.dist[k] = offset_length(dir_ox(k), dir_oy(k), p->dx, p->dy);
     if (a.dist[k] == 1.0) a.dist_one |= 1u << k;
   }
@@ -206,13 +279,18 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if (lut_entries < 2) lut_entries = 2;
   a.lut_entries = lut_entries;
 
-  // host-libm tables (bit-identical with the reference's pow on this host)
-  std::vector<double> kdt(M), mexp(M), lut((size_t)M * lut_entries);
+  // host-libm tables (bit-identical with the reference's pow on this host):
+  // F(a, class) = ((K*dt) * pow(a*w0, m)) / pow(dist_class, n), the exact
+  // rounding sequence of erode_one_cell (erosion.cpp:38-39)
+  std::vector<double> kdt(M), mexp(M), lut((size_t)M * 3 * lut_entries);
+  const double pdc[3] = {a.powdist_h, a.powdist_v, a.powdist_d};
   for (uint32_t m = 0; m < M; ++m) {
     kdt[m] = ctx->members[m].K * p->dt;  // erosion.cpp:38: K * dt first
     mexp[m] = ctx->members[m].m_exp;
-    double* row = lut.data() + (size_t)m * lut_entries;
-    for (uint32_t i = 0; i < lut_entries; ++i) row[i] = std::pow((double)i * a.w0, mexp[m]);
+    for (uint32_t i = 0; i < lut_entries; ++i) {
+      const double kp = kdt[m] * std::pow((double)i * a.w0, mexp[m]);
+      for (int c = 0; c < 3; ++c) lut[((size_t)m * 3 + c) * lut_entries + i] = kp / pdc[c];
+    }
   }
 
   int rc;
@@ -224,12 +302,15 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
       (rc = dmalloc(ctx, &a.cbound, ((size_t)N / kChunkRoots + 2) * kCBS)) ||
       (rc = dmalloc(ctx, &a.Aq, N)) || (rc = dmalloc(ctx, &a.hq, N)) ||
       (rc = dmalloc(ctx, &a.levels, (size_t)N + 2)) ||
-      (rc = dmalloc(ctx, &a.tstat, (size_t)N / kExTile + 2)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
+      (rc = dmalloc(ctx, &a.pdm, N)) || (rc = dmalloc(ctx, &a.part, 4096)) ||
+      (rc = dmalloc(ctx, &a.bins, 3 * 4096)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
       (rc = dmalloc(ctx, &ctx->d_diag, ctx->diag_cap)))
     return bail(rc);
   a.kdt = ctx->d_kdt;
   a.mexp = ctx->d_mexp;
-  a.lut = ctx->d_lut;
+  a.ftab = ctx->d_lut;
+  a.cb_stride = N / kChunkRoots + 2;
+  a.diag = ctx->d_diag;
 #define CUB(call)                          \
   do {                                     \
     if ((call) != cudaSuccess) {           \
@@ -243,59 +324,130 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   CUB(cudaMemset(a.h, 0, (size_t)N * sizeof(double)));
   CUB(cudaMemset(a.rcode, 0, (size_t)N + 16));
   CUB(cudaMemset(a.dmask, 0, (size_t)N + 16));
-  CUB(cudaMemset(a.tstat, 0, ((size_t)N / kExTile + 2) * 8));
+  CUB(cudaMemset(a.bins, 0, 3 * 4096 * sizeof(uint32_t)));
   Ctl c0{};
-  c0.epoch = 1;
   c0.err_cell = LEMGPU_NOFLOW;
   c0.t_k1_begin = ~0ull;
   c0.t_k1_end = 0;
   CUB(cudaMemcpy(a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
 
-  // one persistent CTA set: every CTA must be co-resident (cooperative launch)
-  int per_sm = 0;
-  const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
-  for (const void* f : {(const void*)k_flow<0>, (const void*)k_flow<1>, (const void*)k_flow<2>})
-    CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmemBytes));
-  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kTPB, kFlowSmemBytes));
-  if (per_sm < 1) {
-    fail(ctx, LEMGPU_ECUDA, "k_flow cannot be resident");
-    return bail(LEMGPU_ECUDA);
+  // launch geometry
+  int occ = 0;
+  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kTPB, 0));
+  ctx->scan_grid = (occ > 0 ? occ : 1) * nsm;
+  if (ctx->scan_grid > 4096) ctx->scan_grid = 4096;  // part/bins capacity
+  a.eager = 0;
+  if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
+  const void* fchunks = a.nkind == 1 ? (const void*)k_chunks<1> : a.nkind == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
+  CUB(cudaFuncSetAttribute(fchunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmemBytes));
+  CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fchunks, kChunkTPB, kChunksSmemBytes));
+  ctx->chunk_grid = (occ > 0 ? occ : 1) * nsm;
+  ctx->deep_grid = 8 * nsm;
+  a.scan_grid = ctx->scan_grid;
+  // TMA descriptor of h: rows of W doubles, box = one k_recv_donor halo tile.
+  // The row pitch must be a multiple of 16 bytes (even W); otherwise the
+  // kernel stages h with plain loads.
+  a.use_tma = 0;
+  if ((W % 2) == 0 && !std::getenv("LEMGPU_NO_TMA")) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
+      auto encode = reinterpret_cast<CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill)>(fn);
+      const cuuint64_t gdim[2] = {W, (cuuint64_t)H * M};
+      const cuuint64_t gstride[1] = {(cuuint64_t)W * sizeof(double)};
+      const cuuint32_t box[2] = {kBX + 4, kBY + 4};
+      const cuuint32_t estr[2] = {1, 1};
+      if (encode(&ctx->hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.h, gdim, gstride, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        a.use_tma = 1;
+    }
   }
-  ctx->flow_grid = per_sm * nsm;
-  if (const char* env = std::getenv("LEMGPU_FLOW_CTAS_PER_SM")) {
-    const int want = std::atoi(env);
-    if (want >= 1 && want <= per_sm) ctx->flow_grid = want * nsm;
+  {
+    const int rcg = build_graph(ctx);
+    if (rcg) return bail(rcg);
   }
   *out = ctx;
   return LEMGPU_OK;
 #undef CUB
 }
 
+// Eager (profiling) mode: the same kernels launched one by one; the loop
+// conditions come back through the control block, one small D2H per level.
+// ncu cannot profile kernel nodes of graphs with conditional nodes.
+int enqueue_step_eager(lemgpu_ctx* ctx) {
+  StepArgs& a = ctx->a;
+  cudaStream_t st = ctx->stream;
+  const int nk = a.nkind;
+  const unsigned one = 1, zero = 0;
+  const size_t co = offsetof(Ctl, cond);
+  char* cbase = reinterpret_cast<char*>(a.ctl) + co;
+  CU(ctx, cudaMemcpyAsync(cbase, &one, 4, cudaMemcpyHostToDevice, st));
+  CU(ctx, cudaMemcpyAsync(cbase + 4, &zero, 4, cudaMemcpyHostToDevice, st));
+  CU(ctx, cudaMemcpyAsync(cbase + 8, &zero, 4, cudaMemcpyHostToDevice, st));
+  const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+  if (a.conn == 8)
+    k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap);
+  else
+    k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap);
+  k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+  k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+  unsigned cond[3] = {1, 0, 0};
+  while (cond[0]) {
+    k_expand<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+    CU(ctx, cudaStreamSynchronize(st));
+  }
+  if (nk == 1)
+    k_chunks<1><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
+  else if (nk == 2)
+    k_chunks<2><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
+  else
+    k_chunks<0><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
+  k_deep_prep<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+  while (cond[1]) {
+    k_deep_accum<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+    CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+    CU(ctx, cudaStreamSynchronize(st));
+  }
+  while (cond[2]) {
+    if (nk == 1)
+      k_deep_erode<1><<<ctx->deep_grid, kTPB, 0, st>>>(a);
+    else if (nk == 2)
+      k_deep_erode<2><<<ctx->deep_grid, kTPB, 0, st>>>(a);
+    else
+      k_deep_erode<0><<<ctx->deep_grid, kTPB, 0, st>>>(a);
+    CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+    CU(ctx, cudaStreamSynchronize(st));
+  }
+  k_deep_final<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+  k_finalize<<<1, 32, 0, st>>>(a);
+  CU(ctx, cudaGetLastError());
+  return LEMGPU_OK;
+}
+
 int enqueue_step(lemgpu_ctx* ctx) {
-  StepArgs a = ctx->a;
   if (ctx->pending >= ctx->diag_cap) return fail(ctx, LEMGPU_EOTHER, "too many steps pending");
-  a.diag = ctx->d_diag + ctx->pending;
   cudaEvent_t* ev = nullptr;
   if (ctx->timing) {
-    while (ctx->ev.size() < 3 * (size_t)(ctx->pending + 1)) {
+    while (ctx->ev.size() < 2 * (size_t)(ctx->pending + 1)) {
       cudaEvent_t e;
       CU(ctx, cudaEventCreate(&e));
       ctx->ev.push_back(e);
     }
-    ev = &ctx->ev[3 * ctx->pending];
+    ev = &ctx->ev[2 * ctx->pending];
     CU(ctx, cudaEventRecord(ev[0], ctx->stream));
   }
-  const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-  if (a.conn == 8)
-    k_recv_donor<8><<<g1, kTPB, 0, ctx->stream>>>(a);
-  else
-    k_recv_donor<4><<<g1, kTPB, 0, ctx->stream>>>(a);
-  CU(ctx, cudaGetLastError());
+  if (ctx->a.eager) {
+    const int rc = enqueue_step_eager(ctx);
+    if (rc) return rc;
+  } else {
+    CU(ctx, cudaGraphLaunch(ctx->exec, ctx->stream));
+  }
   if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
-  void* args[] = {&a};
-  const void* fk = a.nkind == 1 ? (const void*)k_flow<1> : a.nkind == 2 ? (const void*)k_flow<2> : (const void*)k_flow<0>;
-  CU(ctx, cudaLaunchCooperativeKernel(fk, dim3(ctx->flow_grid), dim3(kTPB), args, kFlowSmemBytes, ctx->stream));
-  if (ev) CU(ctx, cudaEventRecord(ev[2], ctx->stream));
   ++ctx->pending;
   ctx->have_graph = true;
   return LEMGPU_OK;
@@ -324,11 +476,13 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
   void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, a.h,   a.rcode,  a.dmask, a.order,
-                  a.ppos,     a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.tstat,
+                  a.ppos,     a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -413,15 +567,17 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
   if (n) CU(ctx, cudaMemcpy(d.data(), ctx->d_diag, n * sizeof(lemgpu_diag), cudaMemcpyDeviceToHost));
   if (ctx->timing && n) {
     for (uint32_t s = 0; s < n; ++s) {
-      float t1 = 0, t2 = 0;
-      cudaEventElapsedTime(&t1, ctx->ev[3 * s], ctx->ev[3 * s + 1]);
-      cudaEventElapsedTime(&t2, ctx->ev[3 * s + 1], ctx->ev[3 * s + 2]);
-      ctx->kernel_ms[0] += t1;
-      ctx->kernel_ms[1] += t2;
+      float t = 0;
+      cudaEventElapsedTime(&t, ctx->ev[2 * s], ctx->ev[2 * s + 1]);
+      ctx->kernel_ms[0] += t;
+      ctx->kernel_ms[1] += d[s].seconds[LEMGPU_PHASE_RECEIVERS] * 1e3;
+      ctx->kernel_ms[2] += d[s].seconds[LEMGPU_PHASE_ORDER] * 1e3;
+      ctx->kernel_ms[3] += d[s].seconds[LEMGPU_PHASE_EROSION] * 1e3;
     }
     ctx->kernel_launches += n;
   }
   ctx->pending = 0;
+  if (n) CU(ctx, cudaMemset(reinterpret_cast<char*>(ctx->a.ctl) + offsetof(Ctl, slot), 0, sizeof(uint32_t)));
   int status = LEMGPU_OK;
   for (uint32_t s = 0; s < n; ++s) {
     if (d[s].status != 0) {
@@ -440,8 +596,7 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
       CU(ctx, cudaMemcpy(&c0, ctx->a.ctl, sizeof c0, cudaMemcpyDeviceToHost));
       c0.err_flag = 0;
       c0.err_cell = LEMGPU_NOFLOW;
-      c0.t_k1_begin = ~0ull;
-      c0.t_k1_end = 0;
+      c0.slot = 0;
       CU(ctx, cudaMemcpy(ctx->a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
       break;
     }
@@ -546,15 +701,14 @@ int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable) {
     if (rc) return rc;
   }
   ctx->timing = enable != 0;
-  ctx->kernel_ms[0] = ctx->kernel_ms[1] = 0;
+  for (double& v : ctx->kernel_ms) v = 0;
   ctx->kernel_launches = 0;
   return LEMGPU_OK;
 }
 
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches) {
   if (!ctx || !ms) return LEMGPU_ECONFIG;
-  ms[0] = ctx->kernel_ms[0];
-  ms[1] = ctx->kernel_ms[1];
+  for (int i = 0; i < 4; ++i) ms[i] = ctx->kernel_ms[i];
   if (launches) *launches = ctx->kernel_launches;
   return LEMGPU_OK;
 }
@@ -565,8 +719,8 @@ int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t*
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   Ctl c{};
   CU(ctx, cudaMemcpy(&c, ctx->a.ctl, sizeof c, cudaMemcpyDeviceToHost));
-  const uint32_t n = c.ntl < cap ? c.ntl : cap;
-  for (uint32_t i = 0; i < n; ++i) ns[i] = c.tl[i];
+  const uint32_t n = c.nltl < cap ? c.nltl : cap;
+  for (uint32_t i = 0; i < n; ++i) ns[i] = c.ltl[i];
   if (count) *count = n;
   return LEMGPU_OK;
 }

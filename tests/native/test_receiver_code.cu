@@ -10,7 +10,7 @@
 #include <cstdint>
 #include <random>
 
-#include "../../paper_1803_02977_b200/csrc/lemgpu_kernels.cuh"
+#include "../../paper_1803_02977_b200/csrc/k_recv_donor.cuh"
 
 using namespace lemgpu;
 
