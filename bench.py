@@ -120,16 +120,17 @@ class ClockSampler:
 
 
 def member_table(workload, rank, world):
-    """Member ids / seeds / (K, m) owned by this rank."""
+    """Member ids / seeds / (K, m) owned by this rank (paper_1803_02977_b200.ensemble)."""
+    from paper_1803_02977_b200 import ensemble
+
     wl = WORKLOADS[workload]
     if wl["members"] == 1:
-        # replicas only: one realisation per rank
-        return [rank], [42 + rank], [(2e-6, 0.5)]
+        # replicas only: one independent 10000^2 realisation per rank
+        return [rank], [42 + rank], [(2e-6, 0.5)], world
     M = wl["members"]
-    ids = [i for i in range(M) if i * world // M == rank] if M >= world else [rank % M]
-    seeds = [1000 + i for i in ids]
-    km = [(1e-6 * (1 + i % 8), 0.35 + 0.05 * (i // 8)) for i in ids]
-    return ids, seeds, km
+    ids = ensemble.member_ids(M, world, rank)
+    ps = [ensemble.member_params(i) for i in ids]
+    return ids, [p[0] for p in ps], [(p[1], p[2]) for p in ps], M
 
 
 def traffic_from_profiles(workload):
@@ -238,7 +239,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.workload]
     w, h = wl["w"], wl["h"]
-    ids, seeds, km = member_table(args.workload, rank, world)
+    ids, seeds, km, members_total = member_table(args.workload, rank, world)
     M = len(ids)
     params = lem.SimParams(n_exp=wl["n_exp"])
     ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M,
@@ -247,18 +248,17 @@ def main():
     cells = w * h * M
     ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     ens = world > 1 or wl["members"] > 1
-    stats = torch.zeros(4 * max(M, 1), dtype=torch.float64, device=f"cuda:{local}")
-    gstats = torch.zeros(4, dtype=torch.float64, device=f"cuda:{local}")
+    stats = torch.zeros(max(M, 1), 4, dtype=torch.float64, device=f"cuda:{local}")
+    from paper_1803_02977_b200 import ensemble
 
     def one_step():
         ctx.step_async(1)
         if ens:
-            # per-member statistics epilogue + NCCL reduction
+            # per-member statistics + NCCL reduction of the [members, 4] table
             ctx.member_stats_device(stats.data_ptr())
             if world > 1:
                 with torch.cuda.stream(ext):
-                    gstats.copy_(stats.view(M, 4).sum(0))
-                    dist.all_reduce(gstats)
+                    ensemble.reduce_member_stats(stats, ids, members_total)
 
     # ---- warm-up
     for _ in range(args.warmup):

@@ -1,0 +1,186 @@
+// lem_rb_gpu.cpp -- see lem_rb_gpu.hpp.  Host-only C++ over the C-ABI.
+#include "lem_rb_gpu.hpp"
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include <lem/error.hpp>
+#include <lem/neighborhood.hpp>
+
+#include "lemgpu.h"
+
+namespace lem::gpu {
+namespace {
+
+struct Ctx {
+  lemgpu_ctx* h = nullptr;
+  int w = 0, hgt = 0, conn = 0, device = 0;
+  SimParams params{};
+  ~Ctx() {
+    if (h) lemgpu_destroy(h);
+  }
+};
+
+std::mutex g_mu;
+std::unordered_map<const SimWorkspace*, std::unique_ptr<Ctx>>& table() {
+  static std::unordered_map<const SimWorkspace*, std::unique_ptr<Ctx>> t;
+  return t;
+}
+
+// ErrorCollector::rethrow mapping (scheduler.cpp:45-49).
+[[noreturn]] void raise(int status, const std::string& msg, std::uint32_t cell) {
+  switch (status) {
+    case LEMGPU_ECONFIG:
+      throw ConfigError(msg);
+    case LEMGPU_ESTRUCTURE:
+      throw StructureError(msg);
+    case LEMGPU_ECONVERGENCE:
+      throw ConvergenceError(cell, msg);
+    default:
+      throw Error(msg);
+  }
+}
+
+void check(lemgpu_ctx* h, int rc) {
+  if (rc != LEMGPU_OK) raise(rc, lemgpu_error_message(h), lemgpu_error_cell(h));
+}
+
+lemgpu_params to_abi(const SimParams& p, int connectivity) {
+  lemgpu_params q{};
+  q.K = p.K;
+  q.m_exp = p.m_exp;
+  q.n_exp = p.n_exp;
+  q.uplift_rate = p.uplift_rate;
+  q.dt = p.dt;
+  q.epsilon = p.epsilon;
+  q.dx = p.dx;
+  q.dy = p.dy;
+  q.max_newton_iters = p.max_newton_iters;
+  q.connectivity = connectivity;
+  return q;
+}
+
+bool same(const SimParams& a, const SimParams& b) {
+  return a.K == b.K && a.m_exp == b.m_exp && a.n_exp == b.n_exp && a.uplift_rate == b.uplift_rate &&
+         a.dt == b.dt && a.epsilon == b.epsilon && a.dx == b.dx && a.dy == b.dy &&
+         a.max_newton_iters == b.max_newton_iters;
+}
+
+std::unique_ptr<Ctx> make_ctx(int w, int h, int conn, const SimParams& p, int device) {
+  auto c = std::make_unique<Ctx>();
+  const lemgpu_params q = to_abi(p, conn);
+  const int rc = lemgpu_create(device, static_cast<std::uint32_t>(w), static_cast<std::uint32_t>(h), &q, &c->h);
+  if (rc != LEMGPU_OK) raise(rc, lemgpu_error_message(nullptr), kNoFlow);
+  c->w = w;
+  c->hgt = h;
+  c->conn = conn;
+  c->device = device;
+  c->params = p;
+  return c;
+}
+
+Ctx& ctx_for(SimWorkspace& ws, const GridGraph& g, const SimParams& p, int device) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto& slot = table()[&ws];
+  const int conn = g.neighborhood().connectivity;
+  if (!slot || slot->w != g.width() || slot->hgt != g.height() || slot->conn != conn ||
+      slot->device != device || !same(slot->params, p))
+    slot = make_ctx(g.width(), g.height(), conn, p, device);
+  return *slot;
+}
+
+StepDiagnostics to_diag(const lemgpu_diag& d) {
+  StepDiagnostics out;
+  for (int i = 0; i < kNumPhases; ++i) out.timings.seconds[i] = d.seconds[i];
+  out.newton_iters = d.newton_iters;
+  out.interior_noflow = d.interior_noflow;
+  return out;
+}
+
+void check_setup(const StepSetup& setup) {
+  // the device path is the D8/D4 queue plan (like rb_private_queues'
+  // routing restriction, scheduler.cpp:413-416)
+  if (setup.routing == Routing::kMfd) throw ConfigError("rb_gpu requires single-receiver (d8/d4) routing");
+  if (setup.order == OrderKind::kStack) throw ConfigError("rb_gpu uses the breadth-first queue order");
+}
+
+}  // namespace
+
+StepDiagnostics strategy_step_rb_gpu(Raster<double>& elev, const GridGraph& grid, const SimParams& params,
+                                     const StepSetup& setup, SimWorkspace& ws, int device) {
+  check_setup(setup);
+  params.validate();
+  Ctx& c = ctx_for(ws, grid, params, device);
+  lemgpu_diag d{};
+  check(c.h, lemgpu_step_host(c.h, elev.storage().data(), &d));
+  return to_diag(d);
+}
+
+RunResult run_simulation_rb_gpu(Raster<double> initial, const RunConfig& cfg, const StepCallback& on_step,
+                                int device) {
+  cfg.validate();
+  if (initial.width() != static_cast<int>(cfg.width) || initial.height() != static_cast<int>(cfg.height))
+    throw ConfigError("initial raster is " + std::to_string(initial.width()) + "x" +
+                      std::to_string(initial.height()) + " but config says " + std::to_string(cfg.width) + "x" +
+                      std::to_string(cfg.height));
+  StepSetup setup;
+  setup.routing = cfg.routing;
+  check_setup(setup);
+  auto c = make_ctx(initial.width(), initial.height(), cfg.connectivity, cfg.params, device);
+  check(c->h, lemgpu_upload_elev(c->h, initial.storage().data()));  // rejects non-finite input
+  RunResult res;
+  res.elevation = std::move(initial);
+  res.per_step.reserve(cfg.timesteps);
+  if (!on_step) {
+    std::vector<lemgpu_diag> d(cfg.timesteps);
+    if (cfg.timesteps) check(c->h, lemgpu_step(c->h, cfg.timesteps, d.data()));
+    for (const auto& x : d) res.per_step.push_back(to_diag(x));
+  } else {
+    for (std::uint32_t s = 1; s <= cfg.timesteps; ++s) {
+      lemgpu_diag d{};
+      check(c->h, lemgpu_step(c->h, 1, &d));
+      check(c->h, lemgpu_download_elev(c->h, res.elevation.storage().data()));
+      StepDiagnostics sd = to_diag(d);
+      on_step(s, res.elevation, sd);
+      res.per_step.push_back(std::move(sd));
+    }
+  }
+  check(c->h, lemgpu_download_elev(c->h, res.elevation.storage().data()));
+  for (const auto& d : res.per_step) {
+    res.phase_totals += d.timings;
+    res.newton_iters += d.newton_iters;
+    res.interior_noflow_last = d.interior_noflow;
+  }
+  return res;
+}
+
+void fill_workspace(SimWorkspace& ws) {
+  Ctx* c = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = table().find(&ws);
+    if (it == table().end() || !it->second) throw ConfigError("no rb_gpu step has run in this workspace");
+    c = it->second.get();
+  }
+  const std::size_t n = static_cast<std::size_t>(c->w) * c->hgt;
+  ws.fg.resize(c->w, c->hgt, c->conn);
+  std::vector<std::uint32_t> levels(n + 2);
+  std::uint32_t nl = 0;
+  ws.accum.values = Raster<double>(c->w, c->hgt);
+  ws.accum.cell_area = c->params.cell_area();
+  ws.plan.order.resize(n);
+  check(c->h, lemgpu_download_graph(c->h, ws.fg.rec.data(), ws.fg.dnum.data(), ws.fg.donor.data(),
+                                    ws.plan.order.data(), levels.data(), &nl,
+                                    ws.accum.values.storage().data()));
+  ws.plan.levels.assign(levels.begin(), levels.begin() + nl + 1);
+}
+
+void release_workspace(SimWorkspace& ws) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  table().erase(&ws);
+}
+
+}  // namespace lem::gpu

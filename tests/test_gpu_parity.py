@@ -279,3 +279,17 @@ def test_strategy_step_and_run_simulation_dropin(oracle):
     seen = []
     lem.run_simulation(oracle.terrain(w, h, 11), cfg, on_step=lambda s, r, d: seen.append((s, float(r.sum()))))
     assert [s for s, _ in seen] == list(range(1, 11))
+
+
+def test_cpp_dropin_through_reference_api():
+    """The reference's own C++ API (run_simulation / strategy_step / SimWorkspace)
+    driving the rb_gpu shim, byte-compared with the reference strategies."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "test_dropin"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/test_dropin not built (needs /root/reference at build time)")
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failure(s)" in out.stdout
