@@ -38,11 +38,12 @@ constexpr int kBY = 32;
 // scan tiles
 constexpr int kL0IPT = 16;              // level-0 cells per thread (one uint4 of rcodes)
 constexpr int kL0Tile = kTPB * kL0IPT;  // 4096 cells
-constexpr int kExIPT = 4;               // frontier items per thread
-constexpr int kExTile = kTPB * kExIPT;  // 1024 frontier cells
+constexpr int kExIPT = 2;               // frontier items per thread
+constexpr int kExTile = kTPB * kExIPT;  // 512 frontier cells
 // source chunks of the physics sweeps
-constexpr int kChunkRoots = 32;       // level-0 sources per chunk (one warp each)
-constexpr int kChunkCap = 512;        // cells per chunk held in shared memory
+constexpr int kChunkRoots = 24;       // level-0 sources per chunk (one warp each)
+constexpr int kChunkCap = 384;        // cells per chunk held in shared memory
+constexpr int kChunkSlots = kChunkCap / 32;  // cells per lane
 constexpr int kChunkTPB = 128;        // k_chunks CTA: 4 warps, 4 chunks in flight
 constexpr int kChunkMaxLevels = 24;   // shallow (chunked) plans: nlevels <= this
 constexpr int kCBS = kChunkMaxLevels + 1;
@@ -129,7 +130,8 @@ struct StepArgs {
   uint8_t* rcode;
   uint8_t* dmask;
   uint32_t* order;
-  uint32_t* ppos;
+  uint32_t* ppos;     // position-major: queue position of the receiver (levels >= 1)
+  uint8_t* cdir;      // position-major: stencil direction receiver -> cell (levels >= 1)
   uint32_t* fc;
   uint32_t* cbound;  // [level][chunk]: first position of a source chunk at each level
   uint32_t cb_stride;
@@ -142,6 +144,7 @@ struct StepArgs {
   uint32_t scan_grid;  // CTAs of the scan kernels (segments per level)
   int eager;          // 1: no graph; loop conditions go through ctl->cond
   int use_tma;        // k_recv_donor stages h with one TMA box per tile
+  int force_deep;     // testing: use the per-level sweeps even for shallow plans
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
   cudaGraphConditionalHandle h_expand, h_dacc, h_deros;

@@ -34,7 +34,8 @@ struct ScanSmem {
   uint32_t base;
   uint32_t ord[kExTile];
   uint8_t dm[kExTile];
-  uint32_t kids[kKidCap];
+  uint32_t kids[kKidCap];   // child cells of the tile, in queue order
+  uint16_t kpk[kKidCap];    // (tile-local parent index << 3) | direction parent -> child
 };
 
 // Sum of v over the first `upto` entries of bins[] (one CTA, all threads);
@@ -82,8 +83,9 @@ __device__ __forceinline__ void bin_add(uint32_t* bins, uint32_t bin, uint32_t v
 // loads in flight per thread) and the per-segment child counts of the next
 // sweep (segments of Sn positions starting at `base`).
 template <bool KIDS>
-__device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* kids, uint32_t p0, uint32_t p1,
-                                             uint32_t base, uint32_t Sn, uint32_t* bins) {
+__device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* kids, const uint16_t* kpk,
+                                             uint32_t tb, uint32_t p0, uint32_t p1, uint32_t base, uint32_t Sn,
+                                             uint32_t* bins) {
   uint32_t cur_bin = 0xFFFFFFFFu, cur_end = 0, sum = 0;
   for (uint32_t pb = p0 + threadIdx.x; pb < p1; pb += 4 * kTPB) {
     uint32_t cm[4];
@@ -94,7 +96,10 @@ __device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* 
         uint32_t child;
         if (KIDS) {
           child = kids[p - p0];
+          const uint32_t pk = kpk[p - p0];
           a.order[p] = child;
+          a.ppos[p] = tb + (pk >> 3);
+          a.cdir[p] = (uint8_t)(pk & 7u);
         } else {
           child = a.order[p];
         }
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kTPB) k_l0_write(StepArgs a) {
       }
     }
     __syncthreads();  // this tile's queue entries are visible to the whole CTA
-    pdm_and_bins<false>(a, nullptr, first, first + tot, 0u, Sb, a.bins);
+    pdm_and_bins<false>(a, nullptr, nullptr, 0u, first, first + tot, 0u, Sb, a.bins);
   }
   if (last_block_done(ctl) && threadIdx.x == 0) {
     a.levels[0] = 0;
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
           mm &= mm - 1;
           const uint32_t child = (uint32_t)((int)c[j] + dir_off(k, (int)W));
           sm.kids[out - first] = child;
+          sm.kpk[out - first] = (uint16_t)(((threadIdx.x * kExIPT + j) << 3) | k);
           ++out;
         }
       }
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
         const uint32_t p = tb + j * kTPB + threadIdx.x;
         if (p < s1) a.fc[p] = sm.ord[j * kTPB + threadIdx.x];
       }
-      pdm_and_bins<true>(a, sm.kids, first, first + tot, hi, Sn, bins_out);
+      pdm_and_bins<true>(a, sm.kids, sm.kpk, tb, first, first + tot, hi, Sn, bins_out);
       __syncthreads();
     }
   }
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
     } else {
       // plan complete: nlevels = l + 1 (traversal.cpp:45); cycle check (:46)
       ctl->nlev = l + 1;
-      uint32_t mode = l + 1 <= (uint32_t)kChunkMaxLevels ? kModeShallow : kModeDeep;
+      uint32_t mode = (l + 1 <= (uint32_t)kChunkMaxLevels && !a.force_deep) ? kModeShallow : kModeDeep;
       if (!err && hi != a.N) {
         ctl->err_flag = LEMGPU_ESTRUCTURE;
         ctl->err_cell = hi;  // cells placed

@@ -297,7 +297,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if ((rc = dmalloc(ctx, &ctx->d_kdt, M)) || (rc = dmalloc(ctx, &ctx->d_mexp, M)) ||
       (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &a.h, N)) ||
       (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
-      (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) ||
+      (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
       (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) ||
       (rc = dmalloc(ctx, &a.cbound, ((size_t)N / kChunkRoots + 2) * kCBS)) ||
       (rc = dmalloc(ctx, &a.Aq, N)) || (rc = dmalloc(ctx, &a.hq, N)) ||
@@ -337,6 +337,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->scan_grid = (occ > 0 ? occ : 1) * nsm;
   if (ctx->scan_grid > 4096) ctx->scan_grid = 4096;  // part/bins capacity
   a.eager = 0;
+  a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
   const void* fchunks = a.nkind == 1 ? (const void*)k_chunks<1> : a.nkind == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   CUB(cudaFuncSetAttribute(fchunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmemBytes));
@@ -476,7 +477,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
   void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, a.h,   a.rcode,  a.dmask, a.order,
-                  a.ppos,     a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
+                  a.ppos,     a.cdir,      a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);

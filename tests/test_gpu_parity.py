@@ -293,3 +293,25 @@ def test_cpp_dropin_through_reference_api():
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failure(s)" in out.stdout
+
+
+@pytest.mark.parametrize("w,h,seed,kw", [(300, 200, 21, {}), (64, 64, 22, {"n_exp": 2.0}), (90, 61, 23, {"dx": 0.5})])
+def test_per_level_sweeps_match_chunked(oracle, monkeypatch, w, h, seed, kw):
+    """The deep-plan schedule (one kernel per level, global scratch) forced on a
+    shallow plan gives the same bits as the chunked schedule and the oracle."""
+    monkeypatch.setenv("LEMGPU_FORCE_DEEP", "1")
+    deep = device_ctx(w, h, **kw)
+    monkeypatch.delenv("LEMGPU_FORCE_DEEP")
+    chunked = device_ctx(w, h, **kw)
+    e = oracle.terrain(w, h, seed)
+    deep.upload(e)
+    chunked.upload(e)
+    p = make_params(**kw)
+    for _ in range(5):
+        dd = deep.step(1)[0]
+        dc = chunked.step(1)[0]
+        o = oracle.step(e, params=p)
+        hd, hc = deep.download(), chunked.download()
+        assert np.array_equal(hd.view(np.uint64), hc.view(np.uint64))
+        assert dd.newton_iters == dc.newton_iters
+        compare_step(deep, o, hd, e, exact_h=kw.get("n_exp", 1.0) == 1.0, tag="deep")
