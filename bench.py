@@ -57,6 +57,16 @@ def env_int(k, d):
         return d
 
 
+def host_threads():
+    """All host cores this process may use (torchrun sets OMP_NUM_THREADS=1, so
+    the OpenMP default is not used: the reference's strategies take an explicit
+    worker count, scheduler.cpp:365)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -157,7 +167,7 @@ def cpu_baseline_reference(workload, budget_s=30.0):
     if not RefLib.available():
         return None
     ref = RefLib.get()
-    threads = ref.max_threads()
+    threads = host_threads()
     p = make_params(n_exp=wl["n_exp"])
     # bounded sample: ~budget_s of CPU work, at least 2 timed steps after 1 warm-up
     est = 3e-8 * w * h * 16 / max(threads, 1)  # ~3 s per 10000^2 step on 16 cores
@@ -184,7 +194,7 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblemref.so not built"}))
         return 0
     ref = RefLib.get()
-    threads = ref.max_threads()
+    threads = host_threads()
     p = make_params(n_exp=wl["n_exp"])
     members = wl["members"]
     # one "step" = one timestep of the whole workload; for the ensemble, a
@@ -233,10 +243,17 @@ def main():
     import paper_1803_02977_b200 as lem
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    # one process per GPU; LEMGPU_BENCH_BACKEND=gloo lets several ranks share
+    # one device to exercise the multi-rank path on a single-GPU box
+    backend = os.environ.get("LEMGPU_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     wl = WORKLOADS[args.workload]
     w, h = wl["w"], wl["h"]
     ids, seeds, km, members_total = member_table(args.workload, rank, world)
@@ -357,7 +374,7 @@ def main():
         "scaling": "weak" if wl["members"] == 1 else "strong",
         "vs_baseline": value / PAPER_P100 if (args.workload == "dem10000" and world == 1) else None,
         "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM generated on device, bit-exact lem::generate_terrain)",
-        "config": {"workload": wl["desc"] + (" -- one independent replica per GPU, per-step NCCL stats all-reduce"
+        "config": {"workload": wl["desc"] + (f" -- one independent replica per GPU, per-step {backend} stats all-reduce"
                                              if (world > 1 and wl["members"] == 1) else ""),
                    "grid": [w, h], "members_per_gpu": M, "params": "K=2e-6 m=0.5 n=%g u=2e-3 dt=1000 eps=1e-6" % wl["n_exp"],
                    "parallelism": f"replicas{world}" if wl["members"] == 1 else f"members/{world}",

@@ -41,8 +41,13 @@ constexpr int kL0Tile = kTPB * kL0IPT;  // 4096 cells
 constexpr int kExIPT = 2;               // frontier items per thread
 constexpr int kExTile = kTPB * kExIPT;  // 512 frontier cells
 // source chunks of the physics sweeps
-constexpr int kChunkRoots = 24;       // level-0 sources per chunk (one warp each)
-constexpr int kChunkCap = 384;        // cells per chunk held in shared memory
+#ifndef LEMGPU_CHUNK_ROOTS
+#define LEMGPU_CHUNK_ROOTS 16  // measured best of {16,24,32,40,48} at 10000^2 (occupancy-bound)
+#define LEMGPU_CHUNK_CAP 256
+#define LEMGPU_CHUNK_MINB 8
+#endif
+constexpr int kChunkRoots = LEMGPU_CHUNK_ROOTS;  // level-0 sources per chunk (one warp each)
+constexpr int kChunkCap = LEMGPU_CHUNK_CAP;      // cells per chunk held in shared memory
 constexpr int kChunkSlots = kChunkCap / 32;  // cells per lane
 constexpr int kChunkTPB = 128;        // k_chunks CTA: 4 warps, 4 chunks in flight
 constexpr int kChunkMaxLevels = 24;   // shallow (chunked) plans: nlevels <= this

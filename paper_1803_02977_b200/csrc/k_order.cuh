@@ -259,14 +259,27 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
     const uint32_t s0 = lo + min(b * S, hi - lo), s1 = lo + min((b + 1) * S, hi - lo);
     uint32_t carry = hi + pre;
     const uint32_t W = a.W;
+    // register double buffer: the next tile's cells and masks are in flight
+    // while the current tile is scanned and expanded
+    uint32_t nc[kExIPT], nm[kExIPT];
+#pragma unroll
+    for (int j = 0; j < kExIPT; ++j) {
+      const uint32_t p = s0 + j * kTPB + threadIdx.x;
+      nc[j] = p < s1 ? a.order[p] : 0u;
+      nm[j] = p < s1 ? a.pdm[p] : 0u;
+    }
     for (uint32_t tb = s0; tb < s1; tb += kExTile) {
       // coalesced staging of the tile's cells and donor masks
 #pragma unroll
       for (int j = 0; j < kExIPT; ++j) {
-        const uint32_t p = tb + j * kTPB + threadIdx.x;
-        const bool in = p < s1;
-        sm.ord[j * kTPB + threadIdx.x] = in ? a.order[p] : 0u;
-        sm.dm[j * kTPB + threadIdx.x] = in ? a.pdm[p] : (uint8_t)0;
+        sm.ord[j * kTPB + threadIdx.x] = nc[j];
+        sm.dm[j * kTPB + threadIdx.x] = (uint8_t)nm[j];
+      }
+#pragma unroll
+      for (int j = 0; j < kExIPT; ++j) {
+        const uint32_t p = tb + kExTile + j * kTPB + threadIdx.x;
+        nc[j] = p < s1 ? a.order[p] : 0u;
+        nm[j] = p < s1 ? a.pdm[p] : 0u;
       }
       __syncthreads();
       uint32_t c[kExIPT], m[kExIPT], cnt = 0;
