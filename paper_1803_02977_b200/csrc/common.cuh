@@ -2,6 +2,9 @@
 //
 // One timestep is a CUDA graph of these kernels:
 //
+//   k_tiles             the whole step for every drainage tree rooted in a
+//                       64x32 tile whose cells stay within 3 cells of it     (k_tiles.cuh)
+//   then, for the trees that escape their tile (and for the parity export):
 //   k_recv_donor        receivers + donor bitmask, smem-staged stencil   (k_recv_donor.cuh)
 //   k_l0_count/_write   level 0 of the BFS order: stream compaction       (k_order.cuh)
 //   WHILE { k_expand }  one frontier expansion per level                  (k_order.cuh)
@@ -31,6 +34,10 @@ namespace lemgpu {
 constexpr int kTPB = 256;           // threads per CTA (all kernels)
 constexpr int kNW = kTPB / 32;      // warps per CTA
 constexpr uint8_t kNoFlowCode = 8;  // rcode value for kNoFlow
+
+// k_tiles: owned tile, BFS halo (see k_tiles.cuh)
+constexpr int kTX = 64, kTY = 32, kHalo = 3;
+constexpr int kTTPB = 256;
 
 // k_recv_donor tile (output cells): halo of 2 for h, 1 for the receiver codes.
 constexpr int kBX = 128;
@@ -102,6 +109,8 @@ struct Ctl {
   uint32_t dlvl;  // level of the deep sweeps
   uint32_t misses;
   unsigned long long newton;
+  // tile path (k_tiles): escaped roots, cells finished in tiles, interior pits, deepest level + 1
+  uint32_t nesc, tile_cells, n0i, tile_nlev;
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   uint32_t ntl, nltl;
   unsigned long long tl[96];   // debug timeline of the running step (finisher stamps)
@@ -130,8 +139,11 @@ struct StepArgs {
   const double* kdt;   // per member K*dt
   const double* mexp;  // per member m
   const double* ftab;  // per member and offset class: F(a) = (K*dt * pow(a*w0, m)) / pow(dist, n), host libm
-  // state / scratch
+  // state / scratch.  h is the elevation the step reads (never written during
+  // the step), hout the elevation it writes (ping-pong buffers; the step's
+  // receivers always see the complete previous surface)
   double* h;
+  double* hout;
   uint8_t* rcode;
   uint8_t* dmask;
   uint32_t* order;
@@ -150,6 +162,9 @@ struct StepArgs {
   int eager;          // 1: no graph; loop conditions go through ctl->cond
   int use_tma;        // k_recv_donor stages h with one TMA box per tile
   int force_deep;     // testing: use the per-level sweeps even for shallow plans
+  int force_escape;   // testing: 1 = every tree of k_tiles escapes, 2 = trees of odd root cells escape
+  int tiles;          // 1: the step runs k_tiles + the escape path (else the global level path)
+  uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
   cudaGraphConditionalHandle h_expand, h_dacc, h_deros;

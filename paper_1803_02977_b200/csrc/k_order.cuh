@@ -329,7 +329,8 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
       // plan complete: nlevels = l + 1 (traversal.cpp:45); cycle check (:46)
       ctl->nlev = l + 1;
       uint32_t mode = (l + 1 <= (uint32_t)kChunkMaxLevels && !a.force_deep) ? kModeShallow : kModeDeep;
-      if (!err && hi != a.N) {
+      a.fc[hi] = hi;  // end sentinel of the last level's child ranges
+      if (!err && a.expect_cells && hi != a.expect_cells) {
         ctl->err_flag = LEMGPU_ESTRUCTURE;
         ctl->err_cell = hi;  // cells placed
         ctl->err_slot = ctl->slot;

@@ -43,6 +43,18 @@ __global__ void k_export_graph(StepArgs a, uint32_t* rec, uint8_t* dnum, uint32_
   }
 }
 
+// One level of the export accumulation (accumulate_into, accumulation.cpp:
+// 7-17): A = w + the children's A in slot order; children of the last entry
+// of a level end where the next level's children begin (fc is monotone).
+__global__ void k_acc_level(StepArgs a, uint32_t L) {
+  const uint32_t s = a.levels[L], e = a.levels[L + 1];
+  for (uint32_t pos = s + blockIdx.x * blockDim.x + threadIdx.x; pos < e; pos += gridDim.x * blockDim.x) {
+    double acc = a.w0;
+    for (uint32_t j = a.fc[pos], j1 = a.fc[pos + 1]; j < j1; ++j) acc = __dadd_rn(acc, a.Aq[j]);
+    a.Aq[pos] = acc;
+  }
+}
+
 __global__ void k_export_accum(StepArgs a, double* A) {
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < a.N; p += gridDim.x * blockDim.x)
     A[a.order[p]] = a.Aq[p];

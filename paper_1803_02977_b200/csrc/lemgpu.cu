@@ -25,6 +25,7 @@
 #include "k_order.cuh"
 #include "k_physics.cuh"
 #include "k_recv_donor.cuh"
+#include "k_tiles.cuh"
 #include "k_util.cuh"
 
 using namespace lemgpu;
@@ -35,10 +36,18 @@ struct lemgpu_ctx {
   StepArgs a{};
   lemgpu_params params{};
   std::vector<lemgpu_member> members;
-  int scan_grid = 0, chunk_grid = 0, deep_grid = 0;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  CUtensorMap hmap{};  // TMA descriptor of h (k_recv_donor staging)
+  int scan_grid = 0, chunk_grid = 0, deep_grid = 0, tile_grid = 0;
+  int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
+  // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
+  // graph[p] / exec[p] is the step that reads hbuf[p]
+  double* hbuf[2] = {nullptr, nullptr};
+  uint32_t cur = 0;         // buffer holding the elevation after every enqueued step
+  uint32_t cur_synced = 0;  // ... before the pending steps
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  CUtensorMap hmap[2]{};  // TMA descriptors of hbuf[p]: k_recv_donor box
+  CUtensorMap tmap[2]{};  // ... k_tiles box
+  uint32_t* d_levels_esc = nullptr;
   // device allocations
   double* d_kdt = nullptr;
   double* d_mexp = nullptr;
@@ -137,10 +146,9 @@ int dmalloc(lemgpu_ctx* ctx, T** p, size_t count) {
 // value in every kernel node; everything that changes from step to step lives
 // in the device control block.
 int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void* fn, dim3 grid,
-               dim3 block, size_t smem, bool with_map = false) {
+               dim3 block, size_t smem, StepArgs* sa, CUtensorMap* map) {
   cudaKernelNodeParams kp{};
-  void* args[] = {&ctx->a, &ctx->hmap};
-  (void)with_map;
+  void* args[] = {sa, map};  // copied into the node
   kp.func = const_cast<void*>(fn);
   kp.gridDim = grid;
   kp.blockDim = block;
@@ -153,7 +161,7 @@ int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void
 }
 
 int add_while(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, cudaGraphConditionalHandle h,
-              const void* fn, dim3 grid, size_t smem) {
+              const void* fn, dim3 grid, size_t smem, StepArgs* sa) {
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
@@ -163,17 +171,39 @@ int add_while(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, cudaGraphCo
   CU(ctx, cudaGraphAddNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t inner = nullptr;
-  const int rc = add_kernel(ctx, body, &inner, fn, grid, dim3(kTPB), smem);
+  const int rc = add_kernel(ctx, body, &inner, fn, grid, dim3(kTPB), smem, sa, nullptr);
   if (rc) return rc;
   *prev = n;
   return 0;
 }
 
-int build_graph(lemgpu_ctx* ctx) {
-  StepArgs& a = ctx->a;
+// The StepArgs of the step that reads hbuf[p].
+StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
+  StepArgs a = ctx->a;
+  a.h = ctx->hbuf[p];
+  a.hout = ctx->hbuf[p ^ 1u];
+  a.tiles = ctx->use_tiles;
+  a.levels = ctx->use_tiles ? ctx->d_levels_esc : ctx->a.levels;
+  a.expect_cells = ctx->use_tiles ? 0u : a.N;
+  return a;
+}
+
+template <int CONN, bool EX>
+const void* tiles_fn_nk(int nk) {
+  return nk == 1 ? (const void*)k_tiles<CONN, 1, EX> : nk == 2 ? (const void*)k_tiles<CONN, 2, EX>
+                                                                : (const void*)k_tiles<CONN, 0, EX>;
+}
+const void* tiles_fn(const StepArgs& a) {
+  if (a.lut_exact) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
+  return a.conn == 8 ? tiles_fn_nk<8, false>(a.nkind) : tiles_fn_nk<4, false>(a.nkind);
+}
+size_t tiles_smem(const StepArgs& a) { return a.lut_exact ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>(); }
+
+int build_graph(lemgpu_ctx* ctx, uint32_t p) {
+  StepArgs a = step_args(ctx, p);
   cudaGraph_t g;
   CU(ctx, cudaGraphCreate(&g, 0));
-  ctx->graph = g;
+  ctx->graph[p] = g;
   CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
   CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
   CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
@@ -184,18 +214,26 @@ int build_graph(lemgpu_ctx* ctx) {
   cudaGraphNode_t prev = nullptr;
   int rc;
   const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-  if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, true)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_count, dim3(ctx->scan_grid), dim3(kTPB), 0)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0)) ||
-      (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(ctx->scan_grid), 0)) ||
-      (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0)) ||
-      (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0)) ||
-      (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0)))
+  if (ctx->use_tiles) {
+    if ((rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
+                         &ctx->tmap[p])) ||
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_l0, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
+      return rc;
+  } else {
+    if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_count, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)) ||
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
+      return rc;
+  }
+  if ((rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(ctx->scan_grid), 0, &a)) ||
+      (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
+      (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
+      (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0, &a)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
+      (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0, &a, nullptr)))
     return rc;
-  CU(ctx, cudaGraphInstantiate(&ctx->exec, g, 0));
+  CU(ctx, cudaGraphInstantiate(&ctx->exec[p], g, 0));
   return 0;
 }
 
@@ -295,7 +333,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
 
   int rc;
   if ((rc = dmalloc(ctx, &ctx->d_kdt, M)) || (rc = dmalloc(ctx, &ctx->d_mexp, M)) ||
-      (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &a.h, N)) ||
+      (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &ctx->hbuf[0], N)) ||
+      (rc = dmalloc(ctx, &ctx->hbuf[1], N)) || (rc = dmalloc(ctx, &ctx->d_levels_esc, (size_t)N + 2)) ||
       (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
       (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
       (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) ||
@@ -306,6 +345,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
       (rc = dmalloc(ctx, &a.bins, 3 * 4096)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
       (rc = dmalloc(ctx, &ctx->d_diag, ctx->diag_cap)))
     return bail(rc);
+  a.h = ctx->hbuf[0];
+  a.hout = ctx->hbuf[1];
   a.kdt = ctx->d_kdt;
   a.mexp = ctx->d_mexp;
   a.ftab = ctx->d_lut;
@@ -321,7 +362,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   CUB(cudaMemcpy(ctx->d_kdt, kdt.data(), M * sizeof(double), cudaMemcpyHostToDevice));
   CUB(cudaMemcpy(ctx->d_mexp, mexp.data(), M * sizeof(double), cudaMemcpyHostToDevice));
   CUB(cudaMemcpy(ctx->d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice));
-  CUB(cudaMemset(a.h, 0, (size_t)N * sizeof(double)));
+  CUB(cudaMemset(ctx->hbuf[0], 0, (size_t)N * sizeof(double)));
+  CUB(cudaMemset(ctx->hbuf[1], 0, (size_t)N * sizeof(double)));
   CUB(cudaMemset(a.rcode, 0, (size_t)N + 16));
   CUB(cudaMemset(a.dmask, 0, (size_t)N + 16));
   CUB(cudaMemset(a.bins, 0, 3 * 4096 * sizeof(uint32_t)));
@@ -336,6 +378,18 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand, kTPB, 0));
   ctx->scan_grid = (occ > 0 ? occ : 1) * nsm;
   if (ctx->scan_grid > 4096) ctx->scan_grid = 4096;  // part/bins capacity
+  ctx->use_tiles = 1;
+  if (const char* env = std::getenv("LEMGPU_PATH")) ctx->use_tiles = std::strcmp(env, "global") != 0;
+  a.force_escape = 0;
+  if (const char* env = std::getenv("LEMGPU_FORCE_ESCAPE")) a.force_escape = std::atoi(env);
+  {
+    const void* ft = tiles_fn(a);
+    CUB(cudaFuncSetAttribute(ft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiles_smem(a)));
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ft, kTTPB, tiles_smem(a)));
+    const uint32_t ntiles = ((W + kTX - 1) / kTX) * ((H * M + kTY - 1) / kTY);
+    uint32_t tg = (uint32_t)(occ > 0 ? occ : 1) * (uint32_t)nsm;
+    ctx->tile_grid = (int)(tg < ntiles ? tg : ntiles);
+  }
   a.eager = 0;
   a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
@@ -345,9 +399,9 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->chunk_grid = (occ > 0 ? occ : 1) * nsm;
   ctx->deep_grid = 8 * nsm;
   a.scan_grid = ctx->scan_grid;
-  // TMA descriptor of h: rows of W doubles, box = one k_recv_donor halo tile.
-  // The row pitch must be a multiple of 16 bytes (even W); otherwise the
-  // kernel stages h with plain loads.
+  // TMA descriptors of both elevation buffers: rows of W doubles; boxes = one
+  // k_recv_donor halo tile and one k_tiles window.  The row pitch must be a
+  // multiple of 16 bytes (even W); otherwise the kernels stage h with plain loads.
   a.use_tma = 0;
   if ((W % 2) == 0 && !std::getenv("LEMGPU_NO_TMA")) {
     void* fn = nullptr;
@@ -359,16 +413,23 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
                                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill)>(fn);
       const cuuint64_t gdim[2] = {W, (cuuint64_t)H * M};
       const cuuint64_t gstride[1] = {(cuuint64_t)W * sizeof(double)};
-      const cuuint32_t box[2] = {kBX + 4, kBY + 4};
+      const cuuint32_t box_r[2] = {kBX + 4, kBY + 4};
+      const cuuint32_t box_t[2] = {kWP, kWY};
       const cuuint32_t estr[2] = {1, 1};
-      if (encode(&ctx->hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.h, gdim, gstride, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-        a.use_tma = 1;
+      bool ok = true;
+      for (int p = 0; p < 2; ++p) {
+        ok = ok && encode(&ctx->hmap[p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ctx->hbuf[p], gdim, gstride, box_r, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        ok = ok && encode(&ctx->tmap[p], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ctx->hbuf[p], gdim, gstride, box_t, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+      a.use_tma = ok ? 1 : 0;
     }
   }
-  {
-    const int rcg = build_graph(ctx);
+  for (uint32_t p = 0; p < 2; ++p) {
+    const int rcg = build_graph(ctx, p);
     if (rcg) return bail(rcg);
   }
   *out = ctx;
@@ -379,23 +440,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
 // Eager (profiling) mode: the same kernels launched one by one; the loop
 // conditions come back through the control block, one small D2H per level.
 // ncu cannot profile kernel nodes of graphs with conditional nodes.
-int enqueue_step_eager(lemgpu_ctx* ctx) {
-  StepArgs& a = ctx->a;
+int run_levels_eager(lemgpu_ctx* ctx, const StepArgs& a) {
   cudaStream_t st = ctx->stream;
   const int nk = a.nkind;
-  const unsigned one = 1, zero = 0;
   const size_t co = offsetof(Ctl, cond);
   char* cbase = reinterpret_cast<char*>(a.ctl) + co;
-  CU(ctx, cudaMemcpyAsync(cbase, &one, 4, cudaMemcpyHostToDevice, st));
-  CU(ctx, cudaMemcpyAsync(cbase + 4, &zero, 4, cudaMemcpyHostToDevice, st));
-  CU(ctx, cudaMemcpyAsync(cbase + 8, &zero, 4, cudaMemcpyHostToDevice, st));
-  const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-  if (a.conn == 8)
-    k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap);
-  else
-    k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap);
-  k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
-  k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
   unsigned cond[3] = {1, 0, 0};
   while (cond[0]) {
     k_expand<<<ctx->scan_grid, kTPB, 0, st>>>(a);
@@ -409,6 +458,8 @@ int enqueue_step_eager(lemgpu_ctx* ctx) {
   else
     k_chunks<0><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
   k_deep_prep<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+  CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+  CU(ctx, cudaStreamSynchronize(st));
   while (cond[1]) {
     k_deep_accum<<<ctx->deep_grid, kTPB, 0, st>>>(a);
     CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
@@ -425,6 +476,41 @@ int enqueue_step_eager(lemgpu_ctx* ctx) {
     CU(ctx, cudaStreamSynchronize(st));
   }
   k_deep_final<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+  return LEMGPU_OK;
+}
+
+void set_eager_conds(const StepArgs& a, cudaStream_t st) {
+  static const unsigned init[3] = {1, 0, 0};
+  char* cbase = reinterpret_cast<char*>(a.ctl) + offsetof(Ctl, cond);
+  cudaMemcpyAsync(cbase, init, sizeof init, cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);  // init is host memory
+}
+
+int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
+  StepArgs a = step_args(ctx, p);
+  a.eager = 1;
+  cudaStream_t st = ctx->stream;
+  set_eager_conds(a, st);
+  if (ctx->use_tiles) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctx->tile_grid);
+    cfg.blockDim = dim3(kTTPB);
+    cfg.dynamicSmemBytes = tiles_smem(a);
+    cfg.stream = st;
+    void* args[] = {&a, &ctx->tmap[p]};
+    CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
+    k_esc_l0<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+  } else {
+    const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+    if (a.conn == 8)
+      k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+    else
+      k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+    k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+  }
+  const int rc = run_levels_eager(ctx, a);
+  if (rc) return rc;
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
   return LEMGPU_OK;
@@ -442,13 +528,15 @@ int enqueue_step(lemgpu_ctx* ctx) {
     ev = &ctx->ev[2 * ctx->pending];
     CU(ctx, cudaEventRecord(ev[0], ctx->stream));
   }
+  const uint32_t p = ctx->cur;
   if (ctx->a.eager) {
-    const int rc = enqueue_step_eager(ctx);
+    const int rc = enqueue_step_eager(ctx, p);
     if (rc) return rc;
   } else {
-    CU(ctx, cudaGraphLaunch(ctx->exec, ctx->stream));
+    CU(ctx, cudaGraphLaunch(ctx->exec[p], ctx->stream));
   }
   if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
+  ctx->cur = p ^ 1u;
   ++ctx->pending;
   ctx->have_graph = true;
   return LEMGPU_OK;
@@ -476,14 +564,16 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
-  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, a.h,   a.rcode,  a.dmask, a.order,
+  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode,  a.dmask, a.order,
                   a.ppos,     a.cdir,      a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
-  if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
-  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  for (int p = 0; p < 2; ++p) {
+    if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
+    if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -504,11 +594,12 @@ int lemgpu_upload_elev(lemgpu_ctx* ctx, const double* host) {
   if (!ctx || !host) return fail(ctx, LEMGPU_ECONFIG, "null argument");
   CU(ctx, cudaSetDevice(ctx->device));
   const StepArgs& a = ctx->a;
-  CU(ctx, cudaMemcpyAsync(a.h, host, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  double* hc = ctx->hbuf[ctx->cur];
+  CU(ctx, cudaMemcpyAsync(hc, host, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   // reject non-finite input (scheduler.cpp:474-477); reuse fc[N] as scratch
   uint32_t* bad = a.fc + a.N;
   CU(ctx, cudaMemsetAsync(bad, 0xFF, sizeof(uint32_t), ctx->stream));
-  k_check_finite<<<1184, kTPB, 0, ctx->stream>>>(a.h, a.N, bad);
+  k_check_finite<<<1184, kTPB, 0, ctx->stream>>>(hc, a.N, bad);
   uint32_t first = 0;
   CU(ctx, cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -521,7 +612,8 @@ int lemgpu_upload_elev(lemgpu_ctx* ctx, const double* host) {
 int lemgpu_download_elev(lemgpu_ctx* ctx, double* host) {
   if (!ctx || !host) return fail(ctx, LEMGPU_ECONFIG, "null argument");
   CU(ctx, cudaSetDevice(ctx->device));
-  CU(ctx, cudaMemcpyAsync(host, ctx->a.h, (size_t)ctx->a.N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(host, ctx->hbuf[ctx->cur], (size_t)ctx->a.N * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   return LEMGPU_OK;
 }
@@ -536,7 +628,7 @@ int lemgpu_generate_terrain(lemgpu_ctx* ctx, const uint64_t* seeds) {
   unsigned long long* d_seeds = nullptr;
   CU(ctx, cudaMalloc(&d_seeds, a.M * sizeof(unsigned long long)));
   CU(ctx, cudaMemcpy(d_seeds, s.data(), a.M * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-  k_terrain<<<2368, kTPB, 0, ctx->stream>>>(a.h, a.N, a.MN, d_seeds);
+  k_terrain<<<2368, kTPB, 0, ctx->stream>>>(ctx->hbuf[ctx->cur], a.N, a.MN, d_seeds);
   CU(ctx, cudaGetLastError());
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   cudaFree(d_seeds);
@@ -578,6 +670,8 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
     ctx->kernel_launches += n;
   }
   ctx->pending = 0;
+  const uint32_t c0buf = ctx->cur_synced;
+  ctx->cur_synced = ctx->cur;
   if (n) CU(ctx, cudaMemset(reinterpret_cast<char*>(ctx->a.ctl) + offsetof(Ctl, slot), 0, sizeof(uint32_t)));
   int status = LEMGPU_OK;
   for (uint32_t s = 0; s < n; ++s) {
@@ -593,12 +687,16 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
       else
         fail(ctx, status, "step %u failed with status %u", s, d[s].status);
       // clear the sticky device flag so the context can be reused
-      Ctl c0{};
-      CU(ctx, cudaMemcpy(&c0, ctx->a.ctl, sizeof c0, cudaMemcpyDeviceToHost));
-      c0.err_flag = 0;
-      c0.err_cell = LEMGPU_NOFLOW;
-      c0.slot = 0;
-      CU(ctx, cudaMemcpy(ctx->a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
+      Ctl cb{};
+      CU(ctx, cudaMemcpy(&cb, ctx->a.ctl, sizeof cb, cudaMemcpyDeviceToHost));
+      cb.err_flag = 0;
+      cb.err_cell = LEMGPU_NOFLOW;
+      cb.slot = 0;
+      CU(ctx, cudaMemcpy(ctx->a.ctl, &cb, sizeof cb, cudaMemcpyHostToDevice));
+      // a failed step leaves the elevation as it was before that step: its
+      // input buffer (steps never write the buffer they read; later steps
+      // of the batch did not run)
+      ctx->cur = ctx->cur_synced = (c0buf + s) & 1u;
       break;
     }
     ctx->last_nlevels = d[s].nlevels;
@@ -632,14 +730,18 @@ int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag) {
   if (!ctx || !elev_inout) return fail(ctx, LEMGPU_ECONFIG, "null argument");
   CU(ctx, cudaSetDevice(ctx->device));
   const StepArgs& a = ctx->a;
-  CU(ctx, cudaMemcpyAsync(a.h, elev_inout, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->hbuf[ctx->cur], elev_inout, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
   int rc = lemgpu_step_async(ctx, 1);
   if (rc) return rc;
-  CU(ctx, cudaMemcpyAsync(elev_inout, a.h, (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(elev_inout, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
   lemgpu_diag d{};
   uint32_t cnt = 0;
   rc = lemgpu_sync(ctx, &d, 1, &cnt);
   if (diag) *diag = d;
+  if (rc && rc != LEMGPU_ECUDA)  // the failed step left the elevation unchanged
+    cudaMemcpy(elev_inout, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost);
   return rc;
 }
 
@@ -652,7 +754,41 @@ int lemgpu_download_graph(lemgpu_ctx* ctx, uint32_t* rec, uint8_t* dnum, uint32_
     const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
     if (rc) return rc;
   }
-  const StepArgs& a = ctx->a;
+  // The TraversalPlan and the accumulation of the last step, rebuilt from
+  // its flow graph (rcode / dmask, written by the step) with the global
+  // level path: level 0 = all NoFlow cells ascending, one expansion per
+  // level, then A swept deepest level first in slot order -- the reference's
+  // generate_queue + accumulate (traversal.cpp:19-48, accumulation.cpp:7-17).
+  StepArgs a = ctx->a;
+  a.tiles = 0;
+  a.eager = 1;
+  a.expect_cells = a.N;
+  {
+    cudaStream_t st = ctx->stream;
+    set_eager_conds(a, st);
+    k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    const size_t co = offsetof(Ctl, cond);
+    char* cbase = reinterpret_cast<char*>(a.ctl) + co;
+    unsigned cond[3] = {1, 0, 0};
+    while (cond[0]) {
+      k_expand<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+      CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+      CU(ctx, cudaStreamSynchronize(st));
+    }
+    Ctl c{};
+    CU(ctx, cudaMemcpy(&c, a.ctl, sizeof c, cudaMemcpyDeviceToHost));
+    if (c.err_flag) return fail(ctx, LEMGPU_ESTRUCTURE, "receiver graph has a cycle");
+    ctx->last_nlevels = c.nlev;
+    for (int L = (int)c.nlev - 1; L >= 0; --L) k_acc_level<<<ctx->deep_grid, kTPB, 0, st>>>(a, (uint32_t)L);
+    // leave the per-step control state as a step expects it
+    c.lvl = 0;
+    c.done = 0;
+    c.mode = kModeShallow;
+    c.cond[0] = c.cond[1] = c.cond[2] = 0;
+    CU(ctx, cudaMemcpyAsync(a.ctl, &c, sizeof c, cudaMemcpyHostToDevice, st));
+    CU(ctx, cudaStreamSynchronize(st));
+  }
   const size_t N = a.N;
   uint32_t* d_rec = nullptr;
   uint8_t* d_dnum = nullptr;
@@ -688,7 +824,7 @@ int lemgpu_member_stats_device(lemgpu_ctx* ctx, double* device_out) {
   // partials live in the accumulation scratch (Aq), which is per-step scratch
   double* part = a.Aq;
   if ((size_t)a.M * chunks * 3 > a.N) return fail(ctx, LEMGPU_ECONFIG, "members too small for stats scratch");
-  k_stats_partial<<<dim3(chunks, a.M), kTPB, 0, ctx->stream>>>(a.h, a.MN, chunks, part);
+  k_stats_partial<<<dim3(chunks, a.M), kTPB, 0, ctx->stream>>>(ctx->hbuf[ctx->cur], a.MN, chunks, part);
   k_stats_final<<<(a.M + 127) / 128, 128, 0, ctx->stream>>>(part, a.M, chunks, a.MN, device_out);
   CU(ctx, cudaGetLastError());
   ctx->have_graph = false;  // Aq was clobbered

@@ -315,3 +315,55 @@ def test_per_level_sweeps_match_chunked(oracle, monkeypatch, w, h, seed, kw):
         assert np.array_equal(hd.view(np.uint64), hc.view(np.uint64))
         assert dd.newton_iters == dc.newton_iters
         compare_step(deep, o, hd, e, exact_h=kw.get("n_exp", 1.0) == 1.0, tag="deep")
+
+
+def _ramp(w, h, seed):
+    """Tilted plane + noise: long drainage chains (deep plans, trees that leave any tile)."""
+    rng = np.random.default_rng(seed)
+    x = np.arange(w)[None, :].astype(np.float64)
+    y = np.arange(h)[:, None].astype(np.float64)
+    return 0.05 * x + 0.01 * y + 1e-3 * rng.random((h, w))
+
+
+@pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_FORCE_ESCAPE": "2"},
+                                 {"LEMGPU_PATH": "global"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_FORCE_DEEP": "1"}],
+                         ids=["tiles", "all-escape", "half-escape", "global", "all-escape-deep"])
+@pytest.mark.parametrize("w,h,seed,kw,terrain", [
+    (300, 200, 31, {}, "noise"), (130, 97, 32, {"n_exp": 2.0}, "noise"), (77, 65, 33, {"dx": 0.5}, "noise"),
+    (129, 70, 34, {}, "ramp"), (90, 61, 35, {}, "ramp"),
+])
+def test_schedules_agree_with_oracle(oracle, monkeypatch, env, w, h, seed, kw, terrain):
+    """Every schedule -- trees finished inside their tile (k_tiles), trees that
+    escape to the global level path (all of them, or every odd-rooted one),
+    the global path alone, and its per-level sweeps -- gives the oracle's bits."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = device_ctx(w, h, **kw)
+    for k in env:
+        monkeypatch.delenv(k)
+    e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
+    ctx.upload(e)
+    p = make_params(**kw)
+    exact = kw.get("n_exp", 1.0) == 1.0
+    for s in range(4):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, params=p)
+        hg = ctx.download()
+        compare_step(ctx, o, hg, e, exact_h=exact, tag=f"{env} step {s}")
+        if not exact:
+            e[...] = hg  # continue from the same state
+        else:
+            assert d.newton_iters == o["newton_iters"]
+        assert d.interior_noflow == o["interior_noflow"]
+        assert d.nlevels == o["nlevels"]
+
+
+def test_failed_step_leaves_elevation_unchanged(oracle):
+    """A step that raises (ConvergenceError) leaves the device elevation as it
+    was before that step (steps read one ping-pong buffer and write the other)."""
+    ctx = device_ctx(64, 48, max_newton_iters=1)
+    e = oracle.terrain(64, 48, 3)
+    ctx.upload(e)
+    with pytest.raises(lem.ConvergenceError):
+        ctx.step(3)
+    assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
