@@ -185,6 +185,10 @@ int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
  * begin/end, then the end of k_level0, of every k_expand level and of the
  * accumulation/erosion sweeps. */
 int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t* count);
+/* Debug / test hook (no reference counterpart): copy `bytes` of a device
+ * scratch array of the last step to host memory.  which: 0 = queue (order),
+ * 1 = escape-path level bounds, 2 = control block.  Not used by the step. */
+int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes);
 
 /* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */
 int lemgpu_host_register(void* ptr, size_t bytes);

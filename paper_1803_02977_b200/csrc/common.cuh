@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "lemgpu.h"
@@ -94,6 +95,22 @@ __host__ __device__ constexpr bool dir_in(int conn, int k) {
 #define LG_DIV(x, y) ((x) / (y))
 #endif
 
+#ifdef __CUDA_ARCH__
+#define LG_FMA(x, y, z) __fma_rn((x), (y), (z))
+#else
+#define LG_FMA(x, y, z) std::fma((x), (y), (z))
+#endif
+// High 32 bits of a double (sign, exponent, top 20 mantissa bits).
+__host__ __device__ __forceinline__ int hi_word(double x) {
+#ifdef __CUDA_ARCH__
+  return __double2hiint(x);
+#else
+  unsigned long long b;
+  __builtin_memcpy(&b, &x, 8);
+  return (int)(b >> 32);
+#endif
+}
+
 // Device control block (one per context).
 struct Ctl {
   // persistent
@@ -139,6 +156,7 @@ struct StepArgs {
   const double* kdt;   // per member K*dt
   const double* mexp;  // per member m
   const double* ftab;  // per member and offset class: F(a) = (K*dt * pow(a*w0, m)) / pow(dist, n), host libm
+  const double* ftab2;  // same index: {F, RN(1 / RN(1 + F))} pairs
   // state / scratch.  h is the elevation the step reads (never written during
   // the step), hout the elevation it writes (ping-pong buffers; the step's
   // receivers always see the complete previous surface)
@@ -164,6 +182,7 @@ struct StepArgs {
   int force_deep;     // testing: use the per-level sweeps even for shallow plans
   int force_escape;   // testing: 1 = every tree of k_tiles escapes, 2 = trees of odd root cells escape
   int tiles;          // 1: the step runs k_tiles + the escape path (else the global level path)
+  int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)

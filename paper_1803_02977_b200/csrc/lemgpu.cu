@@ -52,6 +52,7 @@ struct lemgpu_ctx {
   double* d_kdt = nullptr;
   double* d_mexp = nullptr;
   double* d_lut = nullptr;
+  double* d_lut2 = nullptr;  // interleaved {F, RN(1 / RN(1 + F))} (n = 1 Newton without IEEE divisions)
   lemgpu_diag* d_diag = nullptr;
   uint32_t diag_cap = 4096;
   uint32_t pending = 0;  // steps enqueued since the last sync
@@ -333,7 +334,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
 
   int rc;
   if ((rc = dmalloc(ctx, &ctx->d_kdt, M)) || (rc = dmalloc(ctx, &ctx->d_mexp, M)) ||
-      (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &ctx->hbuf[0], N)) ||
+      (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &ctx->d_lut2, 2 * lut.size())) || (rc = dmalloc(ctx, &ctx->hbuf[0], N)) ||
       (rc = dmalloc(ctx, &ctx->hbuf[1], N)) || (rc = dmalloc(ctx, &ctx->d_levels_esc, (size_t)N + 2)) ||
       (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
       (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
@@ -350,6 +351,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.kdt = ctx->d_kdt;
   a.mexp = ctx->d_mexp;
   a.ftab = ctx->d_lut;
+  a.ftab2 = ctx->d_lut2;
   a.cb_stride = N / kChunkRoots + 2;
   a.diag = ctx->d_diag;
 #define CUB(call)                          \
@@ -362,6 +364,19 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   CUB(cudaMemcpy(ctx->d_kdt, kdt.data(), M * sizeof(double), cudaMemcpyHostToDevice));
   CUB(cudaMemcpy(ctx->d_mexp, mexp.data(), M * sizeof(double), cudaMemcpyHostToDevice));
   CUB(cudaMemcpy(ctx->d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice));
+  {
+    // slope = 1.0 + (F * n) * pow(diff, n - 1) = 1.0 + F for n = 1 (erosion.cpp:26; pow(x, 0) == 1);
+    // its correctly rounded reciprocal (host IEEE division) for the device's
+    // Markstein-corrected quotients (newton_n1_tab, k_tiles.cuh)
+    std::vector<double> lut2(2 * lut.size());
+    a.tab_ok = 1;
+    for (size_t i = 0; i < lut.size(); ++i) {
+      if (!(lut[i] < 0x1p500)) a.tab_ok = 0;
+      lut2[2 * i] = lut[i];
+      lut2[2 * i + 1] = 1.0 / (1.0 + lut[i]);
+    }
+    CUB(cudaMemcpy(ctx->d_lut2, lut2.data(), lut2.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   CUB(cudaMemset(ctx->hbuf[0], 0, (size_t)N * sizeof(double)));
   CUB(cudaMemset(ctx->hbuf[1], 0, (size_t)N * sizeof(double)));
   CUB(cudaMemset(a.rcode, 0, (size_t)N + 16));
@@ -388,6 +403,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ft, kTTPB, tiles_smem(a)));
     const uint32_t ntiles = ((W + kTX - 1) / kTX) * ((H * M + kTY - 1) / kTY);
     uint32_t tg = (uint32_t)(occ > 0 ? occ : 1) * (uint32_t)nsm;
+    if (const char* env = std::getenv("LEMGPU_TILE_GRID")) tg = (uint32_t)std::atoi(env);  // testing: few CTAs, many tiles each
+    if (tg < 1) tg = 1;
     ctx->tile_grid = (int)(tg < ntiles ? tg : ntiles);
   }
   a.eager = 0;
@@ -564,7 +581,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
-  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode,  a.dmask, a.order,
+  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->d_lut2, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode,  a.dmask, a.order,
                   a.ppos,     a.cdir,      a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
@@ -859,6 +876,17 @@ int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t*
   const uint32_t n = c.nltl < cap ? c.nltl : cap;
   for (uint32_t i = 0; i < n; ++i) ns[i] = c.ltl[i];
   if (count) *count = n;
+  return LEMGPU_OK;
+}
+
+int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes) {
+  if (!ctx || !host) return LEMGPU_ECONFIG;
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  const void* src = which == 0 ? (const void*)ctx->a.order : which == 1 ? (const void*)ctx->d_levels_esc
+                                                                          : (const void*)ctx->a.ctl;
+  const uint64_t cap = which == 0 ? (uint64_t)ctx->a.N * 4 : which == 1 ? ((uint64_t)ctx->a.N + 2) * 4 : sizeof(Ctl);
+  CU(ctx, cudaMemcpy(host, src, bytes < cap ? bytes : cap, cudaMemcpyDeviceToHost));
   return LEMGPU_OK;
 }
 

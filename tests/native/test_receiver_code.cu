@@ -10,7 +10,7 @@
 #include <cstdint>
 #include <random>
 
-#include "../../paper_1803_02977_b200/csrc/k_recv_donor.cuh"
+#include "../../paper_1803_02977_b200/csrc/k_tiles.cuh"
 
 using namespace lemgpu;
 
@@ -42,10 +42,10 @@ int main() {
   long long n = 0, bad = 0;
   auto check = [&](const double (&d)[8]) {
     ++n;
-    const uint8_t want = naive(d, a.dist), got = receiver_code<8>(d, a);
-    if (want != got) {
+    const uint8_t want = naive(d, a.dist), got = receiver_code<8>(d, a), got2 = receiver_code_hi<8>(d, a);
+    if (want != got || want != got2) {
       if (bad < 10) {
-        std::printf("MISMATCH want %d got %d:", want, got);
+        std::printf("MISMATCH want %d got %d / %d:", want, got, got2);
         for (int k = 0; k < 8; ++k) std::printf(" %.17g", d[k]);
         std::printf("\n");
       }
@@ -81,8 +81,11 @@ int main() {
       const double x = std::fabs(d[0]) + scale;
       for (int k : diag) d[k] = (rng() & 1) ? x : std::nextafter(x, -1e300);
       d[card[rng() % 4]] = x / c;
-    } else if (mode == 7) {  // subnormal corner
-      for (int k = 0; k < 8; ++k) d[k] = U(rng) * 1e-310;
+    } else if (mode == 7) {  // subnormal corner, or +0 drops (flats left by the erosion floor)
+      if (rng() & 1)
+        for (int k = 0; k < 8; ++k) d[k] = U(rng) * 1e-310;
+      else
+        for (int k = 0; k < 8; ++k) d[k] = (rng() % 3) ? -std::fabs(d[k]) : 0.0;
     }
     check(d);
   }

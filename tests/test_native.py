@@ -15,3 +15,16 @@ def test_receiver_division_skipping_is_exact(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout
     assert "0 mismatches" in out.stdout
+
+
+def test_division_from_table_reciprocal_is_exact(tmp_path):
+    """div_rn_recip (Markstein correction from the host-rounded reciprocal of
+    the Newton slope) == IEEE a / b on 1.6e8 random, table-shaped and
+    near-midpoint operands."""
+    exe = tmp_path / "test_div_recip"
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-O2", "-I", str(ROOT / "include"),
+                    "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-ffp-contract=off",
+                    "--fmad=false", "-o", str(exe), str(ROOT / "tests/native/test_div_recip.cu")], check=True)
+    out = subprocess.run([str(exe), "160000000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert " 0 mismatches" in out.stdout
