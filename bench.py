@@ -36,10 +36,12 @@ sys.path.insert(0, str(ROOT))
 METRIC = "cell-steps/s, 10000² DEM, 1 GPU; ensemble cell-steps/s at 1/2/4/8 B200"
 UNIT = "cell-steps/s"
 PAPER_P100 = 1e8 * 120 / 70.0  # RB+GPU 10000^2 x 120 steps in 70 s on one P100
-# Algorithmic bytes per cell-step: receivers 12 + donors 5 | order 9 + accum 21 + uplift/erosion 40
-B_RECV_DONOR = 17
-B_FLOW = 70
+# Algorithmic bytes per cell-step: receivers 12 + donors 5 + order 9 + accumulation 21 +
+# uplift/erosion 40 = 87.  k_tiles performs every one of these phases for the cells it finishes, so its
+# algorithmic bytes are 87 per cell; the bytes it actually moves are ~18 per cell (h in, h out, the
+# receiver code and donor mask bytes out) -- the 'traffic' key, from ncu.
 B_STEP = 87
+B_TILES_MIN = 18
 WORKLOADS = {
     "dem10000": dict(w=10000, h=10000, members=1, n_exp=1.0,
                      desc="10000x10000 random-noise DEM, D8, m=0.5 n=1, fixed-perimeter base level, seed 42 (configs[1])"),
@@ -335,13 +337,11 @@ def main():
     peak, peak_src = load_peaks()
     n_l = max(kt["launches"], 1)
     step_ms_ev = kt["step"] / n_l
-    k1_ms, ord_ms, phys_ms = kt["recv_donor"] / n_l, kt["order"] / n_l, kt["physics"] / n_l
-    # dominant kernel group by device time; algorithmic bytes per cell:
-    # recv_donor 17 (receivers 12 + donors 5), order 9, accumulation 21 + uplift/erosion 40
-    groups = {"k_recv_donor": (k1_ms, B_RECV_DONOR), "k_level0+k_expand": (ord_ms, 9),
-              "k_chunks": (phys_ms, 61)}
-    dom = max(groups, key=lambda k: groups[k][0])
-    dom_ms, dom_b = groups[dom]
+    tiles_ms, esc_ord_ms, esc_phys_ms = kt["recv_donor"] / n_l, kt["order"] / n_l, kt["physics"] / n_l
+    # dominant kernel: k_tiles (the whole step for every tree that stays within
+    # its tile's halo); the escape path (level expansion + chunk physics for the
+    # rest) is reported beside it
+    dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_STEP
     achieved = dom_b * cells / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     traffic_tbl, traffic_src = traffic_from_profiles(args.workload)
     traffic = traffic_tbl.get(dom, {}).get("dram_bytes_per_launch") if traffic_tbl else None
@@ -349,8 +349,12 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_cell": dom_b,
-                "kernel_ms": {"step(events)": step_ms_ev, "k_recv_donor": k1_ms, "k_level0+k_expand": ord_ms,
-                              "k_chunks": phys_ms},
+                "alg_bytes_note": "SURVEY 8(d) 87 B/cell-step (receivers 12, donors 5, order 9, accumulation 21, "
+                                  "uplift+erosion 40); k_tiles fuses all phases and moves ~18 B/cell",
+                "moved_bytes_per_cell_min": B_TILES_MIN,
+                "hbm_frac_of_moved_bytes": (B_TILES_MIN * cells / (dom_ms / 1e3) / 1e9 / peak) if dom_ms > 0 else None,
+                "kernel_ms": {"step(events)": step_ms_ev, "k_tiles": tiles_ms,
+                              "escape:k_esc_l0+k_expand": esc_ord_ms, "escape:k_chunks+deep": esc_phys_ms},
                 "timing_source": "CUDA events around each step's graph launch on the context stream; "
                                  "per-kernel split from device %globaltimer stamps taken by the kernels",
                 "step": {"alg_bytes_per_cell": B_STEP, "achieved": per_gpu * B_STEP / 1e9,
@@ -363,10 +367,11 @@ def main():
             cpu = cpu_baseline_reference(args.workload)
         except Exception as e:  # report, never fail the bench
             cpu = {"value": None, "error": str(e)}
-    # per step: k_recv_donor, k_level0, one k_expand per level, k_chunks,
-    # k_deep_prep, k_deep_final, k_finalize (+ 2 stats kernels in ensemble mode)
+    # per step: k_tiles, k_esc_l0, one k_expand per escape level (+1 closing),
+    # k_chunks, k_deep_prep, k_deep_final, k_finalize (+ 2 stats kernels in
+    # ensemble mode); the escape plan is at most as deep as the step's plan
     nlev_last = diags[-1].nlevels if diags else 0
-    launches = args.steps * (6 + nlev_last) + (2 * args.steps if ens else 0)
+    launches = args.steps * (7 + nlev_last) + (2 * args.steps if ens else 0)
     last = diags[-1] if diags else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -382,8 +387,9 @@ def main():
                    "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",
                    "nlevels_last_step": last.nlevels if last else None,
                    "phase_ms_last_step": ({k: round(v * 1e3, 4) for k, v in zip(
-                       ("receivers+donors", "donors", "order", "accum", "uplift", "accum+uplift+erosion"), last.seconds)}
-                       if last else None),
+                       ("k_tiles", "-", "escape:order", "-", "-", "escape:accum+uplift+erosion"), last.seconds)
+                       if k != "-"} if last else None),
+                   "escaped_trees_last_step": last.escaped_trees if last else None,
                    "newton_iters_last_step": last.newton_iters if last else None},
         "clocks": clk.summary(),
         "e2e": e2e,

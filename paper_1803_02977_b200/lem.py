@@ -221,11 +221,12 @@ class StepDiagnostics:
     interior_noflow: int = 0
     nlevels: int = 0
     lut_misses: int = 0
+    escaped_trees: int = 0  # trees finished by the global level path (k_tiles path), else source chunks
 
     @staticmethod
     def from_abi(d: _abi.lemgpu_diag) -> "StepDiagnostics":
         return StepDiagnostics(list(d.seconds), int(d.newton_iters), int(d.interior_noflow),
-                               int(d.nlevels), int(d.lut_misses))
+                               int(d.nlevels), int(d.lut_misses), int(d.reserved))
 
     @property
     def timings(self):
