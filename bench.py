@@ -37,10 +37,12 @@ METRIC = "cell-steps/s, 10000² DEM, 1 GPU; ensemble cell-steps/s at 1/2/4/8 B20
 UNIT = "cell-steps/s"
 PAPER_P100 = 1e8 * 120 / 70.0  # RB+GPU 10000^2 x 120 steps in 70 s on one P100
 # Algorithmic bytes per cell-step: receivers 12 + donors 5 + order 9 + accumulation 21 +
-# uplift/erosion 40 = 87.  k_tiles performs every one of these phases for the cells it finishes, so its
-# algorithmic bytes are 87 per cell; the bytes it actually moves are ~18 per cell (h in, h out, the
-# receiver code and donor mask bytes out) -- the 'traffic' key, from ncu.
+# uplift/erosion 40 = 87.  k_recv_donor does receivers + donors (17 B/cell); k_tiles does order,
+# accumulation, uplift and erosion (70 B/cell) for the cells it finishes, moving only ~18 B/cell
+# (h in 8, h out 8, receiver code 1, code bit planes 0.5) -- the 'traffic' key, from ncu.
 B_STEP = 87
+B_RECV = 17
+B_TILES = 70
 B_TILES_MIN = 18
 WORKLOADS = {
     "dem10000": dict(w=10000, h=10000, members=1, n_exp=1.0,
@@ -337,11 +339,12 @@ def main():
     peak, peak_src = load_peaks()
     n_l = max(kt["launches"], 1)
     step_ms_ev = kt["step"] / n_l
-    tiles_ms, esc_ord_ms, esc_phys_ms = kt["recv_donor"] / n_l, kt["order"] / n_l, kt["physics"] / n_l
-    # dominant kernel: k_tiles (the whole step for every tree that stays within
-    # its tile's halo); the escape path (level expansion + chunk physics for the
-    # rest) is reported beside it
-    dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_STEP
+    k1_ms, tiles_ms = kt["recv_donor"] / n_l, kt["tiles"] / n_l
+    esc_ord_ms, esc_phys_ms = kt["order"] / n_l, kt["physics"] / n_l
+    # dominant kernel: k_tiles (level order, accumulation, uplift and erosion of
+    # every tree that stays within its tile's halo) after k_recv_donor
+    # (receivers, donor masks, code bit planes); the escape path finishes the rest
+    dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_TILES
     achieved = dom_b * cells / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     traffic_tbl, traffic_src = traffic_from_profiles(args.workload)
     traffic = traffic_tbl.get(dom, {}).get("dram_bytes_per_launch") if traffic_tbl else None
@@ -349,11 +352,14 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_cell": dom_b,
-                "alg_bytes_note": "SURVEY 8(d) 87 B/cell-step (receivers 12, donors 5, order 9, accumulation 21, "
-                                  "uplift+erosion 40); k_tiles fuses all phases and moves ~18 B/cell",
+                "alg_bytes_note": "SURVEY 8(d): order 9 + accumulation 21 + uplift/erosion 40 = 70 B/cell for "
+                                  "k_tiles (k_recv_donor: receivers 12 + donors 5); k_tiles moves ~18 B/cell",
+                "k_recv_donor": {"alg_bytes_per_cell": B_RECV, "ms": k1_ms,
+                                 "achieved": B_RECV * cells / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None,
+                                 "frac": (B_RECV * cells / (k1_ms / 1e3) / 1e9 / peak) if k1_ms > 0 else None},
                 "moved_bytes_per_cell_min": B_TILES_MIN,
                 "hbm_frac_of_moved_bytes": (B_TILES_MIN * cells / (dom_ms / 1e3) / 1e9 / peak) if dom_ms > 0 else None,
-                "kernel_ms": {"step(events)": step_ms_ev, "k_tiles": tiles_ms,
+                "kernel_ms": {"step(events)": step_ms_ev, "k_recv_donor": k1_ms, "k_tiles": tiles_ms,
                               "escape:k_esc_l0+k_expand": esc_ord_ms, "escape:k_chunks+deep": esc_phys_ms},
                 "timing_source": "CUDA events around each step's graph launch on the context stream; "
                                  "per-kernel split from device %globaltimer stamps taken by the kernels",
@@ -387,7 +393,7 @@ def main():
                    "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",
                    "nlevels_last_step": last.nlevels if last else None,
                    "phase_ms_last_step": ({k: round(v * 1e3, 4) for k, v in zip(
-                       ("k_tiles", "-", "escape:order", "-", "-", "escape:accum+uplift+erosion"), last.seconds)
+                       ("k_recv_donor", "-", "escape:order", "k_tiles", "-", "escape:accum+uplift+erosion"), last.seconds)
                        if k != "-"} if last else None),
                    "escaped_trees_last_step": last.escaped_trees if last else None,
                    "newton_iters_last_step": last.newton_iters if last else None},

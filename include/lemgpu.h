@@ -177,7 +177,8 @@ int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
  * ms[0] = whole step (CUDA events around each graph launch on the context
  * stream), ms[1] = k_recv_donor, ms[2] = level order (k_level0 + k_expand),
  * ms[3] = accumulation + uplift + erosion (k_chunks / k_deep_*); the phase
- * split comes from %globaltimer stamps taken on the device.  `ms` holds 4. */
+ * split comes from %globaltimer stamps taken on the device.  `ms` holds 5:
+ * step, k_recv_donor, escape-path order, escape-path physics, k_tiles. */
 int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable);
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
 

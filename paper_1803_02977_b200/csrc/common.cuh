@@ -2,10 +2,11 @@
 //
 // One timestep is a CUDA graph of these kernels:
 //
-//   k_tiles             the whole step for every drainage tree rooted in a
-//                       64x32 tile whose cells stay within 3 cells of it     (k_tiles.cuh)
+//   k_recv_donor        receivers + donor bitmask + code bit planes      (k_recv_donor.cuh)
+//   k_tiles             level order, accumulation, uplift and erosion of
+//                       every drainage tree rooted in a 64x32 tile whose
+//                       cells stay within 3 cells of it                  (k_tiles.cuh)
 //   then, for the trees that escape their tile (and for the parity export):
-//   k_recv_donor        receivers + donor bitmask, smem-staged stencil   (k_recv_donor.cuh)
 //   k_l0_count/_write   level 0 of the BFS order: stream compaction       (k_order.cuh)
 //   WHILE { k_expand }  one frontier expansion per level                  (k_order.cuh)
 //   k_chunks            accumulation + uplift + erosion per source chunk  (k_physics.cuh)
@@ -129,6 +130,7 @@ struct Ctl {
   // tile path (k_tiles): escaped roots, cells finished in tiles, interior pits, deepest level + 1
   uint32_t nesc, tile_cells, n0i, tile_nlev;
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
+  unsigned long long t_t_begin, t_t_end;  // k_tiles
   uint32_t ntl, nltl;
   unsigned long long tl[96];   // debug timeline of the running step (finisher stamps)
   unsigned long long ltl[98];  // ... and of the last completed step
@@ -164,6 +166,8 @@ struct StepArgs {
   double* hout;
   uint8_t* rcode;
   uint8_t* dmask;
+  uint32_t* planes;  // 4 bit planes of rcode, [plane][row][W32] words (k_recv_donor -> k_tiles)
+  uint32_t W32;      // words per plane row
   uint32_t* order;
   uint32_t* ppos;     // position-major: queue position of the receiver (levels >= 1)
   uint8_t* cdir;      // position-major: stencil direction receiver -> cell (levels >= 1)

@@ -87,6 +87,49 @@ __host__ __device__ __forceinline__ uint8_t receiver_code(const double (&d)[8], 
   return receiver_code_ref<CONN>(d, a);
 }
 
+// D8, unit cardinal spacing: receiver code without divisions.  t_k = d_k
+// (cardinal, exact) or RN(d_k * RN(1/sqrt2)) (diagonal, within 2^-51 relative
+// of the reference slope RN(d_k / sqrt2)).  The high words of positive
+// doubles order them; when exactly one t_k has a high word within 1 of the
+// largest, every other t_j is below it by more than 2^-22 relative, so it is
+// the unique strict maximum of the reference slopes as well.  Ties, near
+// ties, subnormal or non-finite maxima take the reference loop
+// (tests/native/test_receiver_code.cu checks this against the loop).
+template <int CONN>
+__host__ __device__ __forceinline__ uint8_t receiver_code_hi(const double (&d)[8], const StepArgs& a) {
+  if (CONN == 8 && a.unit_card) {
+    int hi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool diag = (k == 0 || k == 2 || k == 5 || k == 7);
+      hi[k] = hi_word(diag ? LG_MUL(d[k], a.rinv_diag) : d[k]);
+    }
+    auto mx2 = [](int u, int v) { return u > v ? u : v; };
+    const int mx = mx2(mx2(mx2(hi[0], hi[1]), mx2(hi[2], hi[3])), mx2(mx2(hi[4], hi[5]), mx2(hi[6], hi[7])));
+    if (mx < 0) return kNoFlowCode;  // every drop negative or -0: no downhill neighbour
+    if (mx < 0x00100000) {           // no normal positive slope: +0 drops (flats) or subnormal ones
+      bool pos = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pos |= d[k] > 0.0;
+      return pos ? receiver_code_ref<CONN>(d, a) : kNoFlowCode;
+    }
+    if (mx >= 0x7FF00000) return receiver_code_ref<CONN>(d, a);
+    const int thr = mx - 1;
+    uint32_t cand = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cand |= (hi[k] >= thr ? 1u : 0u) << k;
+    if ((cand & (cand - 1u)) == 0) {  // a single candidate: the maximum
+#ifdef __CUDA_ARCH__
+      return (uint8_t)(__ffs(cand) - 1);
+#else
+      return (uint8_t)__builtin_ctz(cand);
+#endif
+    }
+    return receiver_code_ref<CONN>(d, a);
+  }
+  return receiver_code_ref<CONN>(d, a);
+}
+
 // ---- TMA (cp.async.bulk.tensor) staging of the h tile, mbarrier completion
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -205,7 +248,7 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
         d[6] = LG_SUB(ec, w2[1]);
         d[7] = LG_SUB(ec, w2[2]);
         if (CONN == 4) d[0] = d[2] = d[5] = d[7] = 0.0;
-        code = receiver_code<CONN>(d, a);
+        code = receiver_code_hi<CONN>(d, a);
       }
       rc[r][c] = code;
 #pragma unroll
@@ -224,7 +267,7 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
       double d[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) d[k] = dir_in(CONN, k) ? LG_SUB(ec, sh[r + 1 + dir_oy(k)][c + 1 + dir_ox(k)]) : 0.0;
-      code = receiver_code<CONN>(d, a);
+      code = receiver_code_hi<CONN>(d, a);
     }
     rc[r][c] = code;
   }
@@ -264,6 +307,28 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
           a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
           a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
+    }
+  }
+  // ---- bit planes of the receiver codes (k_tiles' level discovery): bit b
+  // of code (gx, gy) at planes[b][gy][gx / 32], one ballot per 32 columns;
+  // columns beyond W read as code 15 (no receiver, no source)
+  if (a.planes) {
+    for (int pr = warp; pr < kBY * (kBX / 32); pr += kNW) {
+      const int r = pr / (kBX / 32), wj = pr % (kBX / 32);
+      const uint32_t gy = y0 + r, gx = x0 + 32 * wj + lane;
+      if (gy >= Ht) continue;  // uniform in the warp
+      const uint32_t code = gx < W ? (uint32_t)rc[r + 1][32 * wj + lane + 1] : 15u;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, code & 1u), b1 = __ballot_sync(0xffffffffu, code & 2u);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, code & 4u), b3 = __ballot_sync(0xffffffffu, code & 8u);
+      const uint32_t j = x0 / 32 + wj;
+      if (lane == 0 && j < a.W32) {
+        const size_t ps = (size_t)Ht * a.W32;
+        uint32_t* pw = a.planes + (size_t)gy * a.W32 + j;
+        pw[0] = b0;
+        pw[ps] = b1;
+        pw[2 * ps] = b2;
+        pw[3 * ps] = b3;
+      }
     }
   }
   __syncthreads();

@@ -17,22 +17,22 @@
 // queue per worker over a slice of the sources; here the private queue
 // belongs to a CTA and the sources are the level-0 cells of a 64x32 tile.
 //
-// A CTA (persistent, looping over tiles) does, for its tile T:
-//   1. one TMA box brings h for T grown by 5 cells (kWY x kWP doubles);
-//   2. receiver codes for T grown by 4 cells (register sliding 3x3 window);
-//   3. donor masks for T grown by 3 cells (SWAR byte compares) = the domain;
-//      T's own rcode / dmask bytes go to HBM (they are the step's compact
-//      FlowGraph, used by the escape path and the parity export);
-//   4. bitmaps of the domain: cells by receiver direction, cells with a
-//      donor outside the domain, T's level-0 cells (one ballot per word);
-//   5. breadth first from T's level-0 cells: level l+1 = the domain cells
+// k_recv_donor has already written, for every cell, the receiver code, the
+// donor mask and the four bit planes of the code.  A CTA (persistent,
+// looping over tiles) does, for its tile T:
+//   1. one TMA box brings h for the BFS domain (T grown by kHalo cells); the
+//      codes of the domain and the ring around it are loaded, and the code
+//      bit planes are shifted to the window's word grid;
+//   2. bitmaps: domain cells with a receiver, T's level-0 cells (code 8), and
+//      the border cells that have a donor in the ring (outside the domain);
+//   3. breadth first from T's level-0 cells: level l+1 = the domain cells
 //      whose receiver is in level l, one bitmap pass per level (shift + and
 //      per direction), listed level-major (block prefix of the word counts):
 //      the level structure of the reference's TraversalPlan for T's sources;
-//   6. drainage area: exact cell counts (every cell adds 1 to each ancestor;
+//   4. drainage area: exact cell counts (every cell adds 1 to each ancestor;
 //      integer adds commute) or, for a cell area that is not exact, the
 //      reference's FP pull in slot order level by level;
-//   7. uplift + implicit erosion level by level (block barrier per level),
+//   5. uplift + implicit erosion level by level (block barrier per level),
 //      each cell reading its receiver's already updated elevation; the new
 //      elevations go to hout.
 // A tree with a cell whose donor lies outside the domain (its cells reach
@@ -54,100 +54,53 @@
 namespace lemgpu {
 
 // Window coordinates: column x, row y; q = y * kWP + x; global cell =
-// (wx0 + x, wy0 + y).
+// (wx0 + x, wy0 + y).  The tile T is columns [kLX, kLX+kTX) x rows [kLY,
+// kLY+kTY); the BFS domain is T grown by kHalo; the receiver codes of the
+// ring around the domain tell which domain cells have donors outside it.
 constexpr int kWP = 84;             // window pitch = TMA box width (doubles)
 constexpr int kLX = 8;              // first tile column in the window
 constexpr int kLY = kHalo + 2;      // first tile row in the window
 constexpr int kWY = kTY + 2 * kLY;  // window rows
-constexpr int kWN = kWY * kWP;      // window cells
 constexpr int kDX0 = kLX - kHalo, kDX1 = kLX + kTX + kHalo;  // domain columns [kDX0, kDX1)
 constexpr int kDY0 = kLY - kHalo, kDY1 = kLY + kTY + kHalo;  // domain rows
 constexpr int kDW = kDX1 - kDX0, kDH = kDY1 - kDY0;
-constexpr int kRX0 = kDX0 - 1, kRX1 = kDX1 + 1;  // receiver-code columns
-constexpr int kRY0 = kDY0 - 1, kRY1 = kDY1 + 1;  // receiver-code rows
-constexpr int kCap = kDW * kDH;                  // queue: every domain cell at most once
-constexpr int kTMaxLev = 64;                     // deeper trees escape
-constexpr int kRCols = kRX1 - kRX0;              // 72
-constexpr int kRSegs = kTTPB / kRCols;           // row segments of the receiver sweep (3)
-constexpr int kDGroups = (kRX1 - kRX0) / 4;      // 4-cell donor-mask groups per row (18)
-static_assert(kRX0 % 4 == 0 && (kRX1 - kRX0) % 4 == 0 && kWP % 4 == 0, "donor groups must be word aligned");
-static_assert(kLX % 4 == 0 && kTX % 4 == 0, "tile groups must be word aligned");
-static_assert(kRX1 + 1 <= kWP && kRY1 + 1 == kWY, "h window covers the receiver stencils");
-static_assert(kWN < 65535, "16-bit window indices");
+constexpr int kQ0 = kDY0 * kWP;          // q of the first domain row
+constexpr int kDN = kDH * kWP;           // per-cell arrays: the domain rows
+constexpr int kRN = (kDH + 2) * kWP;     // receiver codes: the domain rows and the ring rows
+constexpr int kCap = kDW * kDH;          // queue: every domain cell at most once
+constexpr int kTMaxLev = 64;             // deeper trees escape
+static_assert(kLX % 4 == 0 && kWP % 4 == 0 && kDX1 + 1 <= kWP, "window geometry");
+static_assert(kWY * kWP < 65535, "16-bit window indices");
 
 // Bitmaps of the window: row y, 32-column word w (columns 32w .. 32w+31).
 constexpr int kBW = 3;            // words per row (96 >= kWP columns)
 constexpr int kBN = kWY * kBW;    // words per bitmap
 constexpr int kBPairs = kDH * kBW;  // (row, word) pairs of the domain rows
 constexpr int kBWarps = (kBPairs + 31) / 32;  // warps holding them
-static_assert(kBW * 32 >= kWP && kBPairs <= kTTPB, "bitmap geometry");
+static_assert(kBW * 32 >= kWP && kBPairs <= kTTPB && (kDH + 2) * kBW <= kTTPB, "bitmap geometry");
 
 // EX: the drainage area is an exact multiple of the cell area (lut_exact), so
 // it is carried as an integer cell count and indexes the host-libm F table
 // directly; otherwise it is the reference's FP sum (f64).
 template <bool EX>
 struct TileSmem {
-  double hw[kWN];  // h window (TMA destination), updated in place by the erosion
-  typename std::conditional<EX, uint32_t, double>::type acc[kWN];  // drainage area: cell count (EX) or FP sum
+  double hw[kDN];  // h of the domain rows (TMA destination), updated in place by the erosion
+  typename std::conditional<EX, uint32_t, double>::type acc[kDN];  // drainage area: cell count (EX) or FP sum
   uint16_t list[kCap];         // the tile's queue, level-major
-  uint8_t rc[kWN + 8];         // receiver codes; the code of q is at q + 1
-  uint8_t dm[kWN];             // donor masks restricted to the domain
-  uint8_t fl[kWN];             // 1: some donor of the cell lies outside the domain
-  uint8_t esc[kWN];            // the cell's tree escapes (set on roots, inherited downstream -> upstream)
+  uint8_t rc[kRN];             // receiver codes of the domain and ring rows
+  uint8_t dm[EX ? 4 : kDN];    // donor masks (FP accumulation only)
+  uint8_t esc[kDN];            // the cell's tree escapes (set on roots, inherited downstream -> upstream)
   uint8_t rowint[kWY];         // window row holds interior cells
-  uint32_t pl[4][kBN];         // bit planes 0-2 of the receiver code, and "code < 8"
+  uint32_t pl[3][kBN];         // bit planes 0-2 of the receiver codes, aligned to the window
+  uint32_t vr[kBN];            // domain cells with a receiver (code < 8)
   uint32_t lk[kBN];            // domain cells with a donor outside the domain
   uint32_t wsum[2][kTTPB / 32];  // per-warp level counts (double-buffered by level parity)
   uint32_t lv[2][kBN];         // current / next level
   uint32_t lvs[kTMaxLev + 1];  // first queue position of each level
-  uint32_t nlev;
   uint64_t bar;
 };
 template <bool EX>
 constexpr size_t tiles_smem_bytes() { return sizeof(TileSmem<EX>); }
-
-// D8, unit cardinal spacing: receiver code without divisions.  t_k = d_k
-// (cardinal, exact) or RN(d_k * RN(1/sqrt2)) (diagonal, within 2^-51 relative
-// of the reference slope RN(d_k / sqrt2)).  The high words of positive
-// doubles order them; when exactly one t_k has a high word within 1 of the
-// largest, every other t_j is below it by more than 2^-22 relative, so it is
-// the unique strict maximum of the reference slopes as well.  Ties, near
-// ties, subnormal or non-finite maxima take the reference loop
-// (tests/native/test_receiver_code.cu checks this against the loop).
-template <int CONN>
-__host__ __device__ __forceinline__ uint8_t receiver_code_hi(const double (&d)[8], const StepArgs& a) {
-  if (CONN == 8 && a.unit_card) {
-    int hi[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const bool diag = (k == 0 || k == 2 || k == 5 || k == 7);
-      hi[k] = hi_word(diag ? LG_MUL(d[k], a.rinv_diag) : d[k]);
-    }
-    auto mx2 = [](int u, int v) { return u > v ? u : v; };
-    const int mx = mx2(mx2(mx2(hi[0], hi[1]), mx2(hi[2], hi[3])), mx2(mx2(hi[4], hi[5]), mx2(hi[6], hi[7])));
-    if (mx < 0) return kNoFlowCode;  // every drop negative or -0: no downhill neighbour
-    if (mx < 0x00100000) {           // no normal positive slope: +0 drops (flats) or subnormal ones
-      bool pos = false;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pos |= d[k] > 0.0;
-      return pos ? receiver_code_ref<CONN>(d, a) : kNoFlowCode;
-    }
-    if (mx >= 0x7FF00000) return receiver_code_ref<CONN>(d, a);
-    const int thr = mx - 1;
-    uint32_t cand = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) cand |= (hi[k] >= thr ? 1u : 0u) << k;
-    if ((cand & (cand - 1u)) == 0) {  // a single candidate: the maximum
-#ifdef __CUDA_ARCH__
-      return (uint8_t)(__ffs(cand) - 1);
-#else
-      return (uint8_t)__builtin_ctz(cand);
-#endif
-    }
-    return receiver_code_ref<CONN>(d, a);
-  }
-  return receiver_code_ref<CONN>(d, a);
-}
 
 // F = ((K*dt) * pow(A, m)) / pow(dist, n) (erosion.cpp:38-39) from the host
 // libm table when A is an exact multiple of the cell area.
@@ -162,7 +115,7 @@ __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32
 }
 
 template <int CONN, int NK, bool EX>
-__global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
+__global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char smraw[];
   TileSmem<EX>& s = *reinterpret_cast<TileSmem<EX>*>(smraw);
   Ctl* ctl = a.ctl;
@@ -174,12 +127,17 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
   const uint32_t E = a.lut_entries;
   const bool tab = EX && NK == 1 && a.tab_ok;
   if (tid == 0) {
-    atomicMin(&ctl->t_k1_begin, globaltimer());
+    atomicMin(&ctl->t_t_begin, globaltimer());
     if (a.use_tma) mbar_init(&s.bar, 1);
   }
   // the escape path's level-0 and level-1 bins start at zero
   for (uint32_t i = blockIdx.x * kTTPB + tid; i < 2 * a.scan_grid; i += gridDim.x * kTTPB) a.bins[i] = 0;
 
+#define HW(q) s.hw[(q) - kQ0]
+#define ACC(q) s.acc[(q) - kQ0]
+#define ESC(q) s.esc[(q) - kQ0]
+#define DM(q) s.dm[(q) - kQ0]
+#define RC(q) s.rc[(q) - (kDY0 - 1) * kWP]
   unsigned long long iters = 0;  // per thread
   uint32_t misses = 0, cells = 0, n0i = 0, maxl = 0;
   uint32_t phase = 0;
@@ -196,16 +154,65 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
     if (tid == 0 && a.use_tma) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of hw before the TMA overwrite
       mbar_expect_tx(&s.bar, (uint32_t)sizeof(s.hw));
-      tma_load_2d(s.hw, &hmap, wx0, wy0, &s.bar);  // out-of-raster cells arrive as 0
+      tma_load_2d(s.hw, &hmap, wx0, wy0 + kDY0, &s.bar);  // out-of-raster cells arrive as 0
     }
     if (!a.use_tma) {
-      for (int i = (int)tid; i < kWN; i += kTTPB) {
-        const int y = i / kWP, x = i - y * kWP;
+      for (int i = (int)tid; i < kDN; i += kTTPB) {
+        const int y = kDY0 + i / kWP, x = i % kWP;
         const int gx = wx0 + x, gy = wy0 + y;
         s.hw[i] = (gx >= 0 && gx < W && gy >= 0 && gy < Ht) ? __ldg(a.h + (size_t)gy * W + gx) : 0.0;
       }
     }
-    for (int i = (int)tid; i < (kWN + 8) / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.rc)[i] = 0x08080808u;
+    // receiver codes (and donor masks) of rows kDY0-1 .. kDY1 from k_recv_donor's
+    // output; cells outside the raster read as NoFlow
+    for (int i = (int)tid; i < kRN / 4; i += kTTPB) {
+      const int y = kDY0 - 1 + (4 * i) / kWP, x = (4 * i) % kWP;
+      const int gx = wx0 + x, gy = wy0 + y;
+      uint32_t v = 0x08080808u, m = 0;
+      if (gy >= 0 && gy < Ht) {
+        const size_t g = (size_t)gy * a.W + gx;
+        if (gx >= 0 && gx + 3 < W && (a.W & 3u) == 0) {
+          v = __ldg(reinterpret_cast<const uint32_t*>(a.rcode + g));
+          if (!EX) m = __ldg(reinterpret_cast<const uint32_t*>(a.dmask + g));
+        } else {
+          v = m = 0;
+          for (int j = 0; j < 4; ++j) {
+            const bool in = gx + j >= 0 && gx + j < W;
+            v |= (in ? (uint32_t)a.rcode[g + j] : 8u) << (8 * j);
+            if (!EX) m |= (in ? (uint32_t)a.dmask[g + j] : 0u) << (8 * j);
+          }
+        }
+      }
+      reinterpret_cast<uint32_t*>(s.rc)[i] = v;
+      if (!EX && y >= kDY0 && y < kDY1) reinterpret_cast<uint32_t*>(s.dm)[i - kWP / 4] = m;
+    }
+    // bit planes 0-2 of the codes, shifted to the window's columns (rows kDY0-1 .. kDY1);
+    // outside the raster every plane reads 1 (code 15)
+    if (tid < (uint32_t)((kDH + 2) * kBW)) {
+      const int yy = (int)tid / kBW, w = (int)tid % kBW, y = kDY0 - 1 + yy;
+      const int gy = wy0 + y, gx = wx0 + 32 * w;
+      const int j = gx >> 5, sh = gx & 31;
+      uint32_t pw[4];
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) {
+        const uint32_t* row = a.planes + ((size_t)pl * a.Htot + (gy >= 0 && gy < Ht ? gy : 0)) * a.W32;
+        const bool rin = gy >= 0 && gy < Ht;
+        const uint32_t lo = (rin && j >= 0 && j < (int)a.W32) ? __ldg(row + j) : ~0u;
+        const uint32_t hi = (rin && j + 1 >= 0 && j + 1 < (int)a.W32) ? __ldg(row + j + 1) : ~0u;
+        pw[pl] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+      }
+      const int o = y * kBW + w;
+      s.pl[0][o] = pw[0];
+      s.pl[1][o] = pw[1];
+      s.pl[2][o] = pw[2];
+      // domain cells with a receiver, and the tile's level-0 cells (code 8)
+      const uint32_t dom = (y >= kDY0 && y < kDY1) ? (w == 0 ? (~0u << kDX0) : w == 1 ? ~0u : ((1u << (kDX1 - 64)) - 1u)) : 0u;
+      const uint32_t til = (y >= kLY && y < kLY + kTY) ? (w == 0 ? (~0u << kLX) : w == 1 ? ~0u : ((1u << (kLX + kTX - 64)) - 1u)) : 0u;
+      s.vr[o] = ~pw[3] & dom;
+      s.lv[0][o] = pw[3] & ~pw[0] & ~pw[1] & ~pw[2] & til;
+      s.lv[1][o] = 0u;  // rows outside the domain stay empty in both level buffers
+      s.lk[o] = 0u;
+    }
     if (tid < (uint32_t)kWY) {
       const int gy = wy0 + (int)tid;
       uint8_t ok = 0;
@@ -215,133 +222,30 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
       }
       s.rowint[tid] = ok;
     }
-    __syncthreads();
-    if (a.use_tma) mbar_wait(&s.bar, phase);
-
-    // ---- 2. receiver codes: one column per thread, 3x3 register window
-    // sliding down (unrolled by three rows so the window never moves registers)
-    if (tid < (uint32_t)(kRCols * kRSegs)) {
-      const int x = kRX0 + (int)(tid % kRCols), seg = (int)(tid / kRCols);
-      const int nrow = kRY1 - kRY0;
-      const int yb = kRY0 + seg * nrow / kRSegs, ye = kRY0 + (seg + 1) * nrow / kRSegs;
-      const int gx = wx0 + x;
-      const bool colint = gx > 0 && gx < W - 1;
-      const double* col = s.hw + x - 1;
-      uint8_t* rcol = s.rc + x + 1;
-      auto emit = [&](int y, const double (&u)[3], const double (&m)[3], const double (&v)[3]) {
-        uint8_t code = kNoFlowCode;
-        if (colint && s.rowint[y]) {
-          const double ec = m[1];
-          double d[8];
-          d[0] = __dsub_rn(ec, u[0]);
-          d[1] = __dsub_rn(ec, u[1]);
-          d[2] = __dsub_rn(ec, u[2]);
-          d[3] = __dsub_rn(ec, m[0]);
-          d[4] = __dsub_rn(ec, m[2]);
-          d[5] = __dsub_rn(ec, v[0]);
-          d[6] = __dsub_rn(ec, v[1]);
-          d[7] = __dsub_rn(ec, v[2]);
-          if (CONN == 4) d[0] = d[2] = d[5] = d[7] = 0.0;
-          code = receiver_code_hi<CONN>(d, a);
-        }
-        rcol[y * kWP] = code;
-      };
-      auto load = [&](double (&r)[3], int y) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) r[q] = col[y * kWP + q];
-      };
-      double r0[3], r1[3], r2[3];
-      load(r0, yb - 1);
-      load(r1, yb);
-      int y = yb;
-      for (; y + 3 <= ye; y += 3) {
-        load(r2, y + 1);
-        emit(y, r0, r1, r2);
-        load(r0, y + 2);
-        emit(y + 1, r1, r2, r0);
-        load(r1, y + 3);
-        emit(y + 2, r2, r0, r1);
-      }
-      if (y < ye) {
-        load(r2, y + 1);
-        emit(y, r0, r1, r2);
-        if (y + 1 < ye) {
-          load(r0, y + 2);
-          emit(y + 1, r1, r2, r0);
-        }
-      }
+    if (tid < (uint32_t)(2 * kBW)) {  // rows 0 and kWY-1: never part of a level
+      const int o = (tid < kBW ? 0 : (kWY - 1) * kBW) + (int)(tid % kBW);
+      s.lv[0][o] = s.lv[1][o] = 0u;
     }
     __syncthreads();
-
-    // ---- 3. donor masks of the domain (4 cells per item), restricted to the
-    // domain, with a per-cell flag for donors outside it; the tile's own
-    // receiver codes and (complete) donor masks go to HBM
-    for (int it = (int)tid; it < kDH * kDGroups; it += kTTPB) {
-      const int y = kDY0 + it / kDGroups, x = kRX0 + 4 * (it % kDGroups);
-      uint32_t lo[3], hi[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        lo[q] = *reinterpret_cast<const uint32_t*>(s.rc + (y - 1 + q) * kWP + x);
-        hi[q] = *reinterpret_cast<const uint32_t*>(s.rc + (y - 1 + q) * kWP + x + 4);
-      }
-      uint32_t pm = 0;
+    // domain cells on the border with a donor in the ring outside the domain
+    for (int i = (int)tid; i < 2 * (kDW + kDH); i += kTTPB) {
+      int x, y;
+      if (i < kDW) { x = kDX0 + i; y = kDY0; }
+      else if (i < 2 * kDW) { x = kDX0 + i - kDW; y = kDY1 - 1; }
+      else if (i < 2 * kDW + kDH) { x = kDX0; y = kDY0 + i - 2 * kDW; }
+      else { x = kDX1 - 1; y = kDY0 + i - 2 * kDW - kDH; }
+      const int q = y * kWP + x;
+      bool leak = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (!dir_in(CONN, k)) continue;
-        const int q = 1 + dir_oy(k);
-        const uint32_t sel = dir_ox(k) < 0 ? 0x3210u : dir_ox(k) == 0 ? 0x4321u : 0x5432u;
-        pm |= zero_bytes(__byte_perm(lo[q], hi[q], sel) ^ (0x01010101u * (uint32_t)(7 - k))) << k;
+        const int nx = x + dir_ox(k), ny = y + dir_oy(k);
+        if (nx >= kDX0 && nx < kDX1 && ny >= kDY0 && ny < kDY1) continue;
+        leak |= s.rc[q + dir_off(k, kWP) - (kDY0 - 1) * kWP] == (uint8_t)(7 - k);
       }
-      // directions that stay inside the domain, per byte
-      uint32_t dd = 0xFFFFFFFFu;
-      if (x == kRX0) dd &= ~(0x29u << 8);       // cell x+1 = kDX0: no ox = -1
-      if (x + 4 == kRX1) dd &= ~(0x94u << 16);  // cell x+2 = kDX1-1: no ox = +1
-      if (y == kDY0) dd &= ~0x07070707u;        // no oy = -1
-      if (y == kDY1 - 1) dd &= ~0xE0E0E0E0u;    // no oy = +1
-      *reinterpret_cast<uint32_t*>(s.dm + y * kWP + x) = pm & dd;
-      *reinterpret_cast<uint32_t*>(s.fl + y * kWP + x) = ~zero_bytes(pm & ~dd) & 0x01010101u;
-      if (y >= kLY && y < kLY + kTY && x >= kLX && x < kLX + kTX) {
-        const int gy = wy0 + y, gx = wx0 + x;
-        if (gy < Ht && gx < W) {
-          const uint32_t pc = __byte_perm(lo[1], hi[1], 0x4321u);
-          const size_t base = (size_t)gy * a.W + gx;
-          if (gx + 3 < W && (a.W & 3u) == 0) {
-            *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
-            *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
-          } else {
-            for (int j = 0; j < 4 && gx + j < W; ++j) {
-              a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
-              a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
-            }
-          }
-        }
-      }
+      if (leak) atomicOr(&s.lk[y * kBW + (x >> 5)], 1u << (x & 31));
     }
-    __syncthreads();
-    // ---- 4. bitmaps of the domain: the four bit planes of the receiver code
-    // (code 15 outside the domain), cells with leaking donors, and the
-    // tile's roots (level 0); one ballot per (row, word) and bitmap
-    for (uint32_t pr = tid >> 5; pr < (uint32_t)kBN; pr += kTTPB / 32) {
-      const uint32_t y = pr / kBW, w = pr - y * kBW, x = 32 * w + lane;
-      const uint32_t q = y * kWP + x;
-      const bool dom = y - kDY0 < (uint32_t)kDH && x - kDX0 < (uint32_t)kDW;
-      const uint32_t code = dom ? (uint32_t)s.rc[q + 1] : 0xFu;
-      const int gx = wx0 + (int)x, gy = wy0 + (int)y;
-      const bool root = code == kNoFlowCode && x - kLX < (uint32_t)kTX && y - kLY < (uint32_t)kTY && gx < W && gy < Ht;
-      const uint32_t b0 = __ballot_sync(0xffffffffu, code & 1u), b1 = __ballot_sync(0xffffffffu, code & 2u);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, code & 4u), b3 = __ballot_sync(0xffffffffu, code & 8u);
-      const uint32_t bl = __ballot_sync(0xffffffffu, dom && s.fl[q]);
-      const uint32_t br = __ballot_sync(0xffffffffu, root);
-      if (lane == 0) {
-        s.pl[0][pr] = b0;
-        s.pl[1][pr] = b1;
-        s.pl[2][pr] = b2;
-        s.pl[3][pr] = ~b3;  // cells with a receiver direction 0..7
-        s.lk[pr] = bl;
-        s.lv[0][pr] = br;
-        s.lv[1][pr] = 0u;  // rows outside the domain stay empty in both level buffers
-      }
-    }
+    if (a.use_tma) mbar_wait(&s.bar, phase);
     __syncthreads();
     // ---- 5. the levels, breadth first from the tile's roots: level l+1 =
     // the domain cells whose receiver is in level l (one bitmap pass per
@@ -377,7 +281,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
             const uint32_t rk = ((k & 1) ? p0 : ~p0) & ((k & 2) ? p1 : ~p1) & ((k & 4) ? p2 : ~p2);
             word |= rk & sh[dir_oy(k) + 1][dir_ox(k) + 1];
           }
-          word &= s.pl[3][o];
+          word &= s.vr[o];
         }
       }
       const uint32_t cnt = __popc(word);
@@ -408,15 +312,15 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
           word &= word - 1;
           const uint32_t q = y * kWP + 32 * w + b;
           s.list[pos++] = (uint16_t)q;
-          s.esc[q] = 0;
-          if (EX) s.acc[q] = 1u;
+          ESC(q) = 0;
+          if (EX) ACC(q) = 1u;
           if ((leaks >> b) & 1u) {  // a donor outside the domain: the tree escapes
-            uint32_t r = q, code = s.rc[q + 1];
+            uint32_t r = q, code = RC(q);
             while (code != kNoFlowCode) {
               r = (uint32_t)((int)r + dir_off(code, kWP));
-              code = s.rc[r + 1];
+              code = RC(r);
             }
-            s.esc[r] = 1;
+            ESC(r) = 1;
           }
         }
       }
@@ -430,20 +334,20 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
       // level kTMaxLev would not be empty: every tree reaching it escapes
       for (uint32_t i = s.lvs[nl - 1] + tid; i < s.lvs[nl]; i += kTTPB) {
         uint32_t r = s.list[i];
-        if (!s.dm[r]) continue;
-        uint32_t code = s.rc[r + 1];
+        if (!a.dmask[gcell(r)]) continue;  // no donors: the tree ends here
+        uint32_t code = RC(r);
         while (code != kNoFlowCode) {
           r = (uint32_t)((int)r + dir_off(code, kWP));
-          code = s.rc[r + 1];
+          code = RC(r);
         }
-        s.esc[r] = 1;
+        ESC(r) = 1;
       }
       __syncthreads();
     }
     if (a.force_escape) {
       for (uint32_t i = s.lvs[0] + tid; i < s.lvs[nl > 0 ? 1 : 0]; i += kTTPB) {
         const uint32_t q = s.list[i];
-        if (a.force_escape == 1 || (gcell(q) & 1u)) s.esc[q] = 1;
+        if (a.force_escape == 1 || (gcell(q) & 1u)) ESC(q) = 1;
       }
       __syncthreads();
     }
@@ -451,11 +355,11 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
     if (EX) {
       // cell counts: every cell adds 1 to each ancestor (integer adds commute)
       for (uint32_t i = (nl > 1 ? s.lvs[1] : 0u) + tid; i < (nl > 1 ? s.lvs[nl] : 0u); i += kTTPB) {
-        uint32_t p = s.list[i], code = s.rc[p + 1];
+        uint32_t p = s.list[i], code = RC(p);
         do {
           p = (uint32_t)((int)p + dir_off(code, kWP));
-          atomicAdd(reinterpret_cast<uint32_t*>(&s.acc[p]), 1u);
-          code = s.rc[p + 1];
+          atomicAdd(reinterpret_cast<uint32_t*>(&ACC(p)), 1u);
+          code = RC(p);
         } while (code != kNoFlowCode);
       }
       __syncthreads();
@@ -465,14 +369,14 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
       for (int l = (int)nl - 1; l >= 0; --l) {
         for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) {
           const uint32_t q = s.list[i];
-          uint32_t m = s.dm[q];
+          uint32_t m = DM(q);
           double A = a.w0;
           while (m) {
             const uint32_t k = __ffs(m) - 1;
             m &= m - 1;
-            A = __dadd_rn(A, (double)s.acc[(int)q + dir_off(k, kWP)]);
+            A = __dadd_rn(A, (double)ACC((int)q + dir_off(k, kWP)));
           }
-          s.acc[q] = A;
+          ACC(q) = A;
         }
         __syncthreads();
       }
@@ -490,12 +394,12 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
         const int gx = wx0 + (int)x;
         const bool inter = s.rowint[y] && gx > 0 && gx < W - 1;  // interior NoFlow cell (simulation.cpp:42-44)
         n0i += inter ? 1u : 0u;
-        e = s.esc[q] != 0;
+        e = ESC(q) != 0;
         if (!e) {
-          double hv = s.hw[q];
+          double hv = HW(q);
           if (inter) {
             hv = __dadd_rn(hv, a.du);
-            s.hw[q] = hv;
+            HW(q) = hv;
           }
           a.hout[gc] = hv;
           ++cells;
@@ -516,10 +420,10 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
       bool any = false;
       for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) {
         const uint32_t q = s.list[i];
-        const uint32_t code = s.rc[q + 1];
+        const uint32_t code = RC(q);
         const uint32_t p = (uint32_t)((int)q + dir_off(code, kWP));
-        if (s.esc[p]) {  // the tree escapes: inherit the mark, leave the cell to the level path
-          s.esc[q] = 1;
+        if (ESC(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
+          ESC(q) = 1;
           continue;
         }
         any = true;
@@ -527,20 +431,20 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
         uint32_t mem = 0;
         if (a.M > 1) mem = (uint32_t)(wy0 + (int)(q / kWP)) / a.H;
         const uint32_t cls = dir_class(code);  // class of dist(c, rec[c])
-        const double h0 = __dadd_rn(s.hw[q], a.du);  // uplift (every cell below level 0 is interior)
-        const double hn = s.hw[p];
+        const double h0 = __dadd_rn(HW(q), a.du);  // uplift (every cell below level 0 is interior)
+        const double hn = HW(p);
         int itn;
         bool ok;
         double hnew;
         if (tab) {
-          const double2 fy = __ldg(reinterpret_cast<const double2*>(a.ftab2) + (mem * 3 + cls) * E + (uint32_t)s.acc[q]);
+          const double2 fy = __ldg(reinterpret_cast<const double2*>(a.ftab2) + (mem * 3 + cls) * E + (uint32_t)ACC(q));
           hnew = newton_n1_tab(h0, hn, fy.x, fy.y, a.eps, a.maxit, itn, ok);
         } else {
           double F;
           if (EX)
-            F = __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)s.acc[q]);
+            F = __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)ACC(q));
           else
-            F = tile_F(a, mem, cls, (double)s.acc[q], misses);
+            F = tile_F(a, mem, cls, (double)ACC(q), misses);
           if (NK == 1)
             hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
           else
@@ -554,7 +458,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
           ctl->err_slot = ctl->slot;
           atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
         }
-        s.hw[q] = hnew;
+        HW(q) = hnew;
         a.hout[gc] = hnew;
       }
       if (__syncthreads_or(any)) maxl = max(maxl, l + 1);
@@ -562,6 +466,11 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
     if (nl) maxl = max(maxl, 1u);
   }
 
+#undef HW
+#undef ACC
+#undef ESC
+#undef DM
+#undef RC
   // ---- counters: one atomic per warp for the whole kernel
   for (int o = 16; o; o >>= 1) {
     iters += __shfl_down_sync(0xffffffffu, iters, o);
@@ -577,7 +486,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 3 : 2) k_tiles(StepArgs a, const _
   }
   if (tid == 0) atomicMax(&ctl->tile_nlev, maxl);
   __syncthreads();
-  if (tid == 0) atomicMax(&ctl->t_k1_end, globaltimer());
+  if (tid == 0) atomicMax(&ctl->t_t_end, globaltimer());
 }
 
 // Level 0 of the escape path: the escaped roots (listed by k_tiles in
@@ -599,7 +508,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_l0(StepArgs a) {
     ctl->n0 = n;
     ctl->nch = (n + kChunkRoots - 1) / kChunkRoots;
     ctl->lvl = 0;
-    ctl->t_k1_end = max(ctl->t_k1_end, globaltimer());
+    ctl->t_t_end = max(ctl->t_t_end, globaltimer());
     timeline(ctl);
   }
 }

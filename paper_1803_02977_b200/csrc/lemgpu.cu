@@ -37,6 +37,7 @@ struct lemgpu_ctx {
   lemgpu_params params{};
   std::vector<lemgpu_member> members;
   int scan_grid = 0, chunk_grid = 0, deep_grid = 0, tile_grid = 0;
+  int esc_grid = 0;  // CTAs of the level expansion of the escaped trees (a small workload)
   int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
   // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
   // graph[p] / exec[p] is the step that reads hbuf[p]
@@ -62,7 +63,7 @@ struct lemgpu_ctx {
   // timing: CUDA events around each graph launch + device phase stamps
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per pending step
-  double kernel_ms[4] = {0, 0, 0, 0};  // step, recv_donor, order, accumulation+uplift+erosion
+  double kernel_ms[5] = {0, 0, 0, 0, 0};  // step, recv_donor, order (escape), physics (escape), k_tiles
   uint32_t kernel_launches = 0;
   // errors
   std::string msg;
@@ -186,6 +187,8 @@ StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
   a.tiles = ctx->use_tiles;
   a.levels = ctx->use_tiles ? ctx->d_levels_esc : ctx->a.levels;
   a.expect_cells = ctx->use_tiles ? 0u : a.N;
+  if (ctx->use_tiles) a.scan_grid = (uint32_t)ctx->esc_grid;
+  if (!ctx->use_tiles) a.planes = nullptr;  // only k_tiles reads the code bit planes
   return a;
 }
 
@@ -216,9 +219,10 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   int rc;
   const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
   if (ctx->use_tiles) {
-    if ((rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
+    if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
+        (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
-        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_l0, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_l0, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr)))
       return rc;
   } else {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
@@ -226,7 +230,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
         (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
       return rc;
   }
-  if ((rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(ctx->scan_grid), 0, &a)) ||
+  if ((rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a)) ||
       (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
       (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
       (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
@@ -336,7 +340,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if ((rc = dmalloc(ctx, &ctx->d_kdt, M)) || (rc = dmalloc(ctx, &ctx->d_mexp, M)) ||
       (rc = dmalloc(ctx, &ctx->d_lut, lut.size())) || (rc = dmalloc(ctx, &ctx->d_lut2, 2 * lut.size())) || (rc = dmalloc(ctx, &ctx->hbuf[0], N)) ||
       (rc = dmalloc(ctx, &ctx->hbuf[1], N)) || (rc = dmalloc(ctx, &ctx->d_levels_esc, (size_t)N + 2)) ||
-      (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
+      (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) ||
+      (rc = dmalloc(ctx, &a.planes, (size_t)4 * H * M * ((W + 31) / 32))) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
       (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
       (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) ||
       (rc = dmalloc(ctx, &a.cbound, ((size_t)N / kChunkRoots + 2) * kCBS)) ||
@@ -348,6 +353,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     return bail(rc);
   a.h = ctx->hbuf[0];
   a.hout = ctx->hbuf[1];
+  a.W32 = (W + 31) / 32;
   a.kdt = ctx->d_kdt;
   a.mexp = ctx->d_mexp;
   a.ftab = ctx->d_lut;
@@ -386,6 +392,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   c0.err_cell = LEMGPU_NOFLOW;
   c0.t_k1_begin = ~0ull;
   c0.t_k1_end = 0;
+  c0.t_t_begin = ~0ull;
+  c0.t_t_end = 0;
   CUB(cudaMemcpy(a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
 
   // launch geometry
@@ -394,6 +402,9 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->scan_grid = (occ > 0 ? occ : 1) * nsm;
   if (ctx->scan_grid > 4096) ctx->scan_grid = 4096;  // part/bins capacity
   ctx->use_tiles = 1;
+  ctx->esc_grid = nsm;
+  if (const char* env = std::getenv("LEMGPU_ESC_GRID")) ctx->esc_grid = std::atoi(env);
+  if (ctx->esc_grid < 1 || ctx->esc_grid > ctx->scan_grid) ctx->esc_grid = ctx->scan_grid;
   if (const char* env = std::getenv("LEMGPU_PATH")) ctx->use_tiles = std::strcmp(env, "global") != 0;
   a.force_escape = 0;
   if (const char* env = std::getenv("LEMGPU_FORCE_ESCAPE")) a.force_escape = std::atoi(env);
@@ -431,7 +442,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
       const cuuint64_t gdim[2] = {W, (cuuint64_t)H * M};
       const cuuint64_t gstride[1] = {(cuuint64_t)W * sizeof(double)};
       const cuuint32_t box_r[2] = {kBX + 4, kBY + 4};
-      const cuuint32_t box_t[2] = {kWP, kWY};
+      const cuuint32_t box_t[2] = {kWP, kDH};
       const cuuint32_t estr[2] = {1, 1};
       bool ok = true;
       for (int p = 0; p < 2; ++p) {
@@ -464,7 +475,7 @@ int run_levels_eager(lemgpu_ctx* ctx, const StepArgs& a) {
   char* cbase = reinterpret_cast<char*>(a.ctl) + co;
   unsigned cond[3] = {1, 0, 0};
   while (cond[0]) {
-    k_expand<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    k_expand<<<a.scan_grid, kTPB, 0, st>>>(a);
     CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
     CU(ctx, cudaStreamSynchronize(st));
   }
@@ -509,6 +520,11 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   cudaStream_t st = ctx->stream;
   set_eager_conds(a, st);
   if (ctx->use_tiles) {
+    const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+    if (a.conn == 8)
+      k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+    else
+      k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->tile_grid);
     cfg.blockDim = dim3(kTTPB);
@@ -516,7 +532,7 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     cfg.stream = st;
     void* args[] = {&a, &ctx->tmap[p]};
     CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
-    k_esc_l0<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    k_esc_l0<<<a.scan_grid, kTPB, 0, st>>>(a);
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
@@ -581,7 +597,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   StepArgs& a = ctx->a;
-  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->d_lut2, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode,  a.dmask, a.order,
+  void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->d_lut2, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode, a.planes,  a.dmask, a.order,
                   a.ppos,     a.cdir,      a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
@@ -683,6 +699,7 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
       ctx->kernel_ms[1] += d[s].seconds[LEMGPU_PHASE_RECEIVERS] * 1e3;
       ctx->kernel_ms[2] += d[s].seconds[LEMGPU_PHASE_ORDER] * 1e3;
       ctx->kernel_ms[3] += d[s].seconds[LEMGPU_PHASE_EROSION] * 1e3;
+      ctx->kernel_ms[4] += d[s].seconds[LEMGPU_PHASE_ACCUM] * 1e3;
     }
     ctx->kernel_launches += n;
   }
@@ -862,7 +879,7 @@ int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable) {
 
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches) {
   if (!ctx || !ms) return LEMGPU_ECONFIG;
-  for (int i = 0; i < 4; ++i) ms[i] = ctx->kernel_ms[i];
+  for (int i = 0; i < 5; ++i) ms[i] = ctx->kernel_ms[i];
   if (launches) *launches = ctx->kernel_launches;
   return LEMGPU_OK;
 }

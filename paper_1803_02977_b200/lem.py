@@ -353,10 +353,11 @@ class DeviceContext:
         self._check(self._L.lemgpu_kernel_timing(self._h, 1 if enable else 0))
 
     def kernel_times(self):
-        ms = (C.c_double * 4)()
+        ms = (C.c_double * 5)()
         n = C.c_uint32(0)
         self._check(self._L.lemgpu_kernel_times(self._h, ms, C.byref(n)))
-        return {"step": ms[0], "recv_donor": ms[1], "order": ms[2], "physics": ms[3], "launches": n.value}
+        return {"step": ms[0], "recv_donor": ms[1], "order": ms[2], "physics": ms[3], "tiles": ms[4],
+                "launches": n.value}
 
     def debug_timeline(self):
         """k_flow barrier timestamps of the last step, as ms offsets from its start."""
