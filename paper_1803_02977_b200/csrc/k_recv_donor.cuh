@@ -224,37 +224,48 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
     const int rend = (tid < kBX) ? (kBY + 2) / 2 : kBY + 2;
     const int gx = (int)x0 - 1 + c;
     const bool colint = gx > 0 && gx < (int)W - 1;
-    // window rows: w0 = sh row r, w1 = r+1, w2 = r+2 (sh col c..c+2)
-    double w0[3], w1[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      w0[q] = sh[rbeg][c + q];
-      w1[q] = sh[rbeg + 1][c + q];
-    }
-    for (int r = rbeg; r < rend; ++r) {
-      double w2[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) w2[q] = sh[r + 2][c + q];
+    // window rows u = sh row r, m = r+1, v = r+2 (sh columns c..c+2),
+    // unrolled by three rows so the window never moves registers
+    auto emit = [&](int r, const double (&u)[3], const double (&m)[3], const double (&v)[3]) {
       uint8_t code = kNoFlowCode;
       if (colint && rowint[r]) {
-        const double ec = w1[1];
+        const double ec = m[1];
         double d[8];
-        d[0] = LG_SUB(ec, w0[0]);
-        d[1] = LG_SUB(ec, w0[1]);
-        d[2] = LG_SUB(ec, w0[2]);
-        d[3] = LG_SUB(ec, w1[0]);
-        d[4] = LG_SUB(ec, w1[2]);
-        d[5] = LG_SUB(ec, w2[0]);
-        d[6] = LG_SUB(ec, w2[1]);
-        d[7] = LG_SUB(ec, w2[2]);
+        d[0] = LG_SUB(ec, u[0]);
+        d[1] = LG_SUB(ec, u[1]);
+        d[2] = LG_SUB(ec, u[2]);
+        d[3] = LG_SUB(ec, m[0]);
+        d[4] = LG_SUB(ec, m[2]);
+        d[5] = LG_SUB(ec, v[0]);
+        d[6] = LG_SUB(ec, v[1]);
+        d[7] = LG_SUB(ec, v[2]);
         if (CONN == 4) d[0] = d[2] = d[5] = d[7] = 0.0;
         code = receiver_code_hi<CONN>(d, a);
       }
       rc[r][c] = code;
+    };
+    auto load = [&](double (&w)[3], int row) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        w0[q] = w1[q];
-        w1[q] = w2[q];
+      for (int q = 0; q < 3; ++q) w[q] = sh[row][c + q];
+    };
+    double r0[3], r1[3], r2[3];
+    load(r0, rbeg);
+    load(r1, rbeg + 1);
+    int r = rbeg;
+    for (; r + 3 <= rend; r += 3) {
+      load(r2, r + 2);
+      emit(r, r0, r1, r2);
+      load(r0, r + 3);
+      emit(r + 1, r1, r2, r0);
+      load(r1, r + 4);
+      emit(r + 2, r2, r0, r1);
+    }
+    if (r < rend) {
+      load(r2, r + 2);
+      emit(r, r0, r1, r2);
+      if (r + 1 < rend) {
+        load(r0, r + 3);
+        emit(r + 1, r1, r2, r0);
       }
     }
   }
@@ -296,6 +307,23 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
       pm |= zero_bytes(win ^ (0x01010101u * (uint32_t)(7 - k))) << k;
     }
     const uint32_t pc = __byte_perm(lo[1], hi[1], 0x4321u);
+    // bit planes of the receiver codes (k_tiles' level discovery): bit b of
+    // code (gx, gy) at planes[b][gy][gx / 32]; columns beyond W read as code
+    // 15 (no receiver, no source).  16 ballots per row, 16 lanes store.
+    if (a.planes) {
+      uint32_t mine = 0;
+#pragma unroll
+      for (int wj = 0; wj < kBX / 32; ++wj) {
+        const uint32_t code = x0 + 32 * wj + lane < W ? (uint32_t)rc[r + 1][32 * wj + lane + 1] : 15u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t v = __ballot_sync(0xffffffffu, (code >> b) & 1u);
+          if (lane == (uint32_t)(4 * wj + b)) mine = v;
+        }
+      }
+      const uint32_t j = x0 / 32 + (lane >> 2);
+      if (lane < 16 && j < a.W32) a.planes[((size_t)(lane & 3) * Ht + gy) * a.W32 + j] = mine;
+    }
     const uint32_t gx = x0 + c4;
     const size_t base = (size_t)gy * W + gx;
     if (gx + 3 < W && (W & 3) == 0) {
@@ -307,28 +335,6 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
           a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
           a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
-    }
-  }
-  // ---- bit planes of the receiver codes (k_tiles' level discovery): bit b
-  // of code (gx, gy) at planes[b][gy][gx / 32], one ballot per 32 columns;
-  // columns beyond W read as code 15 (no receiver, no source)
-  if (a.planes) {
-    for (int pr = warp; pr < kBY * (kBX / 32); pr += kNW) {
-      const int r = pr / (kBX / 32), wj = pr % (kBX / 32);
-      const uint32_t gy = y0 + r, gx = x0 + 32 * wj + lane;
-      if (gy >= Ht) continue;  // uniform in the warp
-      const uint32_t code = gx < W ? (uint32_t)rc[r + 1][32 * wj + lane + 1] : 15u;
-      const uint32_t b0 = __ballot_sync(0xffffffffu, code & 1u), b1 = __ballot_sync(0xffffffffu, code & 2u);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, code & 4u), b3 = __ballot_sync(0xffffffffu, code & 8u);
-      const uint32_t j = x0 / 32 + wj;
-      if (lane == 0 && j < a.W32) {
-        const size_t ps = (size_t)Ht * a.W32;
-        uint32_t* pw = a.planes + (size_t)gy * a.W32 + j;
-        pw[0] = b0;
-        pw[ps] = b1;
-        pw[2 * ps] = b2;
-        pw[3 * ps] = b3;
-      }
     }
   }
   __syncthreads();
