@@ -69,8 +69,17 @@ constexpr int kDN = kDH * kWP;           // per-cell arrays: the domain rows
 constexpr int kRN = (kDH + 2) * kWP;     // receiver codes: the domain rows and the ring rows
 constexpr int kCap = kDW * kDH;          // queue: every domain cell at most once
 constexpr int kTMaxLev = 64;             // deeper trees escape
+#ifndef LEMGPU_SMALL_BFS
+#define LEMGPU_SMALL_BFS 32
+#endif
+#ifndef LEMGPU_SMALL_ERO
+#define LEMGPU_SMALL_ERO 32
+#endif
+constexpr int kSmallLevel = LEMGPU_SMALL_BFS;  // levels this small are expanded by one warp
+constexpr int kSmallEro = LEMGPU_SMALL_ERO;    // erosion levels this small (in total) run on one warp
 static_assert(kLX % 4 == 0 && kWP % 4 == 0 && kDX1 + 1 <= kWP, "window geometry");
 static_assert(kWY * kWP < 65535, "16-bit window indices");
+static_assert(kDN % 4 == 0, "vector fills of the per-cell arrays");
 
 // Bitmaps of the window: row y, 32-column word w (columns 32w .. 32w+31).
 constexpr int kBW = 3;            // words per row (96 >= kWP columns)
@@ -85,11 +94,11 @@ static_assert(kBW * 32 >= kWP && kBPairs <= kTTPB && (kDH + 2) * kBW <= kTTPB, "
 template <bool EX>
 struct TileSmem {
   double hw[kDN];  // h of the domain rows (TMA destination), updated in place by the erosion
-  typename std::conditional<EX, uint32_t, double>::type acc[kDN];  // drainage area: cell count (EX) or FP sum
+  alignas(16) typename std::conditional<EX, uint32_t, double>::type acc[kDN];  // drainage area: cell count (EX) or FP sum
   uint16_t list[kCap];         // the tile's queue, level-major
   uint8_t rc[kRN];             // receiver codes of the domain and ring rows
   uint8_t dm[EX ? 4 : kDN];    // donor masks (FP accumulation only)
-  uint8_t esc[kDN];            // the cell's tree escapes (set on roots, inherited downstream -> upstream)
+  alignas(16) uint8_t esc[kDN];  // the cell's tree escapes (set on roots, inherited downstream -> upstream)
   uint8_t rowint[kWY];         // window row holds interior cells
   uint32_t pl[3][kBN];         // bit planes 0-2 of the receiver codes, aligned to the window
   uint32_t vr[kBN];            // domain cells with a receiver (code < 8)
@@ -101,6 +110,13 @@ struct TileSmem {
 };
 template <bool EX>
 constexpr size_t tiles_smem_bytes() { return sizeof(TileSmem<EX>); }
+
+// Window-index offset of direction k (0..7, stencil order): one byte permute
+// of the packed table (offset + 128 per byte).
+constexpr uint32_t woff_b(int k) { return (uint32_t)(128 + dir_ox(k) + dir_oy(k) * kWP); }
+constexpr uint32_t kWOffLo = woff_b(0) | woff_b(1) << 8 | woff_b(2) << 16 | woff_b(3) << 24;
+constexpr uint32_t kWOffHi = woff_b(4) | woff_b(5) << 8 | woff_b(6) << 16 | woff_b(7) << 24;
+__device__ __forceinline__ int woff(uint32_t k) { return (int)(__byte_perm(kWOffLo, kWOffHi, k) & 0xFFu) - 128; }
 
 // F = ((K*dt) * pow(A, m)) / pow(dist, n) (erosion.cpp:38-39) from the host
 // libm table when A is an exact multiple of the cell area.
@@ -186,6 +202,11 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       reinterpret_cast<uint32_t*>(s.rc)[i] = v;
       if (!EX && y >= kDY0 && y < kDY1) reinterpret_cast<uint32_t*>(s.dm)[i - kWP / 4] = m;
     }
+    // escape marks 0, cell counts 1 (EX) for the whole domain
+    for (int i = (int)tid; i < kDN / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.esc)[i] = 0u;
+    if (EX)
+      for (int i = (int)tid; i < kDN / 4; i += kTTPB)
+        reinterpret_cast<uint4*>(&s.acc[0])[i] = make_uint4(1u, 1u, 1u, 1u);
     // bit planes 0-2 of the codes, shifted to the window's columns (rows kDY0-1 .. kDY1);
     // outside the raster every plane reads 1 (code 15)
     if (tid < (uint32_t)((kDH + 2) * kBW)) {
@@ -241,7 +262,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
         if (!dir_in(CONN, k)) continue;
         const int nx = x + dir_ox(k), ny = y + dir_oy(k);
         if (nx >= kDX0 && nx < kDX1 && ny >= kDY0 && ny < kDY1) continue;
-        leak |= s.rc[q + dir_off(k, kWP) - (kDY0 - 1) * kWP] == (uint8_t)(7 - k);
+        leak |= s.rc[q + woff(k) - (kDY0 - 1) * kWP] == (uint8_t)(7 - k);
       }
       if (leak) atomicOr(&s.lk[y * kBW + (x >> 5)], 1u << (x & 31));
     }
@@ -252,48 +273,58 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
     // level: shift + and per direction), listed level-major (block prefix of
     // the word counts); a tree reaching a cell with a leaking donor escapes
     // (its root is marked)
+    // Once a level has at most kSmallLevel cells, warp 0 continues alone from
+    // the queue (children = neighbours whose code points back), with warp
+    // barriers only.
     uint32_t nl = 0, qpos = 0;
+    bool warp_mode = false;
     for (uint32_t l = 0;; ++l) {
       const uint32_t* cur = s.lv[(l + 1) & 1];  // level l-1 (level 0: the roots, in lv[0])
       uint32_t* nxt = s.lv[l & 1];              // level l
-      uint32_t word = 0, y = 0, w = 0;
-      if (tid < (uint32_t)kBPairs) {
-        y = kDY0 + tid / kBW;
-        w = tid - (y - kDY0) * kBW;
-        const uint32_t o = y * kBW + w;
-        if (l == 0) {
-          word = nxt[o];
-        } else {
-          // S_k(cur): bit x of row y = bit x + ox_k of row y + oy_k
-          uint32_t sh[3][3];  // [oy+1][ox+1]
-#pragma unroll
-          for (int oy = -1; oy <= 1; ++oy) {
-            const uint32_t* row = cur + (y + oy) * kBW;
-            const uint32_t c = row[w], lo = w > 0 ? row[w - 1] : 0u, hi = w + 1 < (uint32_t)kBW ? row[w + 1] : 0u;
-            sh[oy + 1][0] = (c << 1) | (lo >> 31);
-            sh[oy + 1][1] = c;
-            sh[oy + 1][2] = (c >> 1) | (hi << 31);
-          }
-          const uint32_t p0 = s.pl[0][o], p1 = s.pl[1][o], p2 = s.pl[2][o];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            if (!dir_in(CONN, k)) continue;
-            const uint32_t rk = ((k & 1) ? p0 : ~p0) & ((k & 2) ? p1 : ~p1) & ((k & 4) ? p2 : ~p2);
-            word |= rk & sh[dir_oy(k) + 1][dir_ox(k) + 1];
-          }
-          word &= s.vr[o];
-        }
-      }
-      const uint32_t cnt = __popc(word);
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t yv = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += yv;
-      }
+      uint32_t word = 0, y = 0, w = 0, incl = 0, cnt = 0;
       uint32_t* ws = s.wsum[l & 1];
-      if (lane == 31 && tid < (uint32_t)kBPairs + 31) ws[tid >> 5] = incl;
-      if (l > 0 && tid < (uint32_t)kBPairs) nxt[y * kBW + w] = word;
+      if (tid < (uint32_t)kBWarps * 32) {
+        if (tid < (uint32_t)kBPairs) {
+          y = kDY0 + tid / kBW;
+          w = tid - (y - kDY0) * kBW;
+          const uint32_t o = y * kBW + w;
+          if (l == 0) {
+            word = nxt[o];
+          } else {
+            // S_k(cur): bit x of row y = bit x + ox_k of row y + oy_k
+            uint32_t sh[3][3];  // [oy+1][ox+1]
+            uint32_t any = 0;
+#pragma unroll
+            for (int oy = -1; oy <= 1; ++oy) {
+              const uint32_t* row = cur + (y + oy) * kBW;
+              const uint32_t c = row[w], lo = w > 0 ? row[w - 1] : 0u, hi = w + 1 < (uint32_t)kBW ? row[w + 1] : 0u;
+              sh[oy + 1][0] = (c << 1) | (lo >> 31);
+              sh[oy + 1][1] = c;
+              sh[oy + 1][2] = (c >> 1) | (hi << 31);
+              any |= c | lo | hi;
+            }
+            if (any) {
+              const uint32_t p0 = s.pl[0][o], p1 = s.pl[1][o], p2 = s.pl[2][o];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                if (!dir_in(CONN, k)) continue;
+                const uint32_t rk = ((k & 1) ? p0 : ~p0) & ((k & 2) ? p1 : ~p1) & ((k & 4) ? p2 : ~p2);
+                word |= rk & sh[dir_oy(k) + 1][dir_ox(k) + 1];
+              }
+              word &= s.vr[o];
+            }
+          }
+        }
+        cnt = __popc(word);
+        incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t yv = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= (uint32_t)o) incl += yv;
+        }
+        if (lane == 31) ws[tid >> 5] = incl;
+        if (l > 0 && tid < (uint32_t)kBPairs) nxt[y * kBW + w] = word;
+      }
       __syncthreads();
       uint32_t wbase = 0, tot = 0;
 #pragma unroll
@@ -307,29 +338,94 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       if (tid < (uint32_t)kBPairs) {
         uint32_t pos = qpos + wbase + incl - cnt;
         const uint32_t leaks = word & s.lk[y * kBW + w];
+        const uint32_t qw = y * kWP + 32 * w;
         while (word) {
           const uint32_t b = __ffs(word) - 1;
           word &= word - 1;
-          const uint32_t q = y * kWP + 32 * w + b;
-          s.list[pos++] = (uint16_t)q;
-          ESC(q) = 0;
-          if (EX) ACC(q) = 1u;
-          if ((leaks >> b) & 1u) {  // a donor outside the domain: the tree escapes
-            uint32_t r = q, code = RC(q);
-            while (code != kNoFlowCode) {
-              r = (uint32_t)((int)r + dir_off(code, kWP));
-              code = RC(r);
-            }
-            ESC(r) = 1;
+          s.list[pos++] = (uint16_t)(qw + b);
+        }
+        for (uint32_t lb = leaks; lb; lb &= lb - 1) {  // a donor outside the domain: the tree escapes
+          uint32_t r = qw + __ffs(lb) - 1, code = RC(r);
+          while (code != kNoFlowCode) {
+            r = (uint32_t)((int)r + woff(code));
+            code = RC(r);
           }
+          ESC(r) = 1;
         }
       }
       qpos += tot;
       nl = l + 1;
       if (l + 1 == (uint32_t)kTMaxLev) break;
+      if (tot <= (uint32_t)kSmallLevel && kSmallLevel > 0) {
+        warp_mode = true;
+        break;
+      }
     }
-    if (tid == 0) s.lvs[nl] = qpos;
-    __syncthreads();
+    if (warp_mode) {
+      __syncthreads();  // the last block level is listed
+      if (tid < 32) {
+        uint32_t fs = s.lvs[nl - 1];  // frontier: level nl-1
+        for (;;) {
+          const uint32_t fe = qpos;
+          uint32_t run = 0;
+          for (uint32_t j0 = fs; j0 < fe; j0 += 32) {
+            const uint32_t i = j0 + lane;
+            uint32_t f = 0, kids = 0;
+            if (i < fe) {
+              f = s.list[i];
+              const uint32_t fy = f / kWP, fx = f - fy * kWP;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                if (!dir_in(CONN, k)) continue;
+                const uint32_t nx = fx + dir_ox(k), ny = fy + dir_oy(k);
+                if (nx - kDX0 >= (uint32_t)kDW || ny - kDY0 >= (uint32_t)kDH) continue;
+                if (RC(f + woff(k)) == (uint8_t)(7 - k)) kids |= 1u << k;
+              }
+            }
+            const uint32_t c = __popc(kids);
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t yv = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= (uint32_t)o) inc += yv;
+            }
+            uint32_t pos = qpos + run + inc - c;
+            while (kids) {
+              const uint32_t k = __ffs(kids) - 1;
+              kids &= kids - 1;
+              const uint32_t q = (uint32_t)((int)f + woff(k));
+              s.list[pos++] = (uint16_t)q;
+              const uint32_t qy = q / kWP, qx = q - qy * kWP;
+              if ((s.lk[qy * kBW + (qx >> 5)] >> (qx & 31)) & 1u) {
+                uint32_t r = q, code = RC(q);
+                while (code != kNoFlowCode) {
+                  r = (uint32_t)((int)r + woff(code));
+                  code = RC(r);
+                }
+                ESC(r) = 1;
+              }
+            }
+            run += __shfl_sync(0xffffffffu, inc, 31);
+          }
+          if (run == 0) break;
+          if (lane == 0) s.lvs[nl] = qpos;
+          fs = qpos;
+          qpos += run;
+          ++nl;
+          __syncwarp();
+          if (nl == (uint32_t)kTMaxLev) break;
+        }
+        if (lane == 0) {
+          s.lvs[nl] = qpos;
+          s.wsum[0][0] = nl;
+        }
+      }
+      __syncthreads();
+      nl = s.wsum[0][0];
+    } else {
+      if (tid == 0) s.lvs[nl] = qpos;
+      __syncthreads();
+    }
     if (nl == (uint32_t)kTMaxLev) {
       // level kTMaxLev would not be empty: every tree reaching it escapes
       for (uint32_t i = s.lvs[nl - 1] + tid; i < s.lvs[nl]; i += kTTPB) {
@@ -337,7 +433,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
         if (!a.dmask[gcell(r)]) continue;  // no donors: the tree ends here
         uint32_t code = RC(r);
         while (code != kNoFlowCode) {
-          r = (uint32_t)((int)r + dir_off(code, kWP));
+          r = (uint32_t)((int)r + woff(code));
           code = RC(r);
         }
         ESC(r) = 1;
@@ -357,7 +453,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       for (uint32_t i = (nl > 1 ? s.lvs[1] : 0u) + tid; i < (nl > 1 ? s.lvs[nl] : 0u); i += kTTPB) {
         uint32_t p = s.list[i], code = RC(p);
         do {
-          p = (uint32_t)((int)p + dir_off(code, kWP));
+          p = (uint32_t)((int)p + woff(code));
           atomicAdd(reinterpret_cast<uint32_t*>(&ACC(p)), 1u);
           code = RC(p);
         } while (code != kNoFlowCode);
@@ -374,7 +470,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
           while (m) {
             const uint32_t k = __ffs(m) - 1;
             m &= m - 1;
-            A = __dadd_rn(A, (double)ACC((int)q + dir_off(k, kWP)));
+            A = __dadd_rn(A, (double)ACC((int)q + woff(k)));
           }
           ACC(q) = A;
         }
@@ -416,17 +512,14 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
     }
     __syncthreads();
     // erosion, downstream -> upstream, with the receiver's updated elevation
-    for (uint32_t l = 1; l < nl; ++l) {
-      bool any = false;
-      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) {
+    auto erode = [&](uint32_t i) -> bool {
         const uint32_t q = s.list[i];
         const uint32_t code = RC(q);
-        const uint32_t p = (uint32_t)((int)q + dir_off(code, kWP));
+        const uint32_t p = (uint32_t)((int)q + woff(code));
         if (ESC(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
           ESC(q) = 1;
-          continue;
+          return false;
         }
-        any = true;
         ++cells;
         uint32_t mem = 0;
         if (a.M > 1) mem = (uint32_t)(wy0 + (int)(q / kWP)) / a.H;
@@ -460,17 +553,27 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
         }
         HW(q) = hnew;
         a.hout[gc] = hnew;
-      }
+      return true;
+    };
+    // the last levels, once at most kSmallLevel cells remain, by warp 0 alone
+    uint32_t lw = nl;
+    while (lw > 1 && s.lvs[nl] - s.lvs[lw - 1] <= (uint32_t)kSmallEro) --lw;
+    for (uint32_t l = 1; l < lw; ++l) {
+      bool any = false;
+      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) any |= erode(i);
       if (__syncthreads_or(any)) maxl = max(maxl, l + 1);
+    }
+    if (tid < 32) {
+      for (uint32_t l = lw; l < nl; ++l) {
+        bool any = false;
+        for (uint32_t i = s.lvs[l] + lane; i < s.lvs[l + 1]; i += 32) any |= erode(i);
+        if (__any_sync(0xffffffffu, any)) maxl = max(maxl, l + 1);
+        __syncwarp();
+      }
     }
     if (nl) maxl = max(maxl, 1u);
   }
 
-#undef HW
-#undef ACC
-#undef ESC
-#undef DM
-#undef RC
   // ---- counters: one atomic per warp for the whole kernel
   for (int o = 16; o; o >>= 1) {
     iters += __shfl_down_sync(0xffffffffu, iters, o);

@@ -1,0 +1,6 @@
+#!/bin/bash
+# Bench each tools/var_*.so build (LEMGPU_LIB) on the default workload; one line per variant.
+for so in tools/var_*.so; do
+  LEMGPU_LIB=$so timeout -s KILL 100 python bench.py --no-cpu-baseline --e2e-steps 0 --steps 20 "$@" 2>/dev/null \
+    | python -c "import json,sys; d=json.load(sys.stdin); k=d['roofline']['kernel_ms']; print('$so', round(d['ms_per_step'],4), {a: round(b,4) for a,b in k.items()})"
+done
