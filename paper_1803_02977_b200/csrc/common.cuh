@@ -166,6 +166,7 @@ struct StepArgs {
   double* hout;
   uint8_t* rcode;
   uint8_t* dmask;
+  int dmask_valid;   // dmask holds this step's donor masks (else derived from rcode where needed)
   uint32_t* planes;  // 4 bit planes of rcode, [plane][row][W32] words (k_recv_donor -> k_tiles)
   uint32_t W32;      // words per plane row
   uint32_t* order;
@@ -278,6 +279,24 @@ __device__ __forceinline__ void set_cond(const StepArgs& a, int which, unsigned 
     const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : a.h_deros;
     cudaGraphSetConditional(h, v);
   }
+}
+
+// donors_of (flow_graph.hpp:64-72) as a stencil bitmask: neighbour k drains
+// here when its receiver code is 7-k.  From the materialised mask, or from the
+// receiver codes of the neighbours (off-raster neighbours are skipped, and the
+// perimeter rows separating stacked members never drain anywhere).
+__device__ __forceinline__ uint32_t donor_mask_at(const StepArgs& a, uint32_t c) {
+  if (a.dmask_valid) return __ldg(a.dmask + c);
+  const uint32_t y = c / a.W, x = c - y * a.W;
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (!dir_in(a.conn, k)) continue;
+    const uint32_t nx = x + dir_ox(k), ny = y + dir_oy(k);
+    if (nx >= a.W || ny >= a.Htot) continue;
+    if (__ldg(a.rcode + (size_t)ny * a.W + nx) == (uint8_t)(7 - k)) m |= 1u << k;
+  }
+  return m;
 }
 
 __device__ __forceinline__ bool is_interior(const StepArgs& a, uint32_t c) {

@@ -103,7 +103,7 @@ __device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* 
         } else {
           child = a.order[p];
         }
-        cm[u] = __ldg(a.dmask + child);
+        cm[u] = donor_mask_at(a, child);
       } else {
         cm[u] = 0u;
       }

@@ -292,19 +292,22 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
     if (gy >= Ht) break;
     const int c4 = lane * 4;  // tile columns c4..c4+3 <-> rc columns c4+1..c4+4
     uint32_t lo[3], hi[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      lo[q] = *reinterpret_cast<const uint32_t*>(&rc[r + q][c4]);
-      hi[q] = *reinterpret_cast<const uint32_t*>(&rc[r + q][c4 + 4]);
-    }
+    lo[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4]);
+    hi[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4 + 4]);
     uint32_t pm = 0;
+    if (a.dmask_valid) {  // materialised donor masks (the global level path reads them)
+      lo[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4]);
+      hi[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4 + 4]);
+      lo[2] = *reinterpret_cast<const uint32_t*>(&rc[r + 2][c4]);
+      hi[2] = *reinterpret_cast<const uint32_t*>(&rc[r + 2][c4 + 4]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (!dir_in(CONN, k)) continue;
-      const int q = 1 + dir_oy(k);
-      const uint32_t sel = dir_ox(k) < 0 ? 0x3210u : dir_ox(k) == 0 ? 0x4321u : 0x5432u;
-      const uint32_t win = __byte_perm(lo[q], hi[q], sel);
-      pm |= zero_bytes(win ^ (0x01010101u * (uint32_t)(7 - k))) << k;
+      for (int k = 0; k < 8; ++k) {
+        if (!dir_in(CONN, k)) continue;
+        const int q = 1 + dir_oy(k);
+        const uint32_t sel = dir_ox(k) < 0 ? 0x3210u : dir_ox(k) == 0 ? 0x4321u : 0x5432u;
+        const uint32_t win = __byte_perm(lo[q], hi[q], sel);
+        pm |= zero_bytes(win ^ (0x01010101u * (uint32_t)(7 - k))) << k;
+      }
     }
     const uint32_t pc = __byte_perm(lo[1], hi[1], 0x4321u);
     // bit planes of the receiver codes (k_tiles' level discovery): bit b of
@@ -328,12 +331,12 @@ __global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid
     const size_t base = (size_t)gy * W + gx;
     if (gx + 3 < W && (W & 3) == 0) {
       *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
-      *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
+      if (a.dmask_valid) *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
     } else {
       for (int j = 0; j < 4; ++j)
         if (gx + j < W) {
           a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
-          a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
+          if (a.dmask_valid) a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
     }
   }

@@ -97,7 +97,6 @@ struct TileSmem {
   alignas(16) typename std::conditional<EX, uint32_t, double>::type acc[kDN];  // drainage area: cell count (EX) or FP sum
   uint16_t list[kCap];         // the tile's queue, level-major
   uint8_t rc[kRN];             // receiver codes of the domain and ring rows
-  uint8_t dm[EX ? 4 : kDN];    // donor masks (FP accumulation only)
   alignas(16) uint8_t esc[kDN];  // the cell's tree escapes (set on roots, inherited downstream -> upstream)
   uint8_t rowint[kWY];         // window row holds interior cells
   uint32_t pl[3][kBN];         // bit planes 0-2 of the receiver codes, aligned to the window
@@ -152,7 +151,6 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
 #define HW(q) s.hw[(q) - kQ0]
 #define ACC(q) s.acc[(q) - kQ0]
 #define ESC(q) s.esc[(q) - kQ0]
-#define DM(q) s.dm[(q) - kQ0]
 #define RC(q) s.rc[(q) - (kDY0 - 1) * kWP]
   unsigned long long iters = 0;  // per thread
   uint32_t misses = 0, cells = 0, n0i = 0, maxl = 0;
@@ -179,28 +177,27 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
         s.hw[i] = (gx >= 0 && gx < W && gy >= 0 && gy < Ht) ? __ldg(a.h + (size_t)gy * W + gx) : 0.0;
       }
     }
-    // receiver codes (and donor masks) of rows kDY0-1 .. kDY1 from k_recv_donor's
+    // receiver codes of rows kDY0-1 .. kDY1 from k_recv_donor's
     // output; cells outside the raster read as NoFlow
     for (int i = (int)tid; i < kRN / 4; i += kTTPB) {
       const int y = kDY0 - 1 + (4 * i) / kWP, x = (4 * i) % kWP;
       const int gx = wx0 + x, gy = wy0 + y;
-      uint32_t v = 0x08080808u, m = 0;
+      uint32_t v = 0x08080808u;
       if (gy >= 0 && gy < Ht) {
         const size_t g = (size_t)gy * a.W + gx;
         if (gx >= 0 && gx + 3 < W && (a.W & 3u) == 0) {
           v = __ldg(reinterpret_cast<const uint32_t*>(a.rcode + g));
-          if (!EX) m = __ldg(reinterpret_cast<const uint32_t*>(a.dmask + g));
+
         } else {
-          v = m = 0;
+          v = 0;
           for (int j = 0; j < 4; ++j) {
             const bool in = gx + j >= 0 && gx + j < W;
             v |= (in ? (uint32_t)a.rcode[g + j] : 8u) << (8 * j);
-            if (!EX) m |= (in ? (uint32_t)a.dmask[g + j] : 0u) << (8 * j);
+
           }
         }
       }
       reinterpret_cast<uint32_t*>(s.rc)[i] = v;
-      if (!EX && y >= kDY0 && y < kDY1) reinterpret_cast<uint32_t*>(s.dm)[i - kWP / 4] = m;
     }
     // escape marks 0, cell counts 1 (EX) for the whole domain
     for (int i = (int)tid; i < kDN / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.esc)[i] = 0u;
@@ -430,7 +427,10 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       // level kTMaxLev would not be empty: every tree reaching it escapes
       for (uint32_t i = s.lvs[nl - 1] + tid; i < s.lvs[nl]; i += kTTPB) {
         uint32_t r = s.list[i];
-        if (!a.dmask[gcell(r)]) continue;  // no donors: the tree ends here
+        bool kids = false;  // donors inside the domain (a donor outside already escaped the tree)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) kids |= dir_in(CONN, k) && RC(r + woff(k)) == (uint8_t)(7 - k);
+        if (!kids) continue;
         uint32_t code = RC(r);
         while (code != kNoFlowCode) {
           r = (uint32_t)((int)r + woff(code));
@@ -465,7 +465,13 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       for (int l = (int)nl - 1; l >= 0; --l) {
         for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) {
           const uint32_t q = s.list[i];
-          uint32_t m = DM(q);
+          uint32_t m = 0;  // donors (slot order = stencil order), all inside the domain for a kept tree
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t n = (uint32_t)((int)q + woff(k)), ny = n / kWP, nx = n - ny * kWP;
+            if (dir_in(CONN, k) && nx - kDX0 < (uint32_t)kDW && ny - kDY0 < (uint32_t)kDH && RC(n) == (uint8_t)(7 - k))
+              m |= 1u << k;
+          }
           double A = a.w0;
           while (m) {
             const uint32_t k = __ffs(m) - 1;

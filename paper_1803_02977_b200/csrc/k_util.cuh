@@ -26,6 +26,16 @@ __global__ void k_check_finite(const double* h, uint32_t N, uint32_t* first_bad)
     if (!isfinite(h[i])) atomicMin(first_bad, i);
 }
 
+// Donor masks of every cell from the receiver codes (the tile path does not
+// materialise them in the step; the parity export and the global level path
+// read them).
+__global__ void k_fill_dmask(StepArgs a) {
+  StepArgs b = a;
+  b.dmask_valid = 0;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x)
+    a.dmask[c] = (uint8_t)donor_mask_at(b, c);
+}
+
 // FlowGraph export in the reference layout (flow_graph.hpp:19-38).
 __global__ void k_export_graph(StepArgs a, uint32_t* rec, uint8_t* dnum, uint32_t* donor) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < a.N; c += gridDim.x * blockDim.x) {

@@ -189,6 +189,7 @@ StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
   a.expect_cells = ctx->use_tiles ? 0u : a.N;
   if (ctx->use_tiles) a.scan_grid = (uint32_t)ctx->esc_grid;
   if (!ctx->use_tiles) a.planes = nullptr;  // only k_tiles reads the code bit planes
+  a.dmask_valid = ctx->use_tiles ? 0 : 1;   // the tile path derives donor masks from the codes where needed
   return a;
 }
 
@@ -354,6 +355,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.h = ctx->hbuf[0];
   a.hout = ctx->hbuf[1];
   a.W32 = (W + 31) / 32;
+  a.dmask_valid = 1;
   a.kdt = ctx->d_kdt;
   a.mexp = ctx->d_mexp;
   a.ftab = ctx->d_lut;
@@ -799,6 +801,7 @@ int lemgpu_download_graph(lemgpu_ctx* ctx, uint32_t* rec, uint8_t* dnum, uint32_
   a.expect_cells = a.N;
   {
     cudaStream_t st = ctx->stream;
+    if (ctx->use_tiles) k_fill_dmask<<<2368, kTPB, 0, st>>>(a);
     set_eager_conds(a, st);
     k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
