@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define LEMGPU_ABI_VERSION 1
+#define LEMGPU_ABI_VERSION 2
 #define LEMGPU_NOFLOW 0xFFFFFFFFu /* kNoFlow, proj/include/lem/raster.hpp:16 */
 
 enum {

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "liblemgpu.so"
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 NOFLOW = 0xFFFFFFFF
 
 OK, ECONFIG, ESTRUCTURE, ECONVERGENCE, ECUDA, EOTHER = range(6)
