@@ -129,6 +129,7 @@ struct Ctl {
   unsigned long long newton;
   // tile path (k_tiles): escaped roots, cells finished in tiles, interior pits, deepest level + 1
   uint32_t nesc, tile_cells, n0i, tile_nlev;
+  uint32_t gbar_count, gbar_gen;  // grid barrier of the cooperative escape-path kernel
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
   uint32_t ntl, nltl;

@@ -40,11 +40,12 @@ struct ScanSmem {
 
 // Sum of v over the first `upto` entries of bins[] (one CTA, all threads);
 // also the sum of all `nb` entries.
+template <bool COOP = false>
 __device__ __forceinline__ void bins_prefix(const uint32_t* bins, uint32_t upto, uint32_t nb,
                                             uint32_t* scratch, uint32_t& pre, uint32_t& total) {
   uint32_t p = 0, t = 0;
   for (uint32_t i = threadIdx.x; i < nb; i += kTPB) {
-    const uint32_t v = bins[i];
+    const uint32_t v = COOP ? __ldcg(bins + i) : bins[i];
     t += v;
     if (i < upto) p += v;
   }
@@ -224,13 +225,20 @@ __global__ void __launch_bounds__(kTPB) k_l0_write(StepArgs a) {
 // of this level from fc[] of the previous one: a chunk of consecutive sources
 // owns ONE contiguous range per level, P_l(k) = fc[P_{l-1}(k)] (the end of a
 // level maps to the end of the next).
-__global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
-  __shared__ ScanSmem sm;
+// One frontier expansion: level l = positions [lo, hi) -> level l+1 written
+// from position hi; returns the size of level l+1 (every CTA computes it).
+// COOP: called inside one persistent (cooperative) kernel, so data written by
+// other CTAs in earlier levels is read past L1 (__ldcg).
+template <bool COOP>
+__device__ __forceinline__ uint32_t ld_x(const uint32_t* p) { return COOP ? __ldcg(p) : *p; }
+template <bool COOP>
+__device__ __forceinline__ uint32_t ld_x(const uint8_t* p) { return COOP ? (uint32_t)__ldcg(p) : (uint32_t)*p; }
+
+template <bool COOP>
+__device__ __forceinline__ uint32_t expand_level(const StepArgs& a, ScanSmem& sm, uint32_t l, uint32_t lo,
+                                                 uint32_t hi, bool err) {
   Ctl* ctl = a.ctl;
   const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint32_t l = ld_volatile_u32(&ctl->lvl);
-  const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
-  const uint32_t lo = a.levels[l], hi = a.levels[l + 1];
   uint32_t total = 0;
   if (!err) {
     const uint32_t* bins_in = a.bins + (size_t)(l % 3) * G;
@@ -246,14 +254,14 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
         if (l == 0) {
           v = min(k * (uint32_t)kChunkRoots, hi);
         } else {
-          const uint32_t p = cbp[k];
-          v = p >= lo ? hi : a.fc[p];
+          const uint32_t p = ld_x<COOP>(cbp + k);
+          v = p >= lo ? hi : ld_x<COOP>(a.fc + p);
         }
         cb[k] = v;
       }
     }
     uint32_t pre;
-    bins_prefix(bins_in, b, G, sm.scan, pre, total);
+    bins_prefix<COOP>(bins_in, b, G, sm.scan, pre, total);
     const uint32_t S = seg_size(hi - lo, G);
     const uint32_t Sn = seg_size(total, G);  // segment size of the next level
     const uint32_t s0 = lo + min(b * S, hi - lo), s1 = lo + min((b + 1) * S, hi - lo);
@@ -265,8 +273,8 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
 #pragma unroll
     for (int j = 0; j < kExIPT; ++j) {
       const uint32_t p = s0 + j * kTPB + threadIdx.x;
-      nc[j] = p < s1 ? a.order[p] : 0u;
-      nm[j] = p < s1 ? a.pdm[p] : 0u;
+      nc[j] = p < s1 ? ld_x<COOP>(a.order + p) : 0u;
+      nm[j] = p < s1 ? ld_x<COOP>(a.pdm + p) : 0u;
     }
     for (uint32_t tb = s0; tb < s1; tb += kExTile) {
       // coalesced staging of the tile's cells and donor masks
@@ -278,8 +286,8 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
 #pragma unroll
       for (int j = 0; j < kExIPT; ++j) {
         const uint32_t p = tb + kExTile + j * kTPB + threadIdx.x;
-        nc[j] = p < s1 ? a.order[p] : 0u;
-        nm[j] = p < s1 ? a.pdm[p] : 0u;
+        nc[j] = p < s1 ? ld_x<COOP>(a.order + p) : 0u;
+        nm[j] = p < s1 ? ld_x<COOP>(a.pdm + p) : 0u;
       }
       __syncthreads();
       uint32_t c[kExIPT], m[kExIPT], cnt = 0;
@@ -320,32 +328,103 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
       __syncthreads();
     }
   }
-  if (last_block_done(ctl) && threadIdx.x == 0) {
-    if (total > 0) {
-      a.levels[l + 2] = hi + total;
-      ctl->lvl = l + 1;
-      set_cond(a, 0, 1);
-    } else {
-      // plan complete: nlevels = l + 1 (traversal.cpp:45); cycle check (:46)
-      ctl->nlev = l + 1;
-      uint32_t mode = (l + 1 <= (uint32_t)kChunkMaxLevels && !a.force_deep) ? kModeShallow : kModeDeep;
-      a.fc[hi] = hi;  // end sentinel of the last level's child ranges
-      if (!err && a.expect_cells && hi != a.expect_cells) {
-        ctl->err_flag = LEMGPU_ESTRUCTURE;
-        ctl->err_cell = hi;  // cells placed
-        ctl->err_slot = ctl->slot;
-        mode = kModeFailed;
-      }
-      if (err) mode = kModeFailed;
-      ctl->mode = mode;
-      if (mode == kModeDeep) {
-        ctl->dlvl = l;  // deepest level first
-        set_cond(a, 1, 1);
-      }
-      ctl->t_order_end = globaltimer();
-      set_cond(a, 0, 0);
+  return total;
+}
+
+// Bookkeeping after level l is expanded (one thread): the next level's bound,
+// or the plan's completion (nlevels, cycle check, schedule of the physics).
+__device__ __forceinline__ void expand_finish(const StepArgs& a, uint32_t l, uint32_t hi, uint32_t total, bool err,
+                                              bool coop = false) {
+  Ctl* ctl = a.ctl;
+
+  if (total > 0) {
+    a.levels[l + 2] = hi + total;
+    ctl->lvl = l + 1;
+    if (!coop) set_cond(a, 0, 1);
+  } else {
+    // plan complete: nlevels = l + 1 (traversal.cpp:45); cycle check (:46)
+    ctl->nlev = l + 1;
+    uint32_t mode = (l + 1 <= (uint32_t)kChunkMaxLevels && !a.force_deep) ? kModeShallow : kModeDeep;
+    a.fc[hi] = hi;  // end sentinel of the last level's child ranges
+    if (!err && a.expect_cells && hi != a.expect_cells) {
+      ctl->err_flag = LEMGPU_ESTRUCTURE;
+      ctl->err_cell = hi;  // cells placed
+      ctl->err_slot = ctl->slot;
+      mode = kModeFailed;
     }
-    timeline(ctl);
+    if (err) mode = kModeFailed;
+    ctl->mode = mode;
+    if (mode == kModeDeep) {
+      ctl->dlvl = l;  // deepest level first
+      set_cond(a, 1, 1);
+    }
+    ctl->t_order_end = globaltimer();
+    if (!coop) set_cond(a, 0, 0);
+  }
+  timeline(ctl);
+}
+
+__global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
+  __shared__ ScanSmem sm;
+  Ctl* ctl = a.ctl;
+  const uint32_t l = ld_volatile_u32(&ctl->lvl);
+  const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
+  const uint32_t lo = a.levels[l], hi = a.levels[l + 1];
+  const uint32_t total = expand_level<false>(a, sm, l, lo, hi, err);
+  if (last_block_done(ctl) && threadIdx.x == 0) expand_finish(a, l, hi, total, err);
+}
+
+// Barrier of a grid whose CTAs are all resident (cooperative launch): the
+// last CTA to arrive releases the others by bumping the generation.
+__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t gen = ld_volatile_u32(&ctl->gbar_gen);
+    __threadfence();
+    if (atomicAdd(&ctl->gbar_count, 1u) == nb - 1) {
+      ctl->gbar_count = 0;
+      __threadfence();
+      atomicAdd(&ctl->gbar_gen, 1u);
+    } else {
+      while (ld_volatile_u32(&ctl->gbar_gen) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole level expansion of the escaped trees in ONE cooperative kernel
+// (the tile path's small residual workload): level 0 = the roots listed by
+// k_tiles (k_esc_l0's work), then one expand_level per level separated by
+// grid barriers instead of one graph WHILE iteration (kernel launch) each.
+__global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
+  __shared__ ScanSmem sm;
+  Ctl* ctl = a.ctl;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
+  const uint32_t n = ld_volatile_u32(&ctl->nesc);
+  const uint32_t Sb = seg_size(n, G);
+  if (!err) {
+    const uint32_t s0 = min(b * Sb, n), s1 = min(s0 + Sb, n);
+    pdm_and_bins<false>(a, nullptr, nullptr, 0u, s0, s1, 0u, Sb, a.bins);
+  }
+  if (b == 0 && threadIdx.x == 0) {
+    a.levels[0] = 0;
+    a.levels[1] = n;
+    ctl->n0 = n;
+    ctl->nch = (n + kChunkRoots - 1) / kChunkRoots;
+    ctl->lvl = 0;
+    ctl->t_t_end = max(ctl->t_t_end, globaltimer());
+  }
+  grid_barrier(ctl);
+  for (uint32_t l = 0;; ++l) {
+    const uint32_t lo = __ldcg(a.levels + l), hi = __ldcg(a.levels + l + 1);
+    const uint32_t total = expand_level<true>(a, sm, l, lo, hi, err);
+    grid_barrier(ctl);
+    if (b == 0 && threadIdx.x == 0) expand_finish(a, l, hi, total, err, true);
+    if (total == 0) break;
+    grid_barrier(ctl);
   }
 }
 

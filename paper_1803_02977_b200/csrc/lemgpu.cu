@@ -148,7 +148,7 @@ int dmalloc(lemgpu_ctx* ctx, T** p, size_t count) {
 // value in every kernel node; everything that changes from step to step lives
 // in the device control block.
 int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void* fn, dim3 grid,
-               dim3 block, size_t smem, StepArgs* sa, CUtensorMap* map) {
+               dim3 block, size_t smem, StepArgs* sa, CUtensorMap* map, bool cooperative = false) {
   cudaKernelNodeParams kp{};
   void* args[] = {sa, map};  // copied into the node
   kp.func = const_cast<void*>(fn);
@@ -158,6 +158,11 @@ int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void
   kp.kernelParams = args;
   cudaGraphNode_t n;
   CU(ctx, cudaGraphAddKernelNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+  if (cooperative) {  // all CTAs co-resident: the kernel's grid barrier is safe
+    cudaKernelNodeAttrValue v{};
+    v.cooperative = 1;
+    CU(ctx, cudaGraphKernelNodeSetAttribute(n, cudaKernelNodeAttributeCooperative, &v));
+  }
   *prev = n;
   return 0;
 }
@@ -209,7 +214,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   cudaGraph_t g;
   CU(ctx, cudaGraphCreate(&g, 0));
   ctx->graph[p] = g;
-  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
+  if (!ctx->use_tiles)  // the tile path expands the escaped trees inside one cooperative kernel
+    CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
   CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
   CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
   const int nk = a.nkind;
@@ -223,7 +229,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
         (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
-        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_l0, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr)))
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
@@ -231,7 +237,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
         (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
       return rc;
   }
-  if ((rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a)) ||
+  if ((!ctx->use_tiles && (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a))) ||
       (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
       (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
       (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
@@ -475,7 +481,7 @@ int run_levels_eager(lemgpu_ctx* ctx, const StepArgs& a) {
   const int nk = a.nkind;
   const size_t co = offsetof(Ctl, cond);
   char* cbase = reinterpret_cast<char*>(a.ctl) + co;
-  unsigned cond[3] = {1, 0, 0};
+  unsigned cond[3] = {a.tiles ? 0u : 1u, 0, 0};  // the tile path expands inside k_esc_bfs
   while (cond[0]) {
     k_expand<<<a.scan_grid, kTPB, 0, st>>>(a);
     CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
@@ -534,7 +540,8 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     cfg.stream = st;
     void* args[] = {&a, &ctx->tmap[p]};
     CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
-    k_esc_l0<<<a.scan_grid, kTPB, 0, st>>>(a);
+    void* eargs[] = {&a};
+    CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
