@@ -245,21 +245,29 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
       s.lv[0][o] = s.lv[1][o] = 0u;
     }
     __syncthreads();
-    // domain cells on the border with a donor in the ring outside the domain
-    for (int i = (int)tid; i < 2 * (kDW + kDH); i += kTTPB) {
+    // domain cells on the border with a donor in the ring outside the domain:
+    // one thread per border cell, checking only its ring neighbours
+    static_assert(2 * kDW + 2 * (kDH - 2) <= kTTPB, "one thread per border cell");
+    if (tid < (uint32_t)(2 * kDW + 2 * (kDH - 2))) {
       int x, y;
-      if (i < kDW) { x = kDX0 + i; y = kDY0; }
-      else if (i < 2 * kDW) { x = kDX0 + i - kDW; y = kDY1 - 1; }
-      else if (i < 2 * kDW + kDH) { x = kDX0; y = kDY0 + i - 2 * kDW; }
-      else { x = kDX1 - 1; y = kDY0 + i - 2 * kDW - kDH; }
+      uint32_t ring;  // directions whose neighbour lies in the ring
+      if (tid < (uint32_t)kDW) {
+        x = kDX0 + (int)tid, y = kDY0, ring = 0x07u;
+      } else if (tid < (uint32_t)(2 * kDW)) {
+        x = kDX0 + (int)tid - kDW, y = kDY1 - 1, ring = 0xE0u;
+      } else if (tid < (uint32_t)(2 * kDW + kDH - 2)) {
+        x = kDX0, y = kDY0 + 1 + (int)tid - 2 * kDW, ring = 0x29u;
+      } else {
+        x = kDX1 - 1, y = kDY0 + 1 + (int)tid - 2 * kDW - (kDH - 2), ring = 0x94u;
+      }
+      if (x == kDX0) ring |= 0x29u;
+      if (x == kDX1 - 1) ring |= 0x94u;
+      if (CONN == 4) ring &= 0x5Au;
       const int q = y * kWP + x;
       bool leak = false;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (!dir_in(CONN, k)) continue;
-        const int nx = x + dir_ox(k), ny = y + dir_oy(k);
-        if (nx >= kDX0 && nx < kDX1 && ny >= kDY0 && ny < kDY1) continue;
-        leak |= s.rc[q + woff(k) - (kDY0 - 1) * kWP] == (uint8_t)(7 - k);
+      for (uint32_t m = ring; m; m &= m - 1) {
+        const uint32_t k = __ffs(m) - 1;
+        leak |= RC(q + woff(k)) == (uint8_t)(7 - k);
       }
       if (leak) atomicOr(&s.lk[y * kBW + (x >> 5)], 1u << (x & 31));
     }
@@ -519,46 +527,46 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
     __syncthreads();
     // erosion, downstream -> upstream, with the receiver's updated elevation
     auto erode = [&](uint32_t i) -> bool {
-        const uint32_t q = s.list[i];
-        const uint32_t code = RC(q);
-        const uint32_t p = (uint32_t)((int)q + woff(code));
-        if (ESC(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
-          ESC(q) = 1;
-          return false;
-        }
-        ++cells;
-        uint32_t mem = 0;
-        if (a.M > 1) mem = (uint32_t)(wy0 + (int)(q / kWP)) / a.H;
-        const uint32_t cls = dir_class(code);  // class of dist(c, rec[c])
-        const double h0 = __dadd_rn(HW(q), a.du);  // uplift (every cell below level 0 is interior)
-        const double hn = HW(p);
-        int itn;
-        bool ok;
-        double hnew;
-        if (tab) {
-          const double2 fy = __ldg(reinterpret_cast<const double2*>(a.ftab2) + (mem * 3 + cls) * E + (uint32_t)ACC(q));
-          hnew = newton_n1_tab(h0, hn, fy.x, fy.y, a.eps, a.maxit, itn, ok);
-        } else {
-          double F;
-          if (EX)
-            F = __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)ACC(q));
-          else
-            F = tile_F(a, mem, cls, (double)ACC(q), misses);
-          if (NK == 1)
-            hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
-          else
-            hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, ok);
-        }
-        const uint32_t gc = gcell(q);
-        if (ok) {
-          iters += (unsigned long long)itn;
-        } else {
-          atomicMin(&ctl->err_cell, gc);
-          ctl->err_slot = ctl->slot;
-          atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
-        }
-        HW(q) = hnew;
-        a.hout[gc] = hnew;
+      const uint32_t q = s.list[i];
+      const uint32_t code = RC(q);
+      const uint32_t p = (uint32_t)((int)q + woff(code));
+      if (ESC(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
+        ESC(q) = 1;
+        return false;
+      }
+      ++cells;
+      uint32_t mem = 0;
+      if (a.M > 1) mem = (uint32_t)(wy0 + (int)(q / kWP)) / a.H;
+      const uint32_t cls = dir_class(code);  // class of dist(c, rec[c])
+      const double h0 = __dadd_rn(HW(q), a.du);  // uplift (every cell below level 0 is interior)
+      const double hn = HW(p);
+      int itn;
+      bool ok;
+      double hnew;
+      if (tab) {
+        const double2 fy = __ldg(reinterpret_cast<const double2*>(a.ftab2) + (mem * 3 + cls) * E + (uint32_t)ACC(q));
+        hnew = newton_n1_tab(h0, hn, fy.x, fy.y, a.eps, a.maxit, itn, ok);
+      } else {
+        double F;
+        if (EX)
+          F = __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)ACC(q));
+        else
+          F = tile_F(a, mem, cls, (double)ACC(q), misses);
+        if (NK == 1)
+          hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
+        else
+          hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, ok);
+      }
+      const uint32_t gc = gcell(q);
+      if (ok) {
+        iters += (unsigned long long)itn;
+      } else {
+        atomicMin(&ctl->err_cell, gc);
+        ctl->err_slot = ctl->slot;
+        atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+      }
+      HW(q) = hnew;
+      a.hout[gc] = hnew;
       return true;
     };
     // the last levels, once at most kSmallLevel cells remain, by warp 0 alone
