@@ -38,8 +38,13 @@ constexpr int kNW = kTPB / 32;      // warps per CTA
 constexpr uint8_t kNoFlowCode = 8;  // rcode value for kNoFlow
 
 // k_tiles: owned tile, BFS halo (see k_tiles.cuh)
-constexpr int kTX = 64, kTY = 32, kHalo = 3;
-constexpr int kTTPB = 256;
+#ifndef LEMGPU_TILE_Y
+#define LEMGPU_TILE_Y 32
+#define LEMGPU_TILE_TPB 256
+#define LEMGPU_TILE_MINB 4
+#endif
+constexpr int kTX = 64, kTY = LEMGPU_TILE_Y, kHalo = 3;
+constexpr int kTTPB = LEMGPU_TILE_TPB;
 
 // k_recv_donor tile (output cells): halo of 2 for h, 1 for the receiver codes.
 constexpr int kBX = 128;

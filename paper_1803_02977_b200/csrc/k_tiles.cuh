@@ -130,7 +130,7 @@ __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32
 }
 
 template <int CONN, int NK, bool EX>
-__global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
+__global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char smraw[];
   TileSmem<EX>& s = *reinterpret_cast<TileSmem<EX>*>(smraw);
   Ctl* ctl = a.ctl;
@@ -247,18 +247,17 @@ __global__ void __launch_bounds__(kTTPB, EX ? 4 : 2) k_tiles(StepArgs a, const _
     __syncthreads();
     // domain cells on the border with a donor in the ring outside the domain:
     // one thread per border cell, checking only its ring neighbours
-    static_assert(2 * kDW + 2 * (kDH - 2) <= kTTPB, "one thread per border cell");
-    if (tid < (uint32_t)(2 * kDW + 2 * (kDH - 2))) {
+    for (uint32_t bi = tid; bi < (uint32_t)(2 * kDW + 2 * (kDH - 2)); bi += kTTPB) {
       int x, y;
       uint32_t ring;  // directions whose neighbour lies in the ring
-      if (tid < (uint32_t)kDW) {
-        x = kDX0 + (int)tid, y = kDY0, ring = 0x07u;
-      } else if (tid < (uint32_t)(2 * kDW)) {
-        x = kDX0 + (int)tid - kDW, y = kDY1 - 1, ring = 0xE0u;
-      } else if (tid < (uint32_t)(2 * kDW + kDH - 2)) {
-        x = kDX0, y = kDY0 + 1 + (int)tid - 2 * kDW, ring = 0x29u;
+      if (bi < (uint32_t)kDW) {
+        x = kDX0 + (int)bi, y = kDY0, ring = 0x07u;
+      } else if (bi < (uint32_t)(2 * kDW)) {
+        x = kDX0 + (int)bi - kDW, y = kDY1 - 1, ring = 0xE0u;
+      } else if (bi < (uint32_t)(2 * kDW + kDH - 2)) {
+        x = kDX0, y = kDY0 + 1 + (int)bi - 2 * kDW, ring = 0x29u;
       } else {
-        x = kDX1 - 1, y = kDY0 + 1 + (int)tid - 2 * kDW - (kDH - 2), ring = 0x94u;
+        x = kDX1 - 1, y = kDY0 + 1 + (int)bi - 2 * kDW - (kDH - 2), ring = 0x94u;
       }
       if (x == kDX0) ring |= 0x29u;
       if (x == kDX1 - 1) ring |= 0x94u;
