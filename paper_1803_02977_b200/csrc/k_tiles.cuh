@@ -177,28 +177,30 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         s.hw[i] = (gx >= 0 && gx < W && gy >= 0 && gy < Ht) ? __ldg(a.h + (size_t)gy * W + gx) : 0.0;
       }
     }
-    // receiver codes of rows kDY0-1 .. kDY1 from k_recv_donor's
-    // output; cells outside the raster read as NoFlow
+    // receiver codes of rows kDY0-1 .. kDY1 from k_recv_donor's output
+    // (asynchronous 4-byte copies, cp.async); cells outside the raster read as NoFlow
     for (int i = (int)tid; i < kRN / 4; i += kTTPB) {
       const int y = kDY0 - 1 + (4 * i) / kWP, x = (4 * i) % kWP;
       const int gx = wx0 + x, gy = wy0 + y;
-      uint32_t v = 0x08080808u;
-      if (gy >= 0 && gy < Ht) {
-        const size_t g = (size_t)gy * a.W + gx;
-        if (gx >= 0 && gx + 3 < W && (a.W & 3u) == 0) {
-          v = __ldg(reinterpret_cast<const uint32_t*>(a.rcode + g));
-
-        } else {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(s.rc) + i;
+      if (gy >= 0 && gy < Ht && gx >= 0 && gx + 3 < W && (a.W & 3u) == 0) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)),
+                     "l"(a.rcode + (size_t)gy * a.W + gx)
+                     : "memory");
+      } else {
+        uint32_t v = 0x08080808u;
+        if (gy >= 0 && gy < Ht) {
+          const size_t g = (size_t)gy * a.W + gx;
           v = 0;
           for (int j = 0; j < 4; ++j) {
             const bool in = gx + j >= 0 && gx + j < W;
             v |= (in ? (uint32_t)a.rcode[g + j] : 8u) << (8 * j);
-
           }
         }
+        *dst = v;
       }
-      reinterpret_cast<uint32_t*>(s.rc)[i] = v;
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // escape marks 0, cell counts 1 (EX) for the whole domain
     for (int i = (int)tid; i < kDN / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.esc)[i] = 0u;
     if (EX)
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       const int o = (tid < kBW ? 0 : (kWY - 1) * kBW) + (int)(tid % kBW);
       s.lv[0][o] = s.lv[1][o] = 0u;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's code copies have landed
     __syncthreads();
     // domain cells on the border with a donor in the ring outside the domain:
     // one thread per border cell, checking only its ring neighbours
