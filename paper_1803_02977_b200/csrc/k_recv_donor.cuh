@@ -167,7 +167,10 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
 }
 
 template <int CONN>
-__global__ void __launch_bounds__(kTPB, 4) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
+#ifndef LEMGPU_RECV_MINB
+#define LEMGPU_RECV_MINB 5  // measured: 5 CTAs/SM (48 regs) beats 4 (64 regs)
+#endif
+__global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
   __shared__ __align__(4) uint8_t rc[kBY + 2][kBX + 4];
   __shared__ uint8_t rowint[kBY + 2];
