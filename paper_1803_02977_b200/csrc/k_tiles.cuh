@@ -57,8 +57,8 @@ namespace lemgpu {
 // (wx0 + x, wy0 + y).  The tile T is columns [kLX, kLX+kTX) x rows [kLY,
 // kLY+kTY); the BFS domain is T grown by kHalo; the receiver codes of the
 // ring around the domain tell which domain cells have donors outside it.
-constexpr int kWP = 84;             // window pitch = TMA box width (doubles)
-constexpr int kLX = 8;              // first tile column in the window
+constexpr int kWP = 72;             // window pitch = TMA box width (doubles): the ring columns exactly
+constexpr int kLX = kHalo + 1;      // first tile column in the window
 constexpr int kLY = kHalo + 2;      // first tile row in the window
 constexpr int kWY = kTY + 2 * kLY;  // window rows
 constexpr int kDX0 = kLX - kHalo, kDX1 = kLX + kTX + kHalo;  // domain columns [kDX0, kDX1)
