@@ -39,9 +39,11 @@ constexpr uint8_t kNoFlowCode = 8;  // rcode value for kNoFlow
 
 // k_tiles: owned tile, BFS halo (see k_tiles.cuh)
 #ifndef LEMGPU_TILE_Y
+// measured best of {16,24,32,40,48} rows x {128..384} threads x {3..7} CTAs/SM
+// (tools/variants_check.sh): 64x32 tiles, 6 warps, 5 CTAs/SM (45 KB smem each)
 #define LEMGPU_TILE_Y 32
-#define LEMGPU_TILE_TPB 256
-#define LEMGPU_TILE_MINB 4
+#define LEMGPU_TILE_TPB 192
+#define LEMGPU_TILE_MINB 5
 #endif
 constexpr int kTX = 64, kTY = LEMGPU_TILE_Y, kHalo = 3;
 constexpr int kTTPB = LEMGPU_TILE_TPB;

@@ -97,7 +97,7 @@ struct TileSmem {
   alignas(16) typename std::conditional<EX, uint32_t, double>::type acc[kDN];  // drainage area: cell count (EX) or FP sum
   uint16_t list[kCap];         // the tile's queue, level-major
   uint8_t rc[kRN];             // receiver codes of the domain and ring rows
-  alignas(16) uint8_t esc[kDN];  // the cell's tree escapes (set on roots, inherited downstream -> upstream)
+  alignas(16) uint8_t esc[EX ? 16 : kDN];  // the cell's tree escapes (FP path; EX: bit 31 of acc) (set on roots, inherited downstream -> upstream)
   uint8_t rowint[kWY];         // window row holds interior cells
   uint32_t pl[3][kBN];         // bit planes 0-2 of the receiver codes, aligned to the window
   uint32_t vr[kBN];            // domain cells with a receiver (code < 8)
@@ -150,7 +150,15 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
 
 #define HW(q) s.hw[(q) - kQ0]
 #define ACC(q) s.acc[(q) - kQ0]
-#define ESC(q) s.esc[(q) - kQ0]
+// escape mark of a cell: bit 31 of its cell count (EX), else its own byte
+#define ESC_GET(q) (EX ? ((uint32_t)s.acc[(q) - kQ0] >> 31) : (uint32_t)s.esc[(q) - kQ0])
+#define ESC_SET(q)                                                    \
+  do {                                                                \
+    if (EX)                                                           \
+      reinterpret_cast<uint32_t*>(s.acc)[(q) - kQ0] |= 0x80000000u;   \
+    else                                                              \
+      s.esc[(q) - kQ0] = 1;                                           \
+  } while (0)
 #define RC(q) s.rc[(q) - (kDY0 - 1) * kWP]
   unsigned long long iters = 0;  // per thread
   uint32_t misses = 0, cells = 0, n0i = 0, maxl = 0;
@@ -202,7 +210,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     // escape marks 0, cell counts 1 (EX) for the whole domain
-    for (int i = (int)tid; i < kDN / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.esc)[i] = 0u;
+    if (!EX)
+      for (int i = (int)tid; i < kDN / 4; i += kTTPB) reinterpret_cast<uint32_t*>(s.esc)[i] = 0u;
     if (EX)
       for (int i = (int)tid; i < kDN / 4; i += kTTPB)
         reinterpret_cast<uint4*>(&s.acc[0])[i] = make_uint4(1u, 1u, 1u, 1u);
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
             r = (uint32_t)((int)r + woff(code));
             code = RC(r);
           }
-          ESC(r) = 1;
+          ESC_SET(r);
         }
       }
       qpos += tot;
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
                   r = (uint32_t)((int)r + woff(code));
                   code = RC(r);
                 }
-                ESC(r) = 1;
+                ESC_SET(r);
               }
             }
             run += __shfl_sync(0xffffffffu, inc, 31);
@@ -446,14 +455,14 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           r = (uint32_t)((int)r + woff(code));
           code = RC(r);
         }
-        ESC(r) = 1;
+        ESC_SET(r);
       }
       __syncthreads();
     }
     if (a.force_escape) {
       for (uint32_t i = s.lvs[0] + tid; i < s.lvs[nl > 0 ? 1 : 0]; i += kTTPB) {
         const uint32_t q = s.list[i];
-        if (a.force_escape == 1 || (gcell(q) & 1u)) ESC(q) = 1;
+        if (a.force_escape == 1 || (gcell(q) & 1u)) ESC_SET(q);
       }
       __syncthreads();
     }
@@ -506,7 +515,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         const int gx = wx0 + (int)x;
         const bool inter = s.rowint[y] && gx > 0 && gx < W - 1;  // interior NoFlow cell (simulation.cpp:42-44)
         n0i += inter ? 1u : 0u;
-        e = ESC(q) != 0;
+        e = ESC_GET(q) != 0;
         if (!e) {
           double hv = HW(q);
           if (inter) {
@@ -532,8 +541,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       const uint32_t q = s.list[i];
       const uint32_t code = RC(q);
       const uint32_t p = (uint32_t)((int)q + woff(code));
-      if (ESC(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
-        ESC(q) = 1;
+      if (ESC_GET(p)) {  // the tree escapes: inherit the mark, leave the cell to the level path
+        ESC_SET(q);
         return false;
       }
       ++cells;
@@ -607,6 +616,12 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   __syncthreads();
   if (tid == 0) atomicMax(&ctl->t_t_end, globaltimer());
 }
+
+#undef HW
+#undef ACC
+#undef RC
+#undef ESC_GET
+#undef ESC_SET
 
 // Level 0 of the escape path: the escaped roots (listed by k_tiles in
 // order[0, nesc)), their donor masks and the per-segment child counts of
