@@ -396,7 +396,8 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl) {
 
 // The whole level expansion of the escaped trees in ONE cooperative kernel
 // (the tile path's small residual workload): level 0 = the roots listed by
-// k_tiles (k_esc_l0's work), then one expand_level per level separated by
+// k_tiles (their donor masks and the bins of the first expansion), then one
+// expand_level per level separated by
 // grid barriers instead of one graph WHILE iteration (kernel launch) each.
 __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
   __shared__ ScanSmem sm;

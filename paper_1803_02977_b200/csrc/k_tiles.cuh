@@ -623,28 +623,4 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
 #undef ESC_GET
 #undef ESC_SET
 
-// Level 0 of the escape path: the escaped roots (listed by k_tiles in
-// order[0, nesc)), their donor masks and the per-segment child counts of
-// the first expansion.  Order of the list is irrelevant to the results (every
-// schedule of the per-cell arithmetic is bit-identical).
-__global__ void __launch_bounds__(kTPB) k_esc_l0(StepArgs a) {
-  Ctl* ctl = a.ctl;
-  const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint32_t n = ld_volatile_u32(&ctl->nesc);
-  const uint32_t Sb = seg_size(n, G);
-  if (!ld_volatile_u32(&ctl->err_flag)) {
-    const uint32_t s0 = min(b * Sb, n), s1 = min(s0 + Sb, n);
-    pdm_and_bins<false>(a, nullptr, nullptr, 0u, s0, s1, 0u, Sb, a.bins);
-  }
-  if (last_block_done(ctl) && threadIdx.x == 0) {
-    a.levels[0] = 0;
-    a.levels[1] = n;
-    ctl->n0 = n;
-    ctl->nch = (n + kChunkRoots - 1) / kChunkRoots;
-    ctl->lvl = 0;
-    ctl->t_t_end = max(ctl->t_t_end, globaltimer());
-    timeline(ctl);
-  }
-}
-
 }  // namespace lemgpu
