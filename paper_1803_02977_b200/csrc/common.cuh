@@ -307,6 +307,26 @@ __device__ __forceinline__ uint32_t donor_mask_at(const StepArgs& a, uint32_t c)
   return m;
 }
 
+// Barrier of a grid whose CTAs are all resident (cooperative launch): the
+// last CTA to arrive releases the others by bumping the generation.
+__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t gen = ld_volatile_u32(&ctl->gbar_gen);
+    __threadfence();
+    if (atomicAdd(&ctl->gbar_count, 1u) == nb - 1) {
+      ctl->gbar_count = 0;
+      __threadfence();
+      atomicAdd(&ctl->gbar_gen, 1u);
+    } else {
+      while (ld_volatile_u32(&ctl->gbar_gen) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ bool is_interior(const StepArgs& a, uint32_t c) {
   const uint32_t y = c / a.W, x = c - y * a.W, yl = y % a.H;
   return x > 0 && x < a.W - 1 && yl > 0 && yl < a.H - 1;

@@ -356,7 +356,7 @@ __device__ __forceinline__ void expand_finish(const StepArgs& a, uint32_t l, uin
     ctl->mode = mode;
     if (mode == kModeDeep) {
       ctl->dlvl = l;  // deepest level first
-      set_cond(a, 1, 1);
+      if (!coop) set_cond(a, 1, 1);  // the tile path sweeps deep plans in k_deep_coop
     }
     ctl->t_order_end = globaltimer();
     if (!coop) set_cond(a, 0, 0);
@@ -372,26 +372,6 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
   const uint32_t lo = a.levels[l], hi = a.levels[l + 1];
   const uint32_t total = expand_level<false>(a, sm, l, lo, hi, err);
   if (last_block_done(ctl) && threadIdx.x == 0) expand_finish(a, l, hi, total, err);
-}
-
-// Barrier of a grid whose CTAs are all resident (cooperative launch): the
-// last CTA to arrive releases the others by bumping the generation.
-__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
-    const uint32_t gen = ld_volatile_u32(&ctl->gbar_gen);
-    __threadfence();
-    if (atomicAdd(&ctl->gbar_count, 1u) == nb - 1) {
-      ctl->gbar_count = 0;
-      __threadfence();
-      atomicAdd(&ctl->gbar_gen, 1u);
-    } else {
-      while (ld_volatile_u32(&ctl->gbar_gen) == gen) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
 }
 
 // The whole level expansion of the escaped trees in ONE cooperative kernel
@@ -419,13 +399,16 @@ __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
     ctl->t_t_end = max(ctl->t_t_end, globaltimer());
   }
   grid_barrier(ctl);
+  // every CTA derives the next level's bounds itself (the size of level l+1
+  // is the sum of the bins every CTA reads), so one barrier per level suffices
+  uint32_t lo = 0, hi = n;
   for (uint32_t l = 0;; ++l) {
-    const uint32_t lo = __ldcg(a.levels + l), hi = __ldcg(a.levels + l + 1);
     const uint32_t total = expand_level<true>(a, sm, l, lo, hi, err);
     grid_barrier(ctl);
     if (b == 0 && threadIdx.x == 0) expand_finish(a, l, hi, total, err, true);
     if (total == 0) break;
-    grid_barrier(ctl);
+    lo = hi;
+    hi += total;
   }
 }
 

@@ -216,9 +216,12 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   ctx->graph[p] = g;
   if (!ctx->use_tiles)  // the tile path expands the escaped trees inside one cooperative kernel
     CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
-  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
-  CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
+  if (!ctx->use_tiles) {  // the tile path sweeps deep plans inside one cooperative kernel
+    CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
+    CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
+  }
   const int nk = a.nkind;
+  const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
   const void* fk1 = a.conn == 8 ? (const void*)k_recv_donor<8> : (const void*)k_recv_donor<4>;
   const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   const void* fde = nk == 1 ? (const void*)k_deep_erode<1> : nk == 2 ? (const void*)k_deep_erode<2> : (const void*)k_deep_erode<0>;
@@ -239,10 +242,13 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   }
   if ((!ctx->use_tiles && (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a))) ||
       (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
-      (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
-      (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0, &a)) ||
-      (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
+      (ctx->use_tiles &&
+       (rc = add_kernel(ctx, g, &prev, fdc, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true))) ||
+      (!ctx->use_tiles &&
+       ((rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
+        (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
+        (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0, &a)) ||
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)))) ||
       (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0, &a, nullptr)))
     return rc;
   CU(ctx, cudaGraphInstantiate(&ctx->exec[p], g, 0));
@@ -493,6 +499,12 @@ int run_levels_eager(lemgpu_ctx* ctx, const StepArgs& a) {
     k_chunks<2><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
   else
     k_chunks<0><<<ctx->chunk_grid, kChunkTPB, kChunksSmemBytes, st>>>(a);
+  if (a.tiles) {
+    void* dargs[] = {const_cast<StepArgs*>(&a)};
+    const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
+    CU(ctx, cudaLaunchCooperativeKernel(fdc, dim3(a.scan_grid), dim3(kTPB), dargs, 0, st));
+    return LEMGPU_OK;
+  }
   k_deep_prep<<<ctx->deep_grid, kTPB, 0, st>>>(a);
   CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
   CU(ctx, cudaStreamSynchronize(st));

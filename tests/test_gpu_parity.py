@@ -367,3 +367,19 @@ def test_failed_step_leaves_elevation_unchanged(oracle):
     with pytest.raises(lem.ConvergenceError):
         ctx.step(3)
     assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
+
+
+def test_deep_plan_1000(oracle):
+    """A 1000^2 tilted plane: ~1000 levels, every tree escapes its tile, the
+    escape path runs its cooperative level expansion and deep sweeps."""
+    e = _ramp(1000, 1000, 5)
+    ctx = device_ctx(1000, 1000)
+    ctx.upload(e)
+    for s in range(2):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, want_donor=False)
+        assert d.nlevels == o["nlevels"] > 900
+        assert d.newton_iters == o["newton_iters"]
+        assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), f"step {s}"
+    g = ctx.download_graph()
+    assert np.array_equal(g["order"], o["order"]) and np.array_equal(g["levels"], o["levels"])
