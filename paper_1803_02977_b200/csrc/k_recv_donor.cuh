@@ -166,10 +166,13 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
   return (~t & 0x80808080u) >> 7;
 }
 
-template <int CONN>
 #ifndef LEMGPU_RECV_MINB
 #define LEMGPU_RECV_MINB 5  // measured: 5 CTAs/SM (48 regs) beats 4 (64 regs)
 #endif
+// DONORS: also the donor masks of the tile (the global level path reads
+// them), which needs the receiver codes of the ring around it; the tile path
+// derives donors from the codes and skips the ring.
+template <int CONN, bool DONORS>
 __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
   __shared__ __align__(4) uint8_t rc[kBY + 2][kBX + 4];
@@ -223,8 +226,9 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
   // shared loads per cell); the two ring columns are done separately.
   {
     const int c = 1 + (tid & (kBX - 1));
-    const int rbeg = (tid < kBX) ? 0 : (kBY + 2) / 2;
-    const int rend = (tid < kBX) ? (kBY + 2) / 2 : kBY + 2;
+    const int ra = DONORS ? 0 : 1, rz = DONORS ? kBY + 2 : kBY + 1;  // receiver-code rows [ra, rz)
+    const int rbeg = (tid < kBX) ? ra : (ra + rz) / 2;
+    const int rend = (tid < kBX) ? (ra + rz) / 2 : rz;
     const int gx = (int)x0 - 1 + c;
     const bool colint = gx > 0 && gx < (int)W - 1;
     // window rows u = sh row r, m = r+1, v = r+2 (sh columns c..c+2),
@@ -272,7 +276,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
       }
     }
   }
-  if (tid < 2 * (kBY + 2)) {  // ring columns c = 0 and c = kBX+1
+  if (DONORS && tid < 2 * (kBY + 2)) {  // ring columns c = 0 and c = kBX+1
     const int r = tid >> 1, c = (tid & 1) ? kBX + 1 : 0;
     const int gx = (int)x0 - 1 + c;
     uint8_t code = kNoFlowCode;
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
     lo[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4]);
     hi[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4 + 4]);
     uint32_t pm = 0;
-    if (a.dmask_valid) {  // materialised donor masks (the global level path reads them)
+    if (DONORS) {  // materialised donor masks (the global level path reads them)
       lo[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4]);
       hi[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4 + 4]);
       lo[2] = *reinterpret_cast<const uint32_t*>(&rc[r + 2][c4]);
@@ -334,12 +338,12 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
     const size_t base = (size_t)gy * W + gx;
     if (gx + 3 < W && (W & 3) == 0) {
       *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
-      if (a.dmask_valid) *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
+      if (DONORS) *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
     } else {
       for (int j = 0; j < 4; ++j)
         if (gx + j < W) {
           a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
-          if (a.dmask_valid) a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
+          if (DONORS) a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
     }
   }

@@ -222,7 +222,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   }
   const int nk = a.nkind;
   const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
-  const void* fk1 = a.conn == 8 ? (const void*)k_recv_donor<8> : (const void*)k_recv_donor<4>;
+  const void* fk1 = ctx->use_tiles ? (a.conn == 8 ? (const void*)k_recv_donor<8, false> : (const void*)k_recv_donor<4, false>)
+                                   : (a.conn == 8 ? (const void*)k_recv_donor<8, true> : (const void*)k_recv_donor<4, true>);
   const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   const void* fde = nk == 1 ? (const void*)k_deep_erode<1> : nk == 2 ? (const void*)k_deep_erode<2> : (const void*)k_deep_erode<0>;
   cudaGraphNode_t prev = nullptr;
@@ -542,9 +543,9 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   if (ctx->use_tiles) {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
-      k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<8, false><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     else
-      k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<4, false><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->tile_grid);
     cfg.blockDim = dim3(kTTPB);
@@ -557,9 +558,9 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
-      k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<8, true><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     else
-      k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<4, true><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
   }
