@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       s.esc[(q) - kQ0] = 1;                                           \
   } while (0)
 #define RC(q) s.rc[(q) - (kDY0 - 1) * kWP]
-  unsigned long long iters = 0;  // per thread
+  uint32_t iters = 0;               // per thread and tile (cells of the tile x max_newton_iters < 2^32)
+  unsigned long long iters64 = 0;  // per thread
   uint32_t misses = 0, cells = 0, n0i = 0, maxl = 0;
   uint32_t phase = 0;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1u) {
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       const uint32_t y = q / kWP;
       return gbase + q + y * (a.W - (uint32_t)kWP);
     };
+    iters64 += iters;
+    iters = 0;
     __syncthreads();  // the previous tile is finished with every shared array
     if (tid == 0 && a.use_tma) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of hw before the TMA overwrite
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       }
       const uint32_t gc = gcell(q);
       if (ok) {
-        iters += (unsigned long long)itn;
+        iters += (uint32_t)itn;
       } else {
         atomicMin(&ctl->err_cell, gc);
         ctl->err_slot = ctl->slot;
@@ -600,14 +603,15 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   }
 
   // ---- counters: one atomic per warp for the whole kernel
+  iters64 += iters;
   for (int o = 16; o; o >>= 1) {
-    iters += __shfl_down_sync(0xffffffffu, iters, o);
+    iters64 += __shfl_down_sync(0xffffffffu, iters64, o);
     misses += __shfl_down_sync(0xffffffffu, misses, o);
     n0i += __shfl_down_sync(0xffffffffu, n0i, o);
     cells += __shfl_down_sync(0xffffffffu, cells, o);
   }
   if (lane == 0) {
-    if (iters) atomicAdd(&ctl->newton, iters);
+    if (iters64) atomicAdd(&ctl->newton, iters64);
     if (misses) atomicAdd(&ctl->misses, misses);
     if (n0i) atomicAdd(&ctl->n0i, n0i);
     if (cells) atomicAdd(&ctl->tile_cells, cells);
