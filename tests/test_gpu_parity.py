@@ -383,3 +383,26 @@ def test_deep_plan_1000(oracle):
         assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), f"step {s}"
     g = ctx.download_graph()
     assert np.array_equal(g["order"], o["order"]) and np.array_equal(g["levels"], o["levels"])
+
+
+@pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_PATH": "global"}], ids=["tiles", "half-escape", "global"])
+def test_inexact_cell_area(oracle, monkeypatch, env):
+    """dx*dy with a full significand: the drainage area is the reference's FP
+    sum in slot order (bit-exact), pow(A, m) is evaluated on the device (lut
+    misses), so elevations agree within the stated tolerance."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    kw = {"dx": 0.1, "dy": 0.3}
+    ctx = device_ctx(100, 80, **kw)
+    for k in env:
+        monkeypatch.delenv(k)
+    e = oracle.terrain(100, 80, 17)
+    ctx.upload(e)
+    p = make_params(**kw)
+    for s in range(3):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, params=p)
+        hg = ctx.download()
+        compare_step(ctx, o, hg, e, exact_h=False, tag=f"{env} step {s}")
+        assert d.lut_misses > 0 and abs(d.newton_iters - o["newton_iters"]) <= 2
+        e[...] = hg
