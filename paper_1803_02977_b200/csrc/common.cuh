@@ -69,7 +69,7 @@ constexpr int kChunkTPB = 128;        // k_chunks CTA: 4 warps, 4 chunks in flig
 constexpr int kChunkMaxLevels = 24;   // shallow (chunked) plans: nlevels <= this
 constexpr int kCBS = kChunkMaxLevels + 1;
 
-enum : uint32_t { kModeShallow = 0, kModeDeep = 1, kModeFailed = 2 };
+enum : uint32_t { kModeShallow = 0, kModeDeep = 1, kModeFailed = 2, kModeDone = 3 };
 
 // Frozen D8 stencil (src/neighborhood.cpp:12): k -> (ox, oy).  The opposite
 // direction of k is 7-k.  D4 is the cardinal subsequence {1,3,4,6}
@@ -137,6 +137,7 @@ struct Ctl {
   // tile path (k_tiles): escaped roots, cells finished in tiles, interior pits, deepest level + 1
   uint32_t nesc, tile_cells, n0i, tile_nlev;
   uint32_t gbar_count, gbar_gen;  // grid barrier of the cooperative escape-path kernel
+  uint32_t esc_small;             // 1: k_esc_small finished the escaped trees this step
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
   uint32_t ntl, nltl;

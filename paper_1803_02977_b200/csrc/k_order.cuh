@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
 __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
   __shared__ ScanSmem sm;
   Ctl* ctl = a.ctl;
+  if (ld_volatile_u32(&ctl->esc_small)) return;  // k_esc_small finished the escaped trees (uniform)
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
   const uint32_t n = ld_volatile_u32(&ctl->nesc);

@@ -627,4 +627,148 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
 #undef ESC_GET
 #undef ESC_SET
 
+// ---------------------------------------------------------------------------
+// Few escaped trees (small rasters): one CTA finishes them in shared memory --
+// the same breadth-first levels (donor masks from the receiver codes), the
+// reference's FP accumulation in slot order, uplift and erosion level by
+// level -- instead of the cooperative global path, whose ~10 us per level
+// dominates a small step.  Too many roots, more than kEscSmallCap cells or
+// kEscSmallLev levels: nothing is written and the cooperative path runs.
+constexpr int kEscSmallRoots = 1024;
+constexpr int kEscSmallCap = 6144;
+constexpr int kEscSmallLev = 256;
+struct EscSmallSmem {
+  double h[kEscSmallCap];
+  double A[kEscSmallCap];
+  uint32_t cell[kEscSmallCap];
+  uint16_t par[kEscSmallCap];  // parent slot (roots: 0xFFFF)
+  uint16_t fc[kEscSmallCap];   // first child slot
+  uint8_t kd[kEscSmallCap];    // direction parent -> cell
+  uint8_t nk[kEscSmallCap];    // number of children
+  uint32_t lvl[kEscSmallLev + 1];
+  uint32_t scan[kNW + 1];
+  uint32_t flag;
+};
+constexpr size_t kEscSmallSmemBytes = sizeof(EscSmallSmem);
+
+template <int NK>
+__global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  EscSmallSmem& s = *reinterpret_cast<EscSmallSmem*>(smraw);
+  Ctl* ctl = a.ctl;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t n = ld_volatile_u32(&ctl->nesc);
+  if (ld_volatile_u32(&ctl->err_flag) || n > (uint32_t)kEscSmallRoots || n > (uint32_t)kEscSmallCap) return;
+  for (uint32_t i = tid; i < n; i += kTPB) {
+    s.cell[i] = a.order[i];
+    s.par[i] = 0xFFFFu;
+  }
+  if (tid == 0) {
+    s.lvl[0] = 0;
+    s.lvl[1] = n;
+    s.flag = 0;
+  }
+  __syncthreads();
+  // breadth-first levels
+  uint32_t nl = n ? 1u : 0u;
+  bool ok = true;
+  while (nl > 0) {
+    const uint32_t ls = s.lvl[nl - 1], le = s.lvl[nl];
+    uint32_t carry = le;
+    for (uint32_t b0 = ls; b0 < le; b0 += kTPB) {
+      const uint32_t i = b0 + tid;
+      uint32_t m = 0;
+      if (i < le) m = donor_mask_at(a, s.cell[i]);
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan((uint32_t)__popc(m), &tot, s.scan);
+      if (carry + tot > (uint32_t)kEscSmallCap) {
+        ok = false;  // uniform: tot and carry are block-wide
+        break;
+      }
+      if (i < le) {
+        uint32_t c = carry + ex;
+        s.fc[i] = (uint16_t)c;
+        s.nk[i] = (uint8_t)__popc(m);
+        const uint32_t cell = s.cell[i];
+        while (m) {
+          const uint32_t k = __ffs(m) - 1;
+          m &= m - 1;
+          s.cell[c] = (uint32_t)((int)cell + dir_off(k, (int)a.W));
+          s.par[c] = (uint16_t)i;
+          s.kd[c] = (uint8_t)k;
+          ++c;
+        }
+      }
+      carry += tot;
+    }
+    if (!ok) break;
+    __syncthreads();
+    if (carry == le) break;  // the next level is empty
+    if (nl == (uint32_t)kEscSmallLev) {
+      ok = false;
+      break;
+    }
+    if (tid == 0) s.lvl[nl + 1] = carry;
+    ++nl;
+    __syncthreads();
+  }
+  if (!ok) return;  // leave the trees to the cooperative path (nothing written)
+  const unsigned long long t_bfs = globaltimer();
+  // accumulation, deepest level first: A = w + the children's A in slot order
+  for (int l = (int)nl - 1; l >= 0; --l) {
+    for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
+      double A = a.w0;
+      const uint32_t nk = l + 1 < (int)nl ? s.nk[i] : 0u, c0 = s.fc[i];
+      for (uint32_t q = 0; q < nk; ++q) A = __dadd_rn(A, s.A[c0 + q]);
+      s.A[i] = A;
+    }
+    __syncthreads();
+  }
+  // uplift (level 0: interior sources only), erosion level by level
+  uint32_t iters = 0, misses = 0;
+  for (uint32_t l = 0; l < nl; ++l) {
+    for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
+      const uint32_t c = s.cell[i];
+      double hv = a.h[c];
+      if (l == 0) {
+        if (is_interior(a, c)) hv = __dadd_rn(hv, a.du);
+      } else {
+        const double h0 = __dadd_rn(hv, a.du);
+        const double hn = s.h[s.par[i]];
+        const uint32_t mem = a.M > 1 ? c / a.MN : 0u;
+        const double F = tile_F(a, mem, dir_class(s.kd[i]), s.A[i], misses);  // class symmetric in k <-> 7-k
+        int itn;
+        bool okn;
+        if (NK == 1)
+          hv = newton_n1(h0, hn, F, a.eps, a.maxit, itn, okn);
+        else
+          hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, okn);
+        if (okn) {
+          iters += (uint32_t)itn;
+        } else {
+          hv = h0;  // as chunk_in_global: the failed cell keeps its uplifted height
+          atomicMin(&ctl->err_cell, c);
+          ctl->err_slot = ctl->slot;
+          atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+        }
+      }
+      s.h[i] = hv;
+      a.hout[c] = hv;
+    }
+    __syncthreads();
+  }
+  flush_counters(ctl, iters, misses);
+  for (uint32_t l = tid; l <= nl; l += kTPB) a.levels[l] = s.lvl[l];
+  for (uint32_t i = tid; i < s.lvl[nl]; i += kTPB) a.order[i] = s.cell[i];
+  if (tid == 0) {
+    ctl->nlev = nl;
+    ctl->n0 = n;
+    ctl->mode = kModeDone;
+    ctl->esc_small = 1;
+    ctl->t_t_end = max(ctl->t_t_end, t_bfs);
+    ctl->t_order_end = t_bfs;
+    ctl->t_phys_end = globaltimer();
+  }
+}
+
 }  // namespace lemgpu

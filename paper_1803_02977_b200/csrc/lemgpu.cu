@@ -49,6 +49,7 @@ struct lemgpu_ctx {
   CUtensorMap hmap[2]{};  // TMA descriptors of hbuf[p]: k_recv_donor box
   CUtensorMap tmap[2]{};  // ... k_tiles box
   uint32_t* d_levels_esc = nullptr;
+  bool esc_small = true;  // k_esc_small ahead of the cooperative escape path
   // device allocations
   double* d_kdt = nullptr;
   double* d_mexp = nullptr;
@@ -224,6 +225,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
   const void* fk1 = ctx->use_tiles ? (a.conn == 8 ? (const void*)k_recv_donor<8, false> : (const void*)k_recv_donor<4, false>)
                                    : (a.conn == 8 ? (const void*)k_recv_donor<8, true> : (const void*)k_recv_donor<4, true>);
+  const void* fes = nk == 1 ? (const void*)k_esc_small<1> : nk == 2 ? (const void*)k_esc_small<2> : (const void*)k_esc_small<0>;
   const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   const void* fde = nk == 1 ? (const void*)k_deep_erode<1> : nk == 2 ? (const void*)k_deep_erode<2> : (const void*)k_deep_erode<0>;
   cudaGraphNode_t prev = nullptr;
@@ -233,6 +235,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
         (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
+        (ctx->esc_small &&
+         (rc = add_kernel(ctx, g, &prev, fes, dim3(1), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else {
@@ -435,7 +439,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   }
   a.eager = 0;
   a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
+  if (const char* env = std::getenv("LEMGPU_ESC_SMALL")) ctx->esc_small = std::atoi(env) != 0;
+  if (a.force_deep) ctx->esc_small = false;  // testing the deep sweeps of the escape path
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
+  for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
+    CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEscSmallSmemBytes));
   const void* fchunks = a.nkind == 1 ? (const void*)k_chunks<1> : a.nkind == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   CUB(cudaFuncSetAttribute(fchunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmemBytes));
   CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fchunks, kChunkTPB, kChunksSmemBytes));
@@ -553,6 +561,14 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     cfg.stream = st;
     void* args[] = {&a, &ctx->tmap[p]};
     CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
+    if (ctx->esc_small) {
+      if (a.nkind == 1)
+        k_esc_small<1><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+      else if (a.nkind == 2)
+        k_esc_small<2><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+      else
+        k_esc_small<0><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+    }
     void* eargs[] = {&a};
     CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
   } else {

@@ -326,16 +326,19 @@ def _ramp(w, h, seed):
 
 
 @pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_FORCE_ESCAPE": "2"},
-                                 {"LEMGPU_PATH": "global"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_FORCE_DEEP": "1"}],
-                         ids=["tiles", "all-escape", "half-escape", "global", "all-escape-deep"])
+                                 {"LEMGPU_PATH": "global"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_FORCE_DEEP": "1"},
+                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0"}],
+                         ids=["tiles", "all-escape", "half-escape", "global", "all-escape-deep", "all-escape-coop"])
 @pytest.mark.parametrize("w,h,seed,kw,terrain", [
     (300, 200, 31, {}, "noise"), (130, 97, 32, {"n_exp": 2.0}, "noise"), (77, 65, 33, {"dx": 0.5}, "noise"),
-    (129, 70, 34, {}, "ramp"), (90, 61, 35, {}, "ramp"),
+    (129, 70, 34, {}, "ramp"), (90, 61, 35, {}, "ramp"), (400, 12, 36, {}, "ramp"), (61, 40, 37, {"n_exp": 2.0}, "ramp"),
 ])
 def test_schedules_agree_with_oracle(oracle, monkeypatch, env, w, h, seed, kw, terrain):
     """Every schedule -- trees finished inside their tile (k_tiles), trees that
-    escape to the global level path (all of them, or every odd-rooted one),
-    the global path alone, and its per-level sweeps -- gives the oracle's bits."""
+    escape to the global level path (all of them, or every odd-rooted one; in
+    k_esc_small's shared memory when they fit, <= 6144 cells and <= 256 levels,
+    else -- or with LEMGPU_ESC_SMALL=0 -- in the cooperative kernels), the
+    global path alone, and its per-level sweeps -- gives the oracle's bits."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     ctx = device_ctx(w, h, **kw)
