@@ -95,9 +95,9 @@ __host__ __device__ __forceinline__ uint8_t receiver_code(const double (&d)[8], 
 // the unique strict maximum of the reference slopes as well.  Ties, near
 // ties, subnormal or non-finite maxima take the reference loop
 // (tests/native/test_receiver_code.cu checks this against the loop).
-template <int CONN>
+template <int CONN, bool UNIT = false>  // UNIT: the caller knows a.unit_card
 __host__ __device__ __forceinline__ uint8_t receiver_code_hi(const double (&d)[8], const StepArgs& a) {
-  if (CONN == 8 && a.unit_card) {
+  if (CONN == 8 && (UNIT || a.unit_card)) {
     int hi[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -106,14 +106,17 @@ __host__ __device__ __forceinline__ uint8_t receiver_code_hi(const double (&d)[8
     }
     auto mx2 = [](int u, int v) { return u > v ? u : v; };
     const int mx = mx2(mx2(mx2(hi[0], hi[1]), mx2(hi[2], hi[3])), mx2(mx2(hi[4], hi[5]), mx2(hi[6], hi[7])));
-    if (mx < 0) return kNoFlowCode;  // every drop negative or -0: no downhill neighbour
-    if (mx < 0x00100000) {           // no normal positive slope: +0 drops (flats) or subnormal ones
-      bool pos = false;
+    // one unsigned range test for the common case, a normal finite positive maximum
+    if ((uint32_t)(mx - 0x00100000) >= 0x7FE00000u) {
+      if (mx < 0) return kNoFlowCode;  // every drop negative or -0: no downhill neighbour
+      if (mx < 0x00100000) {           // no normal positive slope: +0 drops (flats) or subnormal ones
+        bool pos = false;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pos |= d[k] > 0.0;
-      return pos ? receiver_code_ref<CONN>(d, a) : kNoFlowCode;
+        for (int k = 0; k < 8; ++k) pos |= d[k] > 0.0;
+        return pos ? receiver_code_ref<CONN>(d, a) : kNoFlowCode;
+      }
+      return receiver_code_ref<CONN>(d, a);  // inf / NaN
     }
-    if (mx >= 0x7FF00000) return receiver_code_ref<CONN>(d, a);
     const int thr = mx - 1;
     uint32_t cand = 0;
 #pragma unroll
@@ -346,6 +349,176 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
           if (DONORS) a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());
+}
+
+// ballot of (w & mask) != 0 -- one predicate-setting LOP3 per vote
+__device__ __forceinline__ uint32_t ballot_bits(uint32_t w, uint32_t mask) {
+  uint32_t r;
+  asm volatile(
+      "{ .reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 %0, p, 0xffffffff; }"
+      : "=r"(r)
+      : "r"(w), "r"(mask));
+  return r;
+}
+
+// The tile path's receiver pass: receiver codes (rcode, one byte per cell) and
+// their bit planes, nothing else.  Each thread owns one column of the
+// kBY x kBX tile and half of its rows (16) and slides a 3x3 register window
+// down it.  Pass 1 is branch-free: the division-free selection of
+// receiver_code_hi's common case for all 16 cells, codes packed as nibbles in
+// two registers, undecided cells (near ties, flats, non-finite drops) flagged.
+// Pass 2 settles the flagged cells with the full selection (rare).  Pass 3
+// stores: 32 contiguous code bytes per warp and row, and the bit planes as
+// four ballots of that warp row.  UNIT: D8 with unit cardinal spacing;
+// otherwise every cell takes the reference loop in pass 2.
+template <int CONN, bool UNIT>
+__global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
+    k_recv(const __grid_constant__ StepArgs a, const __grid_constant__ CUtensorMap hmap) {
+  __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
+  __shared__ __align__(8) uint64_t bar;
+  if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+  const uint32_t W = a.W, Ht = a.Htot;
+  if (tid == 0) {
+    atomicMin(&a.ctl->t_k1_begin, globaltimer());
+    if (a.use_tma) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (uint32_t)sizeof(sh));
+      tma_load_2d(&sh[0][0], &hmap, (int)x0 - 2, (int)y0 - 2, &bar);
+    }
+  }
+  if (!a.use_tma) for (int r = warp; r < kBY + 4; r += kNW) {
+    const int gy = (int)y0 - 2 + r;
+    const bool rowok = gy >= 0 && (uint32_t)gy < Ht;
+    const double* row = a.h + (size_t)(rowok ? gy : 0) * W;
+#pragma unroll
+    for (int j = 0; j < kBX / 32; ++j) {
+      const uint32_t gx = x0 + lane + 32 * j;
+      sh[r][2 + lane + 32 * j] = (rowok && gx < W) ? __ldg(row + gx) : 0.0;
+    }
+    if (lane < 4) {
+      const int cc = lane < 2 ? lane : kBX + lane;
+      const int gx = (int)x0 - 2 + cc;
+      sh[r][cc] = (rowok && gx >= 0 && (uint32_t)gx < W) ? __ldg(row + gx) : 0.0;
+    }
+  }
+  static_assert(kBY == 32, "16 rows per thread, codes in two nibble words");
+  const int cx = tid & (kBX - 1);  // window columns sh cx+1..cx+3, centre gx
+  const uint32_t gx = x0 + cx;
+  const int t0 = tid < kBX ? 0 : kBY / 2;  // this thread's rows: t0 .. t0+15
+  // interior rows (members are stacked; their first and last rows are base
+  // level): bit i <-> tile row t0 + i
+  uint32_t rows;
+  {
+    const uint32_t gy = y0 + (uint32_t)t0 + (uint32_t)(lane & 15);
+    bool ok = gy < Ht;
+    if (ok) {
+      const uint32_t yl = gy % a.H;
+      ok = yl > 0 && yl < a.H - 1;
+    }
+    rows = __ballot_sync(0xffffffffu, ok) & 0xFFFFu;
+  }
+  if (!(gx > 0 && gx < W - 1)) rows = 0;
+  __syncthreads();
+  if (a.use_tma) mbar_wait(&bar, 0);
+
+  // ---- pass 1
+  const double* col = &sh[t0][cx + 1];  // sh row t0, window column 0
+  constexpr int kRow = kBX + 4;
+  uint32_t cw0 = 0u, cw1 = 0u;  // code of row i in nibble i&7 of cw0 (i < 8) / cw1
+  uint32_t slow = 0;
+  if (CONN == 8 && UNIT) {
+    const double rinv = a.rinv_diag;
+    double w[3][3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      w[0][q] = col[1 * kRow + q];
+      w[1][q] = col[2 * kRow + q];
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      // window rows: north (i+1)%3, centre (i+2)%3 = the row loaded last, south i%3 (new)
+      double (&s)[3] = w[(i + 2) % 3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) s[q] = col[(i + 3) * kRow + q];
+      const double (&u)[3] = w[i % 3];
+      const double (&m)[3] = w[(i + 1) % 3];
+      const double ec = m[1];
+      const int h0 = hi_word(LG_MUL(LG_SUB(ec, u[0]), rinv)), h1 = hi_word(LG_SUB(ec, u[1]));
+      const int h2 = hi_word(LG_MUL(LG_SUB(ec, u[2]), rinv)), h3 = hi_word(LG_SUB(ec, m[0]));
+      const int h4 = hi_word(LG_SUB(ec, m[2])), h5 = hi_word(LG_MUL(LG_SUB(ec, s[0]), rinv));
+      const int h6 = hi_word(LG_SUB(ec, s[1])), h7 = hi_word(LG_MUL(LG_SUB(ec, s[2]), rinv));
+      const int mx = max(max(max(h0, h1), max(h2, h3)), max(max(h4, h5), max(h6, h7)));
+      const int thr = mx - 1;
+      const uint32_t cand = (h0 >= thr ? 1u : 0u) | (h1 >= thr ? 2u : 0u) | (h2 >= thr ? 4u : 0u) |
+                            (h3 >= thr ? 8u : 0u) | (h4 >= thr ? 16u : 0u) | (h5 >= thr ? 32u : 0u) |
+                            (h6 >= thr ? 64u : 0u) | (h7 >= thr ? 128u : 0u);
+      const bool interior = (rows >> i) & 1u;
+      const bool easy = (uint32_t)(mx - 0x00100000) < 0x7FE00000u && (cand & (cand - 1u)) == 0;
+      const uint32_t code = interior ? (uint32_t)(__ffs(cand) - 1) : kNoFlowCode;
+      if (i < 8)
+        cw0 |= (code & 15u) << (4 * (i & 7));
+      else
+        cw1 |= (code & 15u) << (4 * (i & 7));
+      slow |= (interior && !easy ? 1u : 0u) << i;
+    }
+  } else {
+    cw0 = cw1 = 0x11111111u * kNoFlowCode;  // non-interior cells
+    slow = rows;
+  }
+  // ---- pass 2: cells pass 1 left undecided
+  while (slow) {
+    const int i = __ffs(slow) - 1;
+    slow &= slow - 1;
+    const double* cc = col + (i + 1) * kRow;  // north row of cell i
+    const double ec = cc[kRow + 1];
+    double d[8];
+    d[0] = LG_SUB(ec, cc[0]);
+    d[1] = LG_SUB(ec, cc[1]);
+    d[2] = LG_SUB(ec, cc[2]);
+    d[3] = LG_SUB(ec, cc[kRow]);
+    d[4] = LG_SUB(ec, cc[kRow + 2]);
+    d[5] = LG_SUB(ec, cc[2 * kRow]);
+    d[6] = LG_SUB(ec, cc[2 * kRow + 1]);
+    d[7] = LG_SUB(ec, cc[2 * kRow + 2]);
+    if (CONN == 4) d[0] = d[2] = d[5] = d[7] = 0.0;
+    const uint32_t code = UNIT ? receiver_code_hi<CONN, true>(d, a) : receiver_code_ref<CONN>(d, a);
+    const int sh4 = 4 * (i & 7);
+    if (i < 8)
+      cw0 = (cw0 & ~(15u << sh4)) | (code << sh4);
+    else
+      cw1 = (cw1 & ~(15u << sh4)) | (code << sh4);
+  }
+  // ---- pass 3: stores
+  const int nr = min(kBY / 2, max(0, (int)Ht - (int)(y0 + (uint32_t)t0)));  // rows inside the raster (warp-uniform)
+  const uint32_t j = x0 / 32 + (uint32_t)(cx >> 5);  // plane word of this warp's columns
+  const bool xok = gx < W, pok = lane < 4 && j < a.W32;
+  if (!xok) cw0 = cw1 = 0xFFFFFFFFu;  // bit planes: columns beyond W read as code 15
+  uint8_t* rp = a.rcode + (size_t)(y0 + (uint32_t)t0) * W + gx;
+  uint32_t* pp = a.planes + ((size_t)(lane & 3) * Ht + y0 + (uint32_t)t0) * a.W32 + j;
+  const size_t W32 = a.W32;
+  const bool p1 = lane & 1, p2 = lane & 2;
+  auto store_row = [&](int i) {
+    const uint32_t w = i < 8 ? cw0 : cw1;
+    const int sh4 = 4 * (i & 7);
+    if (xok) *rp = (uint8_t)((w >> sh4) & 15u);
+    const uint32_t b0 = ballot_bits(w, 1u << sh4), b1 = ballot_bits(w, 2u << sh4);
+    const uint32_t b2 = ballot_bits(w, 4u << sh4), b3 = ballot_bits(w, 8u << sh4);
+    if (pok) *pp = p2 ? (p1 ? b3 : b2) : (p1 ? b1 : b0);
+    rp += W;
+    pp += W32;
+  };
+  if (nr == kBY / 2) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) store_row(i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < nr) store_row(i);
   }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());

@@ -653,7 +653,7 @@ constexpr size_t kEscSmallSmemBytes = sizeof(EscSmallSmem);
 
 template <int NK>
 __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   EscSmallSmem& s = *reinterpret_cast<EscSmallSmem*>(smraw);
   Ctl* ctl = a.ctl;
   const uint32_t tid = threadIdx.x;

@@ -208,6 +208,11 @@ const void* tiles_fn(const StepArgs& a) {
   if (a.lut_exact) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
   return a.conn == 8 ? tiles_fn_nk<8, false>(a.nkind) : tiles_fn_nk<4, false>(a.nkind);
 }
+// the tile path's receiver pass (k_recv): division-free selection for D8 with unit cardinal spacing
+const void* recv_fn(const StepArgs& a) {
+  if (a.conn == 4) return (const void*)k_recv<4, false>;
+  return a.unit_card ? (const void*)k_recv<8, true> : (const void*)k_recv<8, false>;
+}
 size_t tiles_smem(const StepArgs& a) { return a.lut_exact ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>(); }
 
 int build_graph(lemgpu_ctx* ctx, uint32_t p) {
@@ -223,7 +228,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   }
   const int nk = a.nkind;
   const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
-  const void* fk1 = ctx->use_tiles ? (a.conn == 8 ? (const void*)k_recv_donor<8, false> : (const void*)k_recv_donor<4, false>)
+  const void* fk1 = ctx->use_tiles ? recv_fn(a)
                                    : (a.conn == 8 ? (const void*)k_recv_donor<8, true> : (const void*)k_recv_donor<4, true>);
   const void* fes = nk == 1 ? (const void*)k_esc_small<1> : nk == 2 ? (const void*)k_esc_small<2> : (const void*)k_esc_small<0>;
   const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
@@ -550,10 +555,10 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   set_eager_conds(a, st);
   if (ctx->use_tiles) {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-    if (a.conn == 8)
-      k_recv_donor<8, false><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
-    else
-      k_recv_donor<4, false><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+    {
+      void* rargs[] = {&a, &ctx->hmap[p]};
+      CU(ctx, cudaLaunchKernel(recv_fn(a), g1, dim3(kTPB), rargs, 0, st));
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->tile_grid);
     cfg.blockDim = dim3(kTTPB);
