@@ -333,7 +333,8 @@ def main():
             lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
         e2e = {"value": total_cells * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": cells * 8,
                "d2h_bytes_per_step": cells * 8, "steps": args.e2e_steps,
-               "path": "lemgpu_step_host (strategy_step on a host raster: H2D, step, D2H per call)",
+               "path": "lemgpu_step_host (strategy_step on a host raster: the whole raster H2D and D2H per call, "
+                       "in bands overlapped with the step; escaped trees patched in)",
                "pinned": bool(reg)}
 
     peak, peak_src = load_peaks()

@@ -196,6 +196,8 @@ struct StepArgs {
   int force_deep;     // testing: use the per-level sweeps even for shallow plans
   int force_escape;   // testing: 1 = every tree of k_tiles escapes, 2 = trees of odd root cells escape
   int tiles;          // 1: the step runs k_tiles + the escape path (else the global level path)
+  uint32_t by0;       // k_recv: first row block of the launch (banded host steps; else 0)
+  uint32_t t_lo, t_hi;  // k_tiles: tile range of the launch (t_hi 0: every tile)
   int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
   Ctl* ctl;

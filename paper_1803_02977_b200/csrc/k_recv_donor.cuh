@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
   __shared__ __align__(8) uint64_t bar;
   if (ld_volatile_u32(&a.ctl->err_flag)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+  const uint32_t x0 = blockIdx.x * kBX, y0 = (blockIdx.y + a.by0) * kBY;
   const uint32_t W = a.W, Ht = a.Htot;
   if (tid == 0) {
     atomicMin(&a.ctl->t_k1_begin, globaltimer());

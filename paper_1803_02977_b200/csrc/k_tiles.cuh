@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   unsigned long long iters64 = 0;  // per thread
   uint32_t misses = 0, cells = 0, n0i = 0, maxl = 0;
   uint32_t phase = 0;
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1u) {
+  const uint32_t t_end = a.t_hi ? a.t_hi : ntiles;  // banded host steps launch one band of tile rows at a time
+  for (uint32_t t = a.t_lo + blockIdx.x; t < t_end; t += gridDim.x, phase ^= 1u) {
     const int tx0 = (int)(t % ntx) * kTX, ty0 = (int)(t / ntx) * kTY;
     const int wx0 = tx0 - kLX, wy0 = ty0 - kLY;
     const uint32_t gbase = (uint32_t)wy0 * a.W + (uint32_t)wx0;  // global index of window (0, 0), mod 2^32
@@ -626,6 +627,24 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
 #undef RC
 #undef ESC_GET
 #undef ESC_SET
+
+// Banded host steps: the final elevation of every cell of the escaped trees
+// (the escape path wrote them after the bands were copied out), for the host
+// to patch in.  count = cells placed by the escape path's level expansion.
+// cells / vals / count are mapped pinned host memory (written over PCIe);
+// more than cap cells: only the count is written.
+__global__ void __launch_bounds__(kTPB) k_esc_gather(StepArgs a, uint32_t* cells, double* vals, uint32_t* count,
+                                                     uint32_t cap) {
+  const Ctl* ctl = a.ctl;
+  const uint32_t n = ctl->nesc && !ctl->err_flag ? a.levels[ctl->nlev] : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
+  if (n > cap) return;
+  for (uint32_t i = blockIdx.x * kTPB + threadIdx.x; i < n; i += gridDim.x * kTPB) {
+    const uint32_t c = a.order[i];
+    cells[i] = c;
+    vals[i] = a.hout[c];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Few escaped trees (small rasters): one CTA finishes them in shared memory --

@@ -10,6 +10,8 @@
 // distances (neighborhood.hpp:17-23), pow(dist, n) and the pow(A, m) table.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -18,6 +20,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lemgpu.h"
@@ -50,6 +53,12 @@ struct lemgpu_ctx {
   CUtensorMap tmap[2]{};  // ... k_tiles box
   uint32_t* d_levels_esc = nullptr;
   bool esc_small = true;  // k_esc_small ahead of the cooperative escape path
+  // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> band_ev;
+  uint32_t* h_patch = nullptr;  // mapped pinned: count, then cells[patch_cap], then vals[patch_cap]
+  uint32_t patch_cap = 0;
+  int bands = 0;  // 0: one band per ~25 MB of raster, at most 32 (fewer than 4: no banding)
   // device allocations
   double* d_kdt = nullptr;
   double* d_mexp = nullptr;
@@ -445,6 +454,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.eager = 0;
   a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
   if (const char* env = std::getenv("LEMGPU_ESC_SMALL")) ctx->esc_small = std::atoi(env) != 0;
+  if (const char* env = std::getenv("LEMGPU_HOST_BANDS")) ctx->bands = std::atoi(env);
+  if (ctx->bands <= 0) {  // measured on 10000^2 (tools/e2e_probe.py): 32 bands of 25 MB beat 16 and 64
+    const uint64_t nbands = N64 * 8 / (25ull << 20);
+    ctx->bands = (int)std::min<uint64_t>(32, nbands < 4 ? 1 : nbands);
+  }
   if (a.force_deep) ctx->esc_small = false;  // testing the deep sweeps of the escape path
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
   for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
@@ -548,6 +562,22 @@ void set_eager_conds(const StepArgs& a, cudaStream_t st) {
   cudaStreamSynchronize(st);  // init is host memory
 }
 
+// The tile path after k_tiles, launched eagerly: k_esc_small, the cooperative
+// level expansion of the escaped trees, their physics.
+int enqueue_escape_eager(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
+  if (ctx->esc_small) {
+    if (a.nkind == 1)
+      k_esc_small<1><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+    else if (a.nkind == 2)
+      k_esc_small<2><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+    else
+      k_esc_small<0><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+  }
+  void* eargs[] = {&a};
+  CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
+  return run_levels_eager(ctx, a);
+}
+
 int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   StepArgs a = step_args(ctx, p);
   a.eager = 1;
@@ -566,16 +596,8 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     cfg.stream = st;
     void* args[] = {&a, &ctx->tmap[p]};
     CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
-    if (ctx->esc_small) {
-      if (a.nkind == 1)
-        k_esc_small<1><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
-      else if (a.nkind == 2)
-        k_esc_small<2><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
-      else
-        k_esc_small<0><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
-    }
-    void* eargs[] = {&a};
-    CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
+    const int rc = enqueue_escape_eager(ctx, a, st);
+    if (rc) return rc;
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
@@ -584,11 +606,182 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
       k_recv_donor<4, true><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
+    const int rc = run_levels_eager(ctx, a);
+    if (rc) return rc;
   }
-  const int rc = run_levels_eager(ctx, a);
-  if (rc) return rc;
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
+  return LEMGPU_OK;
+}
+
+// One step on a HOST raster with the copies overlapped: the raster is cut into
+// bands of tile rows; band b goes up on one stream while the compute stream
+// runs k_recv on band b-1 and k_tiles on band b-2, and a third stream copies
+// band b-3's new elevations down as soon as no tile tree can still write them
+// (the tiles of the band below have run).  The escaped trees are finished
+// after the last band; their cells' final values are gathered and patched
+// into the host raster.  A PCIe-bound step then costs about one raster copy
+// instead of two.  Requires pinned host memory (else the copies would not
+// overlap) and the tile path.
+int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
+  const auto tb0 = std::chrono::steady_clock::now();
+  if (ctx->pending) {
+    const int rc0 = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc0) return rc0;
+  }
+  const uint32_t p = ctx->cur;
+  StepArgs a = step_args(ctx, p);
+  a.eager = 1;
+  cudaStream_t st = ctx->stream;
+  set_eager_conds(a, st);
+  if (!ctx->s_h2d) {
+    CU(ctx, cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+    CU(ctx, cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    // room for the escaped trees of a typical step (a few % of the cells);
+    // more than that and the whole raster is copied down again
+    ctx->patch_cap = std::max<uint32_t>(1u << 20, a.N / 16);
+    if (const char* env = std::getenv("LEMGPU_PATCH_CAP")) ctx->patch_cap = (uint32_t)std::atoi(env);  // testing
+    ctx->patch_cap = (ctx->patch_cap + 63u) & ~63u;  // the vals after the cells stay 8-byte aligned
+    CU(ctx, cudaHostAlloc(&ctx->h_patch, 16 + (size_t)ctx->patch_cap * 12, cudaHostAllocMapped));
+  }
+  const uint32_t W = a.W, Ht = a.Htot;
+  const uint32_t ntx = (W + kTX - 1) / kTX, nty = (Ht + kTY - 1) / kTY;
+  const uint32_t R = (nty + (uint32_t)ctx->bands - 1) / (uint32_t)ctx->bands;  // tile rows per band
+  const uint32_t nb = (nty + R - 1) / R;
+  while (ctx->band_ev.size() < 2 * (size_t)nb + 1) {
+    cudaEvent_t e;
+    CU(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->band_ev.push_back(e);
+  }
+  cudaEvent_t* eh = ctx->band_ev.data();  // band b uploaded
+  cudaEvent_t* et = eh + nb;              // band b's tiles done
+  cudaEvent_t e0 = eh[2 * nb];
+  cudaEvent_t* tev = nullptr;
+  if (ctx->timing) {  // step events as enqueue_step records them
+    while (ctx->ev.size() < 2) {
+      cudaEvent_t e;
+      CU(ctx, cudaEventCreate(&e));
+      ctx->ev.push_back(e);
+    }
+    tev = &ctx->ev[0];
+    CU(ctx, cudaEventRecord(tev[0], st));
+  }
+  CU(ctx, cudaEventRecord(e0, st));  // earlier work on the context stream
+  CU(ctx, cudaStreamWaitEvent(ctx->s_h2d, e0, 0));
+  CU(ctx, cudaStreamWaitEvent(ctx->s_d2h, e0, 0));
+  auto rows = [&](uint32_t b, uint32_t& r0, uint32_t& r1) {
+    r0 = b * R * (uint32_t)kTY;
+    r1 = std::min((b + 1) * R * (uint32_t)kTY, Ht);
+  };
+  for (uint32_t b = 0; b < nb; ++b) {
+    uint32_t r0, r1;
+    rows(b, r0, r1);
+    CU(ctx, cudaMemcpyAsync(ctx->hbuf[p] + (size_t)r0 * W, elev + (size_t)r0 * W, (size_t)(r1 - r0) * W * sizeof(double),
+                            cudaMemcpyHostToDevice, ctx->s_h2d));
+    CU(ctx, cudaEventRecord(eh[b], ctx->s_h2d));
+  }
+  // k_recv of band b reads h two rows into band b+1; k_tiles of band b reads
+  // codes kLY+1 rows into band b+1
+  auto recv = [&](uint32_t b) -> int {
+    CU(ctx, cudaStreamWaitEvent(st, eh[std::min(b + 1, nb - 1)], 0));
+    uint32_t r0, r1;
+    rows(b, r0, r1);
+    StepArgs ab = a;
+    ab.by0 = r0 / kBY;
+    const dim3 g((W + kBX - 1) / kBX, (r1 - r0 + kBY - 1) / kBY);
+    void* rargs[] = {&ab, &ctx->hmap[p]};
+    CU(ctx, cudaLaunchKernel(recv_fn(a), g, dim3(kTPB), rargs, 0, st));
+    return LEMGPU_OK;
+  };
+  static_assert(kBY == kTY, "bands of whole tile rows are whole k_recv row blocks");
+  int rc = recv(0);
+  if (rc) return rc;
+  for (uint32_t b = 0; b < nb; ++b) {
+    if (b + 1 < nb && (rc = recv(b + 1))) return rc;
+    StepArgs ab = a;
+    ab.t_lo = b * R * ntx;
+    ab.t_hi = std::min((b + 1) * R, nty) * ntx;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min<uint32_t>((uint32_t)ctx->tile_grid, ab.t_hi - ab.t_lo));
+    cfg.blockDim = dim3(kTTPB);
+    cfg.dynamicSmemBytes = tiles_smem(a);
+    cfg.stream = st;
+    void* args[] = {&ab, &ctx->tmap[p]};
+    CU(ctx, cudaLaunchKernelExC(&cfg, tiles_fn(a), args));
+    CU(ctx, cudaEventRecord(et[b], st));
+    // once band b's tiles have run, band b is final (escaped trees aside)
+    // except its last kHalo rows, which trees of band b+1 may still reach,
+    // and band b-1's last kHalo rows are final
+    auto down = [&](uint32_t r0, uint32_t r1) -> int {
+      if (r1 > r0)
+        CU(ctx, cudaMemcpyAsync(elev + (size_t)r0 * W, ctx->hbuf[p ^ 1u] + (size_t)r0 * W,
+                                (size_t)(r1 - r0) * W * sizeof(double), cudaMemcpyDeviceToHost, ctx->s_d2h));
+      return LEMGPU_OK;
+    };
+    uint32_t r0, r1;
+    rows(b, r0, r1);
+    CU(ctx, cudaStreamWaitEvent(ctx->s_d2h, et[b], 0));
+    if (b >= 1) {
+      uint32_t q0, q1;
+      rows(b - 1, q0, q1);
+      if ((rc = down(q1 - std::min<uint32_t>(kHalo, q1 - q0), q1))) return rc;
+    }
+    const uint32_t body_end = b + 1 < nb ? r1 - std::min<uint32_t>(kHalo, r1 - r0) : r1;
+    if ((rc = down(r0, body_end))) return rc;
+  }
+  if ((rc = enqueue_escape_eager(ctx, a, st))) return rc;
+  {
+    char* hp = nullptr;
+    CU(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&hp), ctx->h_patch, 0));
+    k_esc_gather<<<ctx->scan_grid, kTPB, 0, st>>>(a, reinterpret_cast<uint32_t*>(hp + 16),
+                                                 reinterpret_cast<double*>(hp + 16 + (size_t)ctx->patch_cap * 4),
+                                                 reinterpret_cast<uint32_t*>(hp), ctx->patch_cap);
+  }
+  k_finalize<<<1, 32, 0, st>>>(a);
+  CU(ctx, cudaGetLastError());
+  if (tev) CU(ctx, cudaEventRecord(tev[1], st));
+  ctx->cur = p ^ 1u;
+  ++ctx->pending;
+  ctx->have_graph = true;
+  using clk = std::chrono::steady_clock;
+  const auto tq0 = clk::now();
+  CU(ctx, cudaStreamSynchronize(ctx->s_d2h));
+  const auto tq1 = clk::now();
+  lemgpu_diag d{};
+  uint32_t cnt = 0;
+  rc = lemgpu_sync(ctx, &d, 1, &cnt);
+  const auto tq2 = clk::now();
+  if (diag) *diag = d;
+  if (rc) {  // the failed step leaves the elevation as it was: its input buffer
+    if (rc != LEMGPU_ECUDA)
+      cudaMemcpy(elev, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost);
+    return rc;
+  }
+  // patch the cells of the escaped trees
+  const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctx->h_patch);
+  if (n > ctx->patch_cap) {
+    CU(ctx, cudaMemcpy(elev, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost));
+  } else {
+    const uint32_t* cells = ctx->h_patch + 4;
+    const double* vals = reinterpret_cast<const double*>(reinterpret_cast<const char*>(ctx->h_patch) + 16 +
+                                                         (size_t)ctx->patch_cap * 4);
+    // random writes into the raster: latency-bound, spread over a few threads
+    const uint32_t nt = n < 65536u ? 1u : std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
+    auto part = [&](uint32_t t) {
+      const uint32_t i0 = (uint32_t)((uint64_t)n * t / nt), i1 = (uint32_t)((uint64_t)n * (t + 1) / nt);
+      for (uint32_t i = i0; i < i1; ++i) elev[cells[i]] = vals[i];
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(part, t);
+    part(0);
+    for (auto& th : pool) th.join();
+  }
+  if (std::getenv("LEMGPU_HOST_PROFILE")) {
+    const auto tq3 = clk::now();
+    auto ms = [](clk::duration x) { return std::chrono::duration<double, std::milli>(x).count(); };
+    std::fprintf(stderr, "step_host_banded: enqueue %.3f ms, then d2h done %.3f ms, sync %.3f ms, patch of %u cells %.3f ms\n",
+                 ms(tq0 - tb0), ms(tq1 - tq0), ms(tq2 - tq1), n, ms(tq3 - tq2));
+  }
   return LEMGPU_OK;
 }
 
@@ -651,6 +844,10 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
     if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
   }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  for (cudaEvent_t e : ctx->band_ev) cudaEventDestroy(e);
+  if (ctx->h_patch) cudaFreeHost(ctx->h_patch);
   delete ctx;
 }
 
@@ -807,6 +1004,12 @@ int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag) {
   if (!ctx || !elev_inout) return fail(ctx, LEMGPU_ECONFIG, "null argument");
   CU(ctx, cudaSetDevice(ctx->device));
   const StepArgs& a = ctx->a;
+  if (ctx->use_tiles && ctx->bands > 1 && !a.eager) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, elev_inout) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+      return step_host_banded(ctx, elev_inout, diag);
+    cudaGetLastError();  // pageable memory: the copies would not overlap
+  }
   CU(ctx, cudaMemcpyAsync(ctx->hbuf[ctx->cur], elev_inout, (size_t)a.N * sizeof(double), cudaMemcpyHostToDevice,
                           ctx->stream));
   int rc = lemgpu_step_async(ctx, 1);

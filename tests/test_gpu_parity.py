@@ -409,3 +409,57 @@ def test_inexact_cell_area(oracle, monkeypatch, env):
         compare_step(ctx, o, hg, e, exact_h=False, tag=f"{env} step {s}")
         assert d.lut_misses > 0 and abs(d.newton_iters - o["newton_iters"]) <= 2
         e[...] = hg
+
+
+def _host_register(a):
+    return lem._abi.lib().lemgpu_host_register(a.ctypes.data, a.nbytes) == 0
+
+
+@pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0"},
+                                 {"LEMGPU_FORCE_ESCAPE": "2", "LEMGPU_PATCH_CAP": "64"}],
+                         ids=["tiles", "half-escape", "all-escape-coop", "patch-overflow"])
+@pytest.mark.parametrize("w,h,terrain", [(300, 250, "noise"), (200, 170, "ramp"), (131, 97, "noise")])
+def test_step_host_banded(oracle, monkeypatch, env, w, h, terrain):
+    """lemgpu_step_host (the strategy_step drop-in) on pinned host memory: the
+    raster goes up and comes down band by band, overlapped with the compute,
+    and the escaped trees' cells are patched in afterwards (or, past the patch
+    capacity, the whole raster comes down again) -- the oracle's bits."""
+    monkeypatch.setenv("LEMGPU_HOST_BANDS", "4")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = device_ctx(w, h)
+    monkeypatch.delenv("LEMGPU_HOST_BANDS")
+    for k in env:
+        monkeypatch.delenv(k)
+    e = oracle.terrain(w, h, 41) if terrain == "noise" else _ramp(w, h, 41)
+    host = e.copy()
+    assert _host_register(host)
+    try:
+        for s in range(3):
+            d = ctx.step_host(host)
+            o = oracle.step(e, want_donor=False)
+            bad = np.nonzero(host.view(np.uint64) != e.view(np.uint64))
+            assert bad[0].size == 0, f"step {s}: {bad[0].size} cells differ, first {list(zip(*bad))[:3]}"
+            assert d.nlevels == o["nlevels"] and d.newton_iters == o["newton_iters"]
+    finally:
+        lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
+
+
+def test_step_host_pageable_and_failure(oracle):
+    """Pageable host memory takes the plain copy-step-copy path (same bits); a
+    failing banded step leaves the pinned host raster as it was."""
+    e = oracle.terrain(150, 120, 43)
+    ctx = device_ctx(150, 120)
+    host = e.copy()
+    ctx.step_host(host)
+    oracle.step(e, want_donor=False)
+    assert np.array_equal(host.view(np.uint64), e.view(np.uint64))
+    bad_ctx = device_ctx(150, 120, max_newton_iters=1)
+    pinned = e.copy()
+    assert _host_register(pinned)
+    try:
+        with pytest.raises(lem.ConvergenceError):
+            bad_ctx.step_host(pinned)
+        assert np.array_equal(pinned.view(np.uint64), e.view(np.uint64))
+    finally:
+        lem._abi.lib().lemgpu_host_unregister(pinned.ctypes.data)
