@@ -37,7 +37,7 @@ METRIC = "cell-steps/s, 10000² DEM, 1 GPU; ensemble cell-steps/s at 1/2/4/8 B20
 UNIT = "cell-steps/s"
 PAPER_P100 = 1e8 * 120 / 70.0  # RB+GPU 10000^2 x 120 steps in 70 s on one P100
 # Algorithmic bytes per cell-step: receivers 12 + donors 5 + order 9 + accumulation 21 +
-# uplift/erosion 40 = 87.  k_recv_donor does receivers + donors (17 B/cell); k_tiles does order,
+# uplift/erosion 40 = 87.  k_recv does receivers + donors (17 B/cell); k_tiles does order,
 # accumulation, uplift and erosion (70 B/cell) for the cells it finishes, moving only ~18 B/cell
 # (h in 8, h out 8, receiver code 1, code bit planes 0.5) -- the 'traffic' key, from ncu.
 B_STEP = 87
@@ -49,6 +49,12 @@ WORKLOADS = {
                      desc="10000x10000 random-noise DEM, D8, m=0.5 n=1, fixed-perimeter base level, seed 42 (configs[1])"),
     "dem1000": dict(w=1000, h=1000, members=1, n_exp=1.0, desc="1000x1000 random-noise DEM, D8, n=1 (configs[0]; L2-resident)"),
     "dem4000n2": dict(w=4000, h=4000, members=1, n_exp=2.0, desc="4000x4000 random-noise DEM, D8, n=2 Newton (configs[2])"),
+    "dem1000fill": dict(w=1000, h=1000, members=1, n_exp=1.0, fill=2,
+                        desc="1000x1000 random-noise DEM, Priority-Flood epsilon-filled (1e-8), D8, n=1: "
+                             "the deep-level regime (SURVEY 8(f) rank 1)"),
+    "dem4000fill": dict(w=4000, h=4000, members=1, n_exp=1.0, fill=2,
+                        desc="4000x4000 random-noise DEM, Priority-Flood epsilon-filled (1e-8), D8, n=1: "
+                             "the deep-level regime (SURVEY 8(f) rank 1)"),
     "ens64": dict(w=2000, h=2000, members=64, n_exp=1.0,
                   desc="ensemble of 64 x 2000^2 DEMs, seeds 1000+i, K_i=1e-6(1+i%8), m_i=0.35+0.05*floor(i/8) (configs[4])"),
 }
@@ -176,12 +182,13 @@ def cpu_baseline_reference(workload, budget_s=30.0):
     # bounded sample: ~budget_s of CPU work, at least 2 timed steps after 1 warm-up
     est = 3e-8 * w * h * 16 / max(threads, 1)  # ~3 s per 10000^2 step on 16 cores
     n = int(max(2, min(10, budget_s // max(est, 1e-3))))
-    samples, _ = ref.bench(w, h, n, warmup=1, strategy="rb_private_queues", workers=threads, params=p)
+    samples, _ = ref.bench(w, h, n, warmup=1, strategy="rb_private_queues", workers=threads, params=p,
+                           fill=wl.get("fill", 0))
     per_step = float(np.median(samples))
     cells = w * h
     return {"value": cells / per_step, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{len(samples)} lem::strategy_step(rb_private_queues, {threads} threads) timesteps of the "
-                      f"{w}x{h} seed-42 DEM, median wall time {per_step:.3f} s/step (oracle/_ref, -O2 -ffp-contract=off)"}
+                      f"{w}x{h} seed-42 DEM{' (priority_flood_fill first)' if wl.get('fill') else ''}, median wall time {per_step:.3f} s/step (oracle/_ref, -O2 -ffp-contract=off)"}
 
 
 def run_reference_arm(args):
@@ -204,13 +211,14 @@ def run_reference_arm(args):
     # one "step" = one timestep of the whole workload; for the ensemble, a
     # bounded sample (one member) scaled to the member count.
     t0 = time.time()
-    wsecs, _ = ref.bench(w, h, 1, warmup=0, strategy="rb_private_queues", workers=threads, params=p)
+    fill = wl.get("fill", 0)
+    wsecs, _ = ref.bench(w, h, 1, warmup=0, strategy="rb_private_queues", workers=threads, params=p, fill=fill)
     est = float(wsecs[0]) * members
     budget = 180.0
     k = args.steps
     warm = max(0, min(args.warmup - 1, int((budget / 4) // max(est, 1e-3))))
     k_run = int(max(1, min(k, (budget - (time.time() - t0)) // max(est, 1e-3) - warm)))
-    secs, _ = ref.bench(w, h, k_run, warmup=warm, strategy="rb_private_queues", workers=threads, params=p)
+    secs, _ = ref.bench(w, h, k_run, warmup=warm, strategy="rb_private_queues", workers=threads, params=p, fill=fill)
     per_step = float(np.mean(secs)) * members
     value = w * h * members / per_step
     sample = (f"{k_run} timed + {warm + 1} warm-up lem::strategy_step(rb_private_queues, {threads} threads) on "
@@ -266,6 +274,12 @@ def main():
     ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M,
                             per_member=km if (wl["members"] > 1) else None)
     ctx.generate_terrain(seeds)
+    fill_ms = None
+    if wl.get("fill"):  # lem::priority_flood_fill on the device, once, before the timed steps
+        torch.cuda.synchronize(local)
+        tf = time.perf_counter()
+        ctx.fill(mode=wl["fill"], epsilon=1e-8)
+        fill_ms = (time.perf_counter() - tf) * 1e3
     cells = w * h * M
     ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     ens = world > 1 or wl["members"] > 1
@@ -343,7 +357,7 @@ def main():
     k1_ms, tiles_ms = kt["recv_donor"] / n_l, kt["tiles"] / n_l
     esc_ord_ms, esc_phys_ms = kt["order"] / n_l, kt["physics"] / n_l
     # dominant kernel: k_tiles (level order, accumulation, uplift and erosion of
-    # every tree that stays within its tile's halo) after k_recv_donor
+    # every tree that stays within its tile's halo) after k_recv
     # (receivers, donor masks, code bit planes); the escape path finishes the rest
     dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_TILES
     achieved = dom_b * cells / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
@@ -354,14 +368,14 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_cell": dom_b,
                 "alg_bytes_note": "SURVEY 8(d): order 9 + accumulation 21 + uplift/erosion 40 = 70 B/cell for "
-                                  "k_tiles (k_recv_donor: receivers 12 + donors 5); k_tiles moves ~18 B/cell",
-                "k_recv_donor": {"alg_bytes_per_cell": B_RECV, "ms": k1_ms,
+                                  "k_tiles (k_recv: receivers 12 + donors 5); k_tiles moves ~18 B/cell",
+                "k_recv": {"alg_bytes_per_cell": B_RECV, "ms": k1_ms,
                                  "achieved": B_RECV * cells / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None,
                                  "frac": (B_RECV * cells / (k1_ms / 1e3) / 1e9 / peak) if k1_ms > 0 else None},
                 "moved_bytes_per_cell_min": B_TILES_MIN,
                 "hbm_frac_of_moved_bytes": (B_TILES_MIN * cells / (dom_ms / 1e3) / 1e9 / peak) if dom_ms > 0 else None,
-                "kernel_ms": {"step(events)": step_ms_ev, "k_recv_donor": k1_ms, "k_tiles": tiles_ms,
-                              "escape:k_esc_l0+k_expand": esc_ord_ms, "escape:k_chunks+deep": esc_phys_ms},
+                "kernel_ms": {"step(events)": step_ms_ev, "k_recv": k1_ms, "k_tiles": tiles_ms,
+                              "escape:levels": esc_ord_ms, "escape:physics": esc_phys_ms},
                 "timing_source": "CUDA events around each step's graph launch on the context stream; "
                                  "per-kernel split from device %globaltimer stamps taken by the kernels",
                 "step": {"alg_bytes_per_cell": B_STEP, "achieved": per_gpu * B_STEP / 1e9,
@@ -374,11 +388,10 @@ def main():
             cpu = cpu_baseline_reference(args.workload)
         except Exception as e:  # report, never fail the bench
             cpu = {"value": None, "error": str(e)}
-    # per step: k_tiles, k_esc_l0, one k_expand per escape level (+1 closing),
-    # k_chunks, k_deep_prep, k_deep_final, k_finalize (+ 2 stats kernels in
-    # ensemble mode); the escape plan is at most as deep as the step's plan
-    nlev_last = diags[-1].nlevels if diags else 0
-    launches = args.steps * (7 + nlev_last) + (2 * args.steps if ens else 0)
+    # per step (one CUDA graph): k_recv, k_tiles, k_esc_small, k_esc_bfs
+    # (cooperative, every escape level inside), k_chunks, k_deep_coop
+    # (cooperative), k_finalize (+ 2 stats kernels in ensemble mode)
+    launches = args.steps * 7 + (2 * args.steps if ens else 0)
     last = diags[-1] if diags else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -394,10 +407,12 @@ def main():
                    "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",
                    "nlevels_last_step": last.nlevels if last else None,
                    "phase_ms_last_step": ({k: round(v * 1e3, 4) for k, v in zip(
-                       ("k_recv_donor", "-", "escape:order", "k_tiles", "-", "escape:accum+uplift+erosion"), last.seconds)
+                       ("k_recv", "-", "escape:order", "k_tiles", "-", "escape:accum+uplift+erosion"), last.seconds)
                        if k != "-"} if last else None),
                    "escaped_trees_last_step": last.escaped_trees if last else None,
-                   "newton_iters_last_step": last.newton_iters if last else None},
+                   "newton_iters_last_step": last.newton_iters if last else None,
+                   **({"fill": "lem::priority_flood_fill epsilon_ascending 1e-8 on the device (lemgpu_fill), once, "
+                               "untimed", "fill_ms": fill_ms} if fill_ms is not None else {})},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,

@@ -124,6 +124,15 @@ int lemgpu_download_elev(lemgpu_ctx* ctx, double* host);
  * seeds[m] for member m (seeds may be NULL -> seed 42 for every member). */
 int lemgpu_generate_terrain(lemgpu_ctx* ctx, const uint64_t* seeds);
 
+/* Priority-Flood depression filling of the device elevation, in place
+ * (every member): lem::priority_flood_fill (proj/src/depressions.cpp:26-68),
+ * bit-identical.  mode: LEMGPU_FILL_OFF (no-op), LEMGPU_FILL_EXACT (raise to
+ * the spill elevation), LEMGPU_FILL_EPSILON (spill + epsilon; epsilon must be
+ * > 0, config.cpp:164-165 -> LEMGPU_ECONFIG).  Replaces the fill that
+ * run_simulation applies to the generated terrain (proj/src/scheduler.cpp:505). */
+enum { LEMGPU_FILL_OFF = 0, LEMGPU_FILL_EXACT = 1, LEMGPU_FILL_EPSILON = 2 };
+int lemgpu_fill(lemgpu_ctx* ctx, int mode, double epsilon);
+
 /* ---- stepping ---------------------------------------------------------- */
 
 /* Run nsteps timesteps with the elevation device-resident, then synchronise.

@@ -344,3 +344,78 @@ int lo_run(double* elev, int w, int h, int connectivity, const lo_params* p, uin
   free(o.A);
   return rc;
 }
+
+/* ---- Priority-Flood fill (src/depressions.cpp:26-68) ----------------------
+ * Min-heap entries (spill elevation, cell); the lower elevation first, ties
+ * by the lower cell index (HeapGreater, depressions.cpp:17-22).  The
+ * perimeter seeds the flood at its own elevation (:38-44); every neighbour
+ * (D8, stencil order, :50-56) not yet visited is raised to the spill
+ * elevation (exact, :58-59) or to spill + eps when at or below it (epsilon
+ * ascending, :60-62) and pushed with its new elevation. */
+typedef struct { double v; uint32_t c; } lo_he;
+
+static int lo_he_less(lo_he a, lo_he b) { return a.v < b.v || (a.v == b.v && a.c < b.c); }
+
+static void lo_heap_push(lo_he* hp, size_t* n, lo_he e) {
+  size_t i = (*n)++;
+  while (i > 0) {
+    const size_t p = (i - 1) / 2;
+    if (!lo_he_less(e, hp[p])) break;
+    hp[i] = hp[p];
+    i = p;
+  }
+  hp[i] = e;
+}
+
+static lo_he lo_heap_pop(lo_he* hp, size_t* n) {
+  const lo_he top = hp[0];
+  const lo_he last = hp[--(*n)];
+  size_t i = 0;
+  for (;;) {
+    size_t c = 2 * i + 1;
+    if (c >= *n) break;
+    if (c + 1 < *n && lo_he_less(hp[c + 1], hp[c])) ++c;
+    if (!lo_he_less(hp[c], last)) break;
+    hp[i] = hp[c];
+    i = c;
+  }
+  if (*n > 0) hp[i] = last;
+  return top;
+}
+
+void lo_fill(const double* elev, int w, int h, int mode, double eps, double* out) {
+  const size_t n = (size_t)w * h;
+  memcpy(out, elev, n * sizeof(double));
+  if (mode == LO_FILL_OFF) return;
+  static const int ox[8] = {-1, 0, 1, -1, 1, -1, 0, 1}, oy[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+  lo_he* hp = (lo_he*)malloc(n * sizeof(lo_he));
+  char* vis = (char*)calloc(n, 1);
+  size_t hn = 0;
+  for (size_t c = 0; c < n; ++c) {
+    const int x = (int)(c % (size_t)w), y = (int)(c / (size_t)w);
+    if (!(x == 0 || y == 0 || x == w - 1 || y == h - 1)) continue;
+    lo_he e = {out[c], (uint32_t)c};
+    lo_heap_push(hp, &hn, e);
+    vis[c] = 1;
+  }
+  while (hn > 0) {
+    const lo_he top = lo_heap_pop(hp, &hn);
+    const int cx = (int)(top.c % (uint32_t)w), cy = (int)(top.c / (uint32_t)w);
+    for (int k = 0; k < 8; ++k) {
+      const int nx = cx + ox[k], ny = cy + oy[k];
+      if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+      const size_t nc = (size_t)ny * w + nx;
+      if (vis[nc]) continue;
+      vis[nc] = 1;
+      if (mode == LO_FILL_EXACT) {
+        if (out[nc] < top.v) out[nc] = top.v;
+      } else if (out[nc] <= top.v) {
+        out[nc] = top.v + eps;
+      }
+      lo_he e = {out[nc], (uint32_t)nc};
+      lo_heap_push(hp, &hn, e);
+    }
+  }
+  free(hp);
+  free(vis);
+}

@@ -93,6 +93,13 @@ int lo_step(double* elev, int w, int h, int connectivity, const lo_params* p,
 int lo_run(double* elev, int w, int h, int connectivity, const lo_params* p, uint32_t steps,
            uint64_t* newton_total, uint32_t* err_cell);
 
+/* Priority-Flood depression filling (src/depressions.cpp:26-68,
+ * include/lem/depressions.hpp:8-27): mode 0 off, 1 exact (raise to the spill
+ * elevation), 2 epsilon ascending (spill + eps).  A binary min-heap over
+ * (elevation, cell index) -- the reference's std::priority_queue order. */
+enum { LO_FILL_OFF = 0, LO_FILL_EXACT = 1, LO_FILL_EPSILON = 2 };
+void lo_fill(const double* elev, int w, int h, int mode, double eps, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 #include <exception>
 #include <string>
 
+#include <lem/depressions.hpp>
 #include <lem/error.hpp>
 #include <lem/scheduler.hpp>
 #include <lem/simulation.hpp>
@@ -156,14 +157,22 @@ int lr_run(int w, int h, int connectivity, const LrParams* p, const char* strate
 // calls of one strategy on a persistent workspace (the run_simulation loop
 // body, scheduler.cpp:490-498).  seconds[i] = wall time of timed step i,
 // including the per-step FlowGraph::resize the phase timers miss.
+// fill_mode: 0 off, 1 exact, 2 epsilon ascending (run_simulation's
+// generate_terrain + priority_flood_fill, scheduler.cpp:503-506)
 int lr_bench(int w, int h, int connectivity, const LrParams* p, const char* strategy,
              std::uint32_t workers, std::uint64_t seed, std::uint32_t warmup, std::uint32_t steps,
-             double* seconds, std::uint64_t* newton) {
+             double* seconds, std::uint64_t* newton, int fill_mode, double fill_eps) {
   return guarded(
       [&] {
         auto kind = lem::strategy_from_string(strategy);
         if (!kind) throw lem::ConfigError(std::string("unknown strategy ") + strategy);
         lem::Raster<double> r = lem::generate_terrain(w, h, seed);
+        if (fill_mode) {
+          lem::FillOptions o;
+          o.mode = fill_mode == 1 ? lem::FillMode::kExact : lem::FillMode::kEpsilonAscending;
+          o.epsilon_increment = fill_eps;
+          r = lem::priority_flood_fill(r, o);
+        }
         const lem::Neighborhood nbh = lem::Neighborhood::make(connectivity, p->dx, p->dy);
         const lem::GridGraph g(w, h, nbh);
         const lem::SimParams sp = to_params(p);
@@ -182,6 +191,20 @@ int lr_bench(int w, int h, int connectivity, const LrParams* p, const char* stra
           }
         }
         if (newton) *newton = it;
+      },
+      nullptr);
+}
+
+// lem::priority_flood_fill (src/depressions.cpp:26-68): mode 0 off, 1 exact, 2 epsilon ascending
+int lr_fill(int w, int h, const double* elev, int mode, double eps, double* out) {
+  return guarded(
+      [&] {
+        lem::Raster<double> r(w, h, std::vector<double>(elev, elev + (std::size_t)w * h));
+        lem::FillOptions o;
+        o.mode = mode == 1 ? lem::FillMode::kExact : mode == 2 ? lem::FillMode::kEpsilonAscending : lem::FillMode::kOff;
+        o.epsilon_increment = eps;
+        const lem::Raster<double> f = lem::priority_flood_fill(r, o);
+        std::memcpy(out, f.storage().data(), sizeof(double) * (std::size_t)w * h);
       },
       nullptr);
 }

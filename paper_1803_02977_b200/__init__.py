@@ -10,6 +10,8 @@ from .lem import (  # noqa: F401
     ConvergenceError,
     DeviceContext,
     Error,
+    FillMode,
+    FillOptions,
     GridGraph,
     Neighborhood,
     NoFlow,
@@ -25,6 +27,7 @@ from .lem import (  # noqa: F401
     StrategyKind,
     StructureError,
     generate_terrain,
+    priority_flood_fill,
     run_simulation,
     strategy_step,
 )

@@ -69,6 +69,7 @@ _SIGS = {
     "lemgpu_upload_elev": (C.c_int, [_P, _P]),
     "lemgpu_download_elev": (C.c_int, [_P, _P]),
     "lemgpu_generate_terrain": (C.c_int, [_P, _P]),
+    "lemgpu_fill": (C.c_int, [_P, C.c_int, C.c_double]),
     "lemgpu_step": (C.c_int, [_P, C.c_uint32, C.POINTER(lemgpu_diag)]),
     "lemgpu_step_async": (C.c_int, [_P, C.c_uint32]),
     "lemgpu_sync": (C.c_int, [_P, C.POINTER(lemgpu_diag), C.c_uint32, C.POINTER(C.c_uint32)]),

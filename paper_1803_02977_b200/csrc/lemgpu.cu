@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <numeric>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +29,7 @@
 #include "k_order.cuh"
 #include "k_physics.cuh"
 #include "k_recv_donor.cuh"
+#include "k_fill.cuh"
 #include "k_tiles.cuh"
 #include "k_util.cuh"
 
@@ -41,6 +43,7 @@ struct lemgpu_ctx {
   std::vector<lemgpu_member> members;
   int scan_grid = 0, chunk_grid = 0, deep_grid = 0, tile_grid = 0;
   int esc_grid = 0;  // CTAs of the level expansion of the escaped trees (a small workload)
+  int deep_coop_grid = 0;  // CTAs of k_deep_coop (kDeepTPB threads, co-resident)
   int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
   // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
   // graph[p] / exec[p] is the step that reads hbuf[p]
@@ -262,7 +265,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   if ((!ctx->use_tiles && (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a))) ||
       (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
       (ctx->use_tiles &&
-       (rc = add_kernel(ctx, g, &prev, fdc, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true))) ||
+       (rc = add_kernel(ctx, g, &prev, fdc, dim3(ctx->deep_coop_grid), dim3(kDeepTPB), kDeepSmemBytes, &a, nullptr,
+                        true))) ||
       (!ctx->use_tiles &&
        ((rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
         (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
@@ -463,6 +467,15 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
   for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
     CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEscSmallSmemBytes));
+  for (const void* f : {(const void*)k_deep_coop<0>, (const void*)k_deep_coop<1>, (const void*)k_deep_coop<2>})
+    CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDeepSmemBytes));
+  {
+    const void* fdc = a.nkind == 1 ? (const void*)k_deep_coop<1> : a.nkind == 2 ? (const void*)k_deep_coop<2>
+                                                                              : (const void*)k_deep_coop<0>;
+    int occd = 0;
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, fdc, kDeepTPB, kDeepSmemBytes));
+    ctx->deep_coop_grid = (occd > 0 ? occd : 1) * nsm;
+  }
   const void* fchunks = a.nkind == 1 ? (const void*)k_chunks<1> : a.nkind == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   CUB(cudaFuncSetAttribute(fchunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmemBytes));
   CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fchunks, kChunkTPB, kChunksSmemBytes));
@@ -530,7 +543,7 @@ int run_levels_eager(lemgpu_ctx* ctx, const StepArgs& a) {
   if (a.tiles) {
     void* dargs[] = {const_cast<StepArgs*>(&a)};
     const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
-    CU(ctx, cudaLaunchCooperativeKernel(fdc, dim3(a.scan_grid), dim3(kTPB), dargs, 0, st));
+    CU(ctx, cudaLaunchCooperativeKernel(fdc, dim3(ctx->deep_coop_grid), dim3(kDeepTPB), dargs, kDeepSmemBytes, st));
     return LEMGPU_OK;
   }
   k_deep_prep<<<ctx->deep_grid, kTPB, 0, st>>>(a);
@@ -646,7 +659,9 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   }
   const uint32_t W = a.W, Ht = a.Htot;
   const uint32_t ntx = (W + kTX - 1) / kTX, nty = (Ht + kTY - 1) / kTY;
-  const uint32_t R = (nty + (uint32_t)ctx->bands - 1) / (uint32_t)ctx->bands;  // tile rows per band
+  // tile rows per band: bands start on k_recv row blocks too
+  constexpr uint32_t kRq = (uint32_t)(kBY / std::gcd(kBY, kTY));  // lcm(kBY, kTY) / kTY
+  const uint32_t R = ((nty + (uint32_t)ctx->bands - 1) / (uint32_t)ctx->bands + kRq - 1) / kRq * kRq;
   const uint32_t nb = (nty + R - 1) / R;
   while (ctx->band_ev.size() < 2 * (size_t)nb + 1) {
     cudaEvent_t e;
@@ -693,7 +708,6 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     CU(ctx, cudaLaunchKernel(recv_fn(a), g, dim3(kTPB), rargs, 0, st));
     return LEMGPU_OK;
   };
-  static_assert(kBY == kTY, "bands of whole tile rows are whole k_recv row blocks");
   int rc = recv(0);
   if (rc) return rc;
   for (uint32_t b = 0; b < nb; ++b) {
@@ -888,6 +902,58 @@ int lemgpu_download_elev(lemgpu_ctx* ctx, double* host) {
   CU(ctx, cudaMemcpyAsync(host, ctx->hbuf[ctx->cur], (size_t)ctx->a.N * sizeof(double), cudaMemcpyDeviceToHost,
                           ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return LEMGPU_OK;
+}
+
+int lemgpu_fill(lemgpu_ctx* ctx, int mode, double epsilon) {
+  if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
+  if (mode < LEMGPU_FILL_OFF || mode > LEMGPU_FILL_EPSILON) return fail(ctx, LEMGPU_ECONFIG, "unknown fill mode %d", mode);
+  if (mode == LEMGPU_FILL_EPSILON && !(epsilon > 0.0))  // config.cpp:164-165
+    return fail(ctx, LEMGPU_ECONFIG, "fill_epsilon must be > 0 for epsilon_ascending fill");
+  if (mode == LEMGPU_FILL_OFF) return LEMGPU_OK;
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc0 = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc0) return rc0;
+  }
+  const StepArgs& a = ctx->a;
+  cudaStream_t st = ctx->stream;
+  FillArgs fa{};
+  fa.h = ctx->hbuf[ctx->cur];
+  fa.f = ctx->hbuf[ctx->cur ^ 1u];
+  fa.W = a.W;
+  fa.H = a.H;
+  fa.Htot = a.Htot;
+  fa.ntx = (a.W + kFX - 1) / kFX;
+  fa.nty = (a.Htot + kFY - 1) / kFY;
+  fa.mode = mode;
+  fa.eps = epsilon;
+  const uint32_t nt = fa.ntx * fa.nty;
+  uint32_t* d = nullptr;  // dirty[2][nt], any
+  CU(ctx, cudaMalloc(&d, ((size_t)2 * nt + 1) * sizeof(uint32_t)));
+  k_fill_init<<<2368, kTPB, 0, st>>>(fa.h, fa.f, a.W, a.H, a.Htot);
+  int rc = LEMGPU_OK;
+  for (uint32_t pass = 0;; ++pass) {
+    uint32_t* cur = d + (pass & 1u) * nt;
+    fa.dirty_prev = pass ? d + ((pass + 1) & 1u) * nt : nullptr;
+    fa.dirty_cur = cur;
+    fa.any = d + 2 * nt;
+    cudaMemsetAsync(cur, 0, (size_t)nt * sizeof(uint32_t), st);
+    cudaMemsetAsync(fa.any, 0, sizeof(uint32_t), st);
+    k_fill_pass<<<nt, kTPB, 0, st>>>(fa);
+    uint32_t any = 0;
+    if (cudaMemcpyAsync(&any, fa.any, sizeof any, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = fail(ctx, LEMGPU_ECUDA, "fill: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (!any) break;
+  }
+  cudaFree(d);
+  if (rc) return rc;
+  ctx->cur ^= 1u;
+  ctx->cur_synced = ctx->cur;
+  ctx->have_graph = false;
   return LEMGPU_OK;
 }
 

@@ -298,6 +298,12 @@ class DeviceContext:
             arr = (C.c_uint64 * len(seeds))(*seeds)
         self._check(self._L.lemgpu_generate_terrain(self._h, arr))
 
+    def fill(self, opts: Optional["FillOptions"] = None, mode: Optional[int] = None, epsilon: float = 1e-8):
+        """Priority-Flood fill of the device elevation in place (lemgpu_fill)."""
+        if opts is not None:
+            mode, epsilon = int(opts.mode), opts.epsilon_increment
+        self._check(self._L.lemgpu_fill(self._h, int(mode or 0), float(epsilon)))
+
     def step(self, nsteps: int = 1) -> List[StepDiagnostics]:
         diags = (_abi.lemgpu_diag * max(1, nsteps))()
         self._check(self._L.lemgpu_step(self._h, nsteps, diags))
@@ -426,6 +432,38 @@ def strategy_step(elev: np.ndarray, grid: GridGraph, params: SimParams, setup: S
     return ctx.step_host(elev)
 
 
+class FillMode(enum.IntEnum):
+    """lem::FillMode (depressions.hpp:8-12)."""
+
+    kOff = 0
+    kExact = 1
+    kEpsilonAscending = 2
+
+
+@dataclass
+class FillOptions:
+    """lem::FillOptions (depressions.hpp:14-19)."""
+
+    mode: FillMode = FillMode.kOff
+    epsilon_increment: float = 1e-8
+
+
+def priority_flood_fill(elev: np.ndarray, opts: Optional[FillOptions] = None) -> np.ndarray:
+    """lem::priority_flood_fill (depressions.cpp:26-68), computed on the device
+    (lemgpu_fill: tile relaxation to the flood's fixed point, bit-identical)."""
+    opts = opts or FillOptions()
+    a = np.ascontiguousarray(elev, dtype=np.float64)
+    if opts.mode == FillMode.kOff:
+        return a.copy()
+    ctx = DeviceContext(a.shape[-1], a.shape[-2], SimParams())
+    try:
+        ctx.upload(a)
+        ctx.fill(opts)
+        return ctx.download()
+    finally:
+        ctx.close()
+
+
 @dataclass
 class RunConfig:
     """lem::RunConfig subset that the step consumes (config.hpp:55-76)."""
@@ -438,6 +476,7 @@ class RunConfig:
     params: SimParams = field(default_factory=SimParams)
     connectivity: int = 8
     routing: Routing = Routing.kD8
+    fill: FillOptions = field(default_factory=FillOptions)
 
     def validate(self):
         """RunConfig::validate (config.cpp:155-173), step-relevant part."""
@@ -447,6 +486,8 @@ class RunConfig:
             raise ConfigError("grid exceeds 2^32-1 cells")
         self.params.validate()
         Neighborhood.make(self.connectivity)
+        if self.fill.mode == FillMode.kEpsilonAscending and not self.fill.epsilon_increment > 0.0:
+            raise ConfigError("fill_epsilon must be > 0 for epsilon_ascending fill")
 
 
 @dataclass
@@ -484,8 +525,9 @@ def run_simulation(initial, cfg: Optional[RunConfig] = None,
     _check_strategy(StepSetup(routing=cfg.routing), cfg.strategy)
     ctx = DeviceContext(cfg.width, cfg.height, cfg.params, cfg.connectivity, cfg.strategy.device)
     try:
-        if initial is None:
+        if initial is None:  # generate_terrain + optional depression fill (scheduler.cpp:503-506)
             ctx.generate_terrain([cfg.seed])
+            ctx.fill(cfg.fill)
         else:
             a = np.asarray(initial, dtype=np.float64)
             if a.shape != (cfg.height, cfg.width):

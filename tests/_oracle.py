@@ -73,6 +73,7 @@ class Oracle:
                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
         L.lo_newton.restype = C.c_double
         L.lo_newton.argtypes = [C.c_double] * 5 + [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.lo_fill.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p]
         L.lo_generate_queue.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                         C.c_void_p, C.POINTER(C.c_uint32)]
         L.lo_accumulate.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p]
@@ -94,6 +95,14 @@ class Oracle:
             return cls.get()
         except OSError:
             return None
+
+    def fill(self, elev: np.ndarray, mode: int, eps: float = 1e-8) -> np.ndarray:
+        """Priority-Flood fill (depressions.cpp:26-68); mode 1 exact, 2 epsilon ascending."""
+        h, w = elev.shape
+        e = np.ascontiguousarray(elev, np.float64)
+        out = np.empty_like(e)
+        self.L.lo_fill(e.ctypes.data, w, h, mode, eps, out.ctypes.data)
+        return out
 
     def terrain(self, w, h, seed):
         out = np.empty((h, w), np.float64)
@@ -149,8 +158,9 @@ class RefLib:
             C.POINTER(C.c_uint32), C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.lr_run.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32, C.c_uint32,
                              C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
+        L.lr_fill.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_void_p]
         L.lr_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32, C.c_uint64,
-                               C.c_uint32, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64)]
+                               C.c_uint32, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.c_double]
         self.L = L
 
     @classmethod
@@ -192,16 +202,27 @@ class RefLib:
             raise RuntimeError(self.L.lr_last_error().decode())
         return rc, nt.value, ec.value
 
-    def bench(self, w, h, steps, warmup=0, strategy="rb_private_queues", workers=None, seed=42, conn=8, params=None):
-        """Per-step wall seconds of lem::strategy_step on a persistent workspace."""
+    def bench(self, w, h, steps, warmup=0, strategy="rb_private_queues", workers=None, seed=42, conn=8, params=None,
+              fill=0, fill_eps=1e-8):
+        """Per-step wall seconds of lem::strategy_step on a persistent workspace
+        (fill: 0 off, 1 exact, 2 epsilon -- lem::priority_flood_fill first)."""
         p = params or make_params()
         secs = np.zeros(max(1, steps), np.float64)
         nt = C.c_uint64(0)
         rc = self.L.lr_bench(w, h, conn, C.byref(p), strategy.encode(), workers or self.max_threads(), seed, warmup,
-                             steps, secs.ctypes.data, C.byref(nt))
+                             steps, secs.ctypes.data, C.byref(nt), int(fill), float(fill_eps))
         if rc != 0:
             raise RuntimeError(self.L.lr_last_error().decode())
         return secs[:steps], nt.value
+
+    def fill(self, elev: np.ndarray, mode: int, eps: float = 1e-8) -> np.ndarray:
+        """lem::priority_flood_fill itself."""
+        h, w = elev.shape
+        e = np.ascontiguousarray(elev, np.float64)
+        out = np.empty_like(e)
+        if self.L.lr_fill(w, h, e.ctypes.data, mode, eps, out.ctypes.data) != 0:
+            raise RuntimeError(self.L.lr_last_error().decode())
+        return out
 
     def max_threads(self) -> int:
         return int(self.L.lr_max_threads())

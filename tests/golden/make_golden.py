@@ -7,8 +7,10 @@ writes:
   anchors.json        FNV-1a-64 fingerprints of full-size runs
                       (1000^2 / 10000^2, seed 42, defaults, fill=off)
   small_*.npz         complete step-1 outputs of small rasters (every array)
+  fill_*.npz          lem::priority_flood_fill of small rasters (exact and
+                      epsilon-ascending modes)
 
-Usage:  python tests/golden/make_golden.py [--big] [--big120]
+Usage:  python tests/golden/make_golden.py [--big] [--big120] [--fill-only]
   --big     add the 10000^2 step-1 anchors (~1 min, 6 GB RAM)
   --big120  add the 10000^2 120-step anchor (rb_private_queues, ~10 min)
 """
@@ -62,12 +64,31 @@ def anchors_for(ref: RefLib, n: int, steps: int, strategy: str, workers: int):
     return out
 
 
+FILL = [
+    # w, h, seed, mode (1 exact, 2 epsilon ascending), epsilon
+    (100, 100, 1, 1, 1e-8), (100, 100, 1, 2, 1e-8), (100, 100, 2, 2, 1e-8), (100, 100, 3, 1, 1e-8),
+    (257, 131, 7, 2, 1e-8), (257, 131, 7, 1, 1e-8), (70, 45, 9, 2, 1e-3), (3, 3, 1, 2, 1e-8),
+]
+
+
+def fill_goldens(ref: RefLib):
+    for w, h, seed, mode, eps in FILL:
+        e0 = ref.terrain(w, h, seed)
+        f = ref.fill(e0, mode, eps)
+        name = f"fill_{'exact' if mode == 1 else 'eps'}_{w}x{h}_s{seed}" + ("" if eps == 1e-8 else "_e3")
+        np.savez_compressed(HERE / f"{name}.npz", w=w, h=h, seed=seed, mode=mode, eps=eps, h0=e0, f=f)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--big120", action="store_true")
+    ap.add_argument("--fill-only", action="store_true")
     args = ap.parse_args()
     ref = RefLib.get()
+    fill_goldens(ref)
+    if args.fill_only:
+        return
     path = HERE / "anchors.json"
     anchors = json.loads(path.read_text()) if path.exists() else {}
     anchors["_about"] = ("FNV-1a-64 of raw little-endian arrays from the unmodified reference "

@@ -463,3 +463,55 @@ def test_step_host_pageable_and_failure(oracle):
         assert np.array_equal(pinned.view(np.uint64), e.view(np.uint64))
     finally:
         lem._abi.lib().lemgpu_host_unregister(pinned.ctypes.data)
+
+
+@pytest.mark.parametrize("mode", [1, 2], ids=["exact", "epsilon"])
+def test_fill_matches_oracle(oracle, golden_dir, mode):
+    """lemgpu_fill (tile relaxation to the flood's fixed point) is bit-identical
+    to lem::priority_flood_fill: the reference fixtures, the 20 seeds of
+    acceptance.cpp:228-249, odd and stacked (ensemble) rasters, 1000^2."""
+    for path in sorted(golden_dir.glob("fill_*.npz")):
+        g = np.load(path)
+        if int(g["mode"]) != mode:
+            continue
+        f = lem.priority_flood_fill(g["h0"], lem.FillOptions(lem.FillMode(mode), float(g["eps"])))
+        assert np.array_equal(f.view(np.uint64), g["f"].view(np.uint64)), path.name
+    for seed in range(1, 21):
+        e = oracle.terrain(100, 100, seed)
+        f = lem.priority_flood_fill(e, lem.FillOptions(lem.FillMode(mode)))
+        assert np.array_equal(f.view(np.uint64), oracle.fill(e, mode).view(np.uint64)), seed
+    for w, h, seed in [(1000, 1000, 42), (131, 517, 5), (65, 33, 6)]:
+        e = oracle.terrain(w, h, seed)
+        f = lem.priority_flood_fill(e, lem.FillOptions(lem.FillMode(mode)))
+        assert np.array_equal(f.view(np.uint64), oracle.fill(e, mode).view(np.uint64)), (w, h)
+    # ensemble: every member filled on its own
+    M, w, h = 3, 90, 70
+    ctx = lem.DeviceContext(w, h, sim_params(), 8, members=M)
+    ctx.generate_terrain([11, 12, 13])
+    ctx.fill(mode=mode)
+    out = ctx.download()
+    for m, seed in enumerate([11, 12, 13]):
+        want = oracle.fill(oracle.terrain(w, h, seed), mode)
+        assert np.array_equal(out[m].view(np.uint64), want.view(np.uint64)), m
+
+
+def test_filled_terrain_drains_and_steps(oracle):
+    """After the epsilon fill no interior cell is a pit (acceptance.cpp:235-242),
+    and the deep plan that follows steps bit-identically to the oracle."""
+    cfg = lem.RunConfig(width=200, height=150, seed=3, timesteps=0,
+                        fill=lem.FillOptions(lem.FillMode.kEpsilonAscending))
+    filled = lem.run_simulation(cfg).elevation
+    want = oracle.fill(oracle.terrain(200, 150, 3), 2)
+    assert np.array_equal(filled.view(np.uint64), want.view(np.uint64))
+    ctx = device_ctx(200, 150)
+    ctx.upload(filled)
+    e = filled.copy()
+    for s in range(3):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, want_donor=False)
+        if s == 0:
+            assert d.interior_noflow == 0 and o["interior_noflow"] == 0
+        assert d.nlevels == o["nlevels"] and d.newton_iters == o["newton_iters"]
+        assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), s
+    with pytest.raises(lem.ConfigError):
+        ctx.fill(mode=2, epsilon=0.0)

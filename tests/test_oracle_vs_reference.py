@@ -77,3 +77,26 @@ def test_live_vs_reference(oracle, w, h, seed, conn, kw):
             assert np.array_equal(so[k], sr[k]), k
         assert np.array_equal(e_o.view(np.uint64), e_r.view(np.uint64))
         assert so["newton_iters"] == sr["newton_iters"]
+
+
+def test_fill_golden_fixtures(oracle, golden_dir):
+    """The oracle's Priority-Flood restatement reproduces lem::priority_flood_fill
+    (fixtures from the real reference, both modes, two epsilons)."""
+    cases = sorted(golden_dir.glob("fill_*.npz"))
+    assert len(cases) >= 8
+    for path in cases:
+        g = np.load(path)
+        f = oracle.fill(g["h0"], int(g["mode"]), float(g["eps"]))
+        assert np.array_equal(f.view(np.uint64), g["f"].view(np.uint64)), path.name
+
+
+@pytest.mark.skipif(not RefLib.available(), reason="reference library not built")
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fill_vs_reference_live(oracle, mode):
+    """acceptance.cpp:228-249's 20 seeds at 100^2, plus a larger raster."""
+    ref = RefLib.get()
+    for seed in range(1, 21):
+        e = ref.terrain(100, 100, seed)
+        assert np.array_equal(oracle.fill(e, mode).view(np.uint64), ref.fill(e, mode).view(np.uint64)), seed
+    e = ref.terrain(400, 300, 77)
+    assert np.array_equal(oracle.fill(e, mode).view(np.uint64), ref.fill(e, mode).view(np.uint64))
