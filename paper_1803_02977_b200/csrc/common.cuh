@@ -138,6 +138,7 @@ struct Ctl {
   uint32_t nesc, tile_cells, n0i, tile_nlev;
   uint32_t gbar_count, gbar_gen;  // grid barrier of the cooperative escape-path kernel
   uint32_t esc_small;             // 1: k_esc_small finished the escaped trees this step
+  uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
   uint32_t ntl, nltl;
@@ -198,6 +199,7 @@ struct StepArgs {
   int tiles;          // 1: the step runs k_tiles + the escape path (else the global level path)
   uint32_t by0;       // k_recv: first row block of the launch (banded host steps; else 0)
   uint32_t t_lo, t_hi;  // k_tiles: tile range of the launch (t_hi 0: every tile)
+  int no_narrow;      // testing: escape expansion / deep sweeps without narrow runs
   int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
   Ctl* ctl;
@@ -307,6 +309,22 @@ __device__ __forceinline__ uint32_t donor_mask_at(const StepArgs& a, uint32_t c)
     if (nx >= a.W || ny >= a.Htot) continue;
     if (__ldg(a.rcode + (size_t)ny * a.W + nx) == (uint8_t)(7 - k)) m |= 1u << k;
   }
+  return m;
+}
+
+// donor_mask_at for a cell below level 0: it has a receiver, so it is interior
+// and all 8 neighbours exist -- the 8 code loads go out together, no bounds
+// tests (the global level path's dmask when it is materialised).
+__device__ __forceinline__ uint32_t donor_mask_interior(const StepArgs& a, uint32_t c) {
+  if (a.dmask_valid) return __ldg(a.dmask + c);
+  const uint8_t* r = a.rcode + c;
+  const int W = (int)a.W;
+  uint32_t v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = dir_in(a.conn, k) ? (uint32_t)__ldg(r + dir_ox(k) + dir_oy(k) * W) : 0xFFu;
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m |= (v[k] == (uint32_t)(7 - k) ? 1u : 0u) << k;
   return m;
 }
 

@@ -104,7 +104,7 @@ __device__ __forceinline__ void pdm_and_bins(const StepArgs& a, const uint32_t* 
         } else {
           child = a.order[p];
         }
-        cm[u] = donor_mask_at(a, child);
+        cm[u] = KIDS ? donor_mask_interior(a, child) : donor_mask_at(a, child);
       } else {
         cm[u] = 0u;
       }
@@ -374,13 +374,113 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
   if (last_block_done(ctl) && threadIdx.x == 0) expand_finish(a, l, hi, total, err);
 }
 
+// Narrow levels of the escape expansion (filled DEMs: thousands of levels of
+// a few hundred cells): CTA 0 expands a run of them alone, the frontier in
+// shared memory, block barriers between levels, while the other CTAs wait at
+// one grid barrier for the whole run.  Per level: counts, a block scan, the
+// children (order / ppos / cdir / fc as the grid expansion writes them), their
+// donor masks.  Only past level kChunkMaxLevels (the plan is then deep, so the
+// chunk bounds of the shallow physics are not needed).  Leaves the narrow run
+// when a level is wider than kNX (then its per-segment child counts are
+// rebuilt for the grid) or the plan is complete; the hand-back point goes to
+// ctl->nr_*.
+constexpr uint32_t kNX = 2048;
+constexpr uint32_t kNXPer = kNX / kTPB;
+struct NarrowSmem {
+  uint32_t cell[2][kNX];
+  uint8_t mask[2][kNX];
+  uint32_t scan[kNW + 1];
+};
+
+__device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l, uint32_t lo, uint32_t hi) {
+  Ctl* ctl = a.ctl;
+  const uint32_t tid = threadIdx.x, G = gridDim.x, W = a.W;
+  for (uint32_t i = tid; i < hi - lo; i += kTPB) {
+    ns.cell[0][i] = __ldcg(a.order + lo + i);
+    ns.mask[0][i] = (uint8_t)__ldcg(a.pdm + lo + i);
+  }
+  __syncthreads();
+  uint32_t cur = 0;
+  bool done = false;
+  for (;;) {
+    const uint32_t n = hi - lo;
+    // this thread's parents: a contiguous chunk, so children stay in queue order
+    const uint32_t per = (n + kTPB - 1) / kTPB, i0 = min(tid * per, n), i1 = min(i0 + per, n);
+    uint32_t cnt = 0;
+    for (uint32_t i = i0; i < i1; ++i) cnt += __popc(ns.mask[cur][i]);
+    uint32_t total;
+    uint32_t out = block_excl_scan(cnt, &total, ns.scan);
+    const bool keep = total <= kNX;  // the next frontier fits in shared memory
+    for (uint32_t i = i0; i < i1; ++i) {
+      a.fc[lo + i] = hi + out;
+      uint32_t m = ns.mask[cur][i];
+      const uint32_t c = ns.cell[cur][i];
+      while (m) {
+        const uint32_t k = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t child = (uint32_t)((int)c + dir_off(k, (int)W));
+        a.order[hi + out] = child;
+        a.ppos[hi + out] = lo + i;
+        a.cdir[hi + out] = (uint8_t)k;
+        if (keep) ns.cell[cur ^ 1u][out] = child;
+        ++out;
+      }
+    }
+    __syncthreads();
+    for (uint32_t q = tid; q < total; q += kTPB) {
+      const uint32_t child = keep ? ns.cell[cur ^ 1u][q] : __ldcg(a.order + hi + q);
+      const uint32_t m = donor_mask_interior(a, child);
+      a.pdm[hi + q] = (uint8_t)m;
+      if (keep) ns.mask[cur ^ 1u][q] = (uint8_t)m;
+    }
+    __syncthreads();
+    if (tid == 0) expand_finish(a, l, hi, total, false, true);
+    if (total == 0) {
+      done = true;
+      break;
+    }
+    lo = hi;
+    hi += total;
+    ++l;
+    cur ^= 1u;
+    if (!keep) {
+      // back to the grid: per-segment child counts of level l for G CTAs,
+      // and the next level's count slot cleared
+      uint32_t* bins_in = a.bins + (size_t)(l % 3) * G;
+      uint32_t* bins_nx = a.bins + (size_t)((l + 1) % 3) * G;
+      for (uint32_t i = tid; i < G; i += kTPB) {
+        bins_in[i] = 0;
+        bins_nx[i] = 0;
+      }
+      __syncthreads();
+      const uint32_t S = seg_size(total, G);
+      for (uint32_t p = lo + tid; p < hi; p += kTPB) {
+        const uint32_t v = __popc(__ldcg(a.pdm + p));
+        if (v) atomicAdd(bins_in + (p - lo) / S, v);
+      }
+      break;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ctl->nr_l = l;
+    ctl->nr_lo = lo;
+    ctl->nr_hi = hi;
+    ctl->nr_done = done ? 1u : 0u;
+  }
+}
+
 // The whole level expansion of the escaped trees in ONE cooperative kernel
 // (the tile path's small residual workload): level 0 = the roots listed by
 // k_tiles (their donor masks and the bins of the first expansion), then one
 // expand_level per level separated by
 // grid barriers instead of one graph WHILE iteration (kernel launch) each.
 __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
-  __shared__ ScanSmem sm;
+  __shared__ union {
+    ScanSmem sm;
+    NarrowSmem ns;
+  } u;
+  ScanSmem& sm = u.sm;
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->esc_small)) return;  // k_esc_small finished the escaped trees (uniform)
   const uint32_t G = gridDim.x, b = blockIdx.x;
@@ -403,13 +503,23 @@ __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
   // every CTA derives the next level's bounds itself (the size of level l+1
   // is the sum of the bins every CTA reads), so one barrier per level suffices
   uint32_t lo = 0, hi = n;
-  for (uint32_t l = 0;; ++l) {
+  for (uint32_t l = 0;;) {
+    if (!err && !a.no_narrow && l >= (uint32_t)kChunkMaxLevels && hi - lo <= kNX) {
+      if (b == 0) expand_narrow_run(a, u.ns, l, lo, hi);
+      grid_barrier(ctl);
+      if (ld_volatile_u32(&ctl->nr_done)) break;
+      l = ld_volatile_u32(&ctl->nr_l);
+      lo = ld_volatile_u32(&ctl->nr_lo);
+      hi = ld_volatile_u32(&ctl->nr_hi);
+      continue;
+    }
     const uint32_t total = expand_level<true>(a, sm, l, lo, hi, err);
     grid_barrier(ctl);
     if (b == 0 && threadIdx.x == 0) expand_finish(a, l, hi, total, err, true);
     if (total == 0) break;
     lo = hi;
     hi += total;
+    ++l;
   }
 }
 

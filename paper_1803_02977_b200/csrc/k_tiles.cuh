@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
     for (uint32_t b0 = ls; b0 < le; b0 += kTPB) {
       const uint32_t i = b0 + tid;
       uint32_t m = 0;
-      if (i < le) m = donor_mask_at(a, s.cell[i]);
+      if (i < le) m = nl > 1 ? donor_mask_interior(a, s.cell[i]) : donor_mask_at(a, s.cell[i]);
       uint32_t tot;
       const uint32_t ex = block_excl_scan((uint32_t)__popc(m), &tot, s.scan);
       if (carry + tot > (uint32_t)kEscSmallCap) {

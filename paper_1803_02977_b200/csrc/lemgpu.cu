@@ -464,6 +464,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     ctx->bands = (int)std::min<uint64_t>(32, nbands < 4 ? 1 : nbands);
   }
   if (a.force_deep) ctx->esc_small = false;  // testing the deep sweeps of the escape path
+  a.no_narrow = std::getenv("LEMGPU_NO_NARROW") ? 1 : 0;  // testing: grid-wide sweeps for every level
   if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
   for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
     CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEscSmallSmemBytes));

@@ -372,11 +372,16 @@ def test_failed_step_leaves_elevation_unchanged(oracle):
     assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
 
 
-def test_deep_plan_1000(oracle):
+@pytest.mark.parametrize("narrow", [True, False], ids=["narrow-runs", "grid-only"])
+def test_deep_plan_1000(oracle, monkeypatch, narrow):
     """A 1000^2 tilted plane: ~1000 levels, every tree escapes its tile, the
-    escape path runs its cooperative level expansion and deep sweeps."""
+    escape path runs its cooperative level expansion and deep sweeps (runs of
+    narrow levels on one CTA, or -- LEMGPU_NO_NARROW -- every level grid-wide)."""
     e = _ramp(1000, 1000, 5)
+    if not narrow:
+        monkeypatch.setenv("LEMGPU_NO_NARROW", "1")
     ctx = device_ctx(1000, 1000)
+    monkeypatch.delenv("LEMGPU_NO_NARROW", raising=False)
     ctx.upload(e)
     for s in range(2):
         d = ctx.step(1)[0]
