@@ -157,6 +157,37 @@ RunResult run_simulation_rb_gpu(Raster<double> initial, const RunConfig& cfg, co
   return res;
 }
 
+namespace {
+int fill_mode(const FillOptions& o) {
+  return o.mode == FillMode::kExact ? LEMGPU_FILL_EXACT
+         : o.mode == FillMode::kEpsilonAscending ? LEMGPU_FILL_EPSILON
+                                                 : LEMGPU_FILL_OFF;
+}
+}  // namespace
+
+Raster<double> priority_flood_fill_rb_gpu(const Raster<double>& elev, const FillOptions& opts, int device) {
+  Raster<double> out = elev;
+  if (opts.mode == FillMode::kOff) return out;
+  auto c = make_ctx(elev.width(), elev.height(), 8, SimParams{}, device);
+  check(c->h, lemgpu_upload_elev(c->h, elev.storage().data()));
+  check(c->h, lemgpu_fill(c->h, fill_mode(opts), opts.epsilon_increment));
+  check(c->h, lemgpu_download_elev(c->h, out.storage().data()));
+  return out;
+}
+
+RunResult run_simulation_rb_gpu(const RunConfig& cfg, const StepCallback& on_step, int device) {
+  cfg.validate();
+  Raster<double> terrain(static_cast<int>(cfg.width), static_cast<int>(cfg.height));
+  {
+    auto c = make_ctx(terrain.width(), terrain.height(), cfg.connectivity, cfg.params, device);
+    const std::uint64_t seed = cfg.seed;
+    check(c->h, lemgpu_generate_terrain(c->h, &seed));
+    check(c->h, lemgpu_fill(c->h, fill_mode(cfg.fill), cfg.fill.epsilon_increment));
+    check(c->h, lemgpu_download_elev(c->h, terrain.storage().data()));
+  }
+  return run_simulation_rb_gpu(std::move(terrain), cfg, on_step, device);
+}
+
 void fill_workspace(SimWorkspace& ws) {
   Ctx* c = nullptr;
   {

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <lem/config.hpp>
+#include <lem/depressions.hpp>
 #include <lem/raster.hpp>
 #include <lem/scheduler.hpp>
 #include <lem/simulation.hpp>
@@ -30,6 +31,15 @@ StepDiagnostics strategy_step_rb_gpu(Raster<double>& elev, const GridGraph& grid
 // on_step is set (the callback needs the raster), and once at the end.
 RunResult run_simulation_rb_gpu(Raster<double> initial, const RunConfig& cfg,
                                 const StepCallback& on_step = {}, int device = 0);
+
+// lem::run_simulation(const RunConfig&, ...) (scheduler.hpp:64-65,
+// scheduler.cpp:503-506) with strategy rb_gpu: generate_terrain(cfg.seed) and
+// the optional depression fill (cfg.fill) on the device, then the run.
+RunResult run_simulation_rb_gpu(const RunConfig& cfg, const StepCallback& on_step = {}, int device = 0);
+
+// lem::priority_flood_fill (depressions.hpp:21-27) on the device (lemgpu_fill),
+// bit-identical in both modes.
+Raster<double> priority_flood_fill_rb_gpu(const Raster<double>& elev, const FillOptions& opts, int device = 0);
 
 // Copy the last step's flow graph, plan and accumulation into ws.fg / ws.plan /
 // ws.accum in the reference layouts (for parity checks and inspection).

@@ -165,6 +165,25 @@ int main() {
     CHECK(want == got, "callback rasters differ");
     std::printf("%s on_step callbacks\n", want == got ? "ok  " : "FAIL");
   }
+  // 5. Priority-Flood fill and the filled-DEM run (scheduler.cpp:503-506)
+  for (FillMode m : {FillMode::kExact, FillMode::kEpsilonAscending}) {
+    const Raster<double> t = generate_terrain(300, 200, 5);
+    FillOptions o;
+    o.mode = m;
+    auto diff = first_difference(priority_flood_fill(t, o), gpu::priority_flood_fill_rb_gpu(t, o));
+    CHECK(!diff, "fill mode %d differs at cell %u", (int)m, diff ? *diff : 0u);
+    std::printf("%s priority_flood_fill mode %d (300x200)\n", diff ? "FAIL" : "ok  ", (int)m);
+  }
+  {
+    RunConfig c = cfg_of(200, 150, 3, 10);
+    c.fill.mode = FillMode::kEpsilonAscending;
+    RunResult want = run_simulation(c);
+    RunResult got = gpu::run_simulation_rb_gpu(c);
+    auto diff = first_difference(want.elevation, got.elevation);
+    CHECK(!diff, "filled run differs at cell %u", diff ? *diff : 0u);
+    CHECK(want.newton_iters == got.newton_iters, "filled run newton");
+    std::printf("%s run_simulation(cfg) with epsilon fill (200x150, 10 steps)\n", diff ? "FAIL" : "ok  ");
+  }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail ? 1 : 0;
 }

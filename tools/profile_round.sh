@@ -12,4 +12,6 @@ LEMGPU_EAGER=1 timeout -s KILL 300 ncu --metrics gpu__time_duration.sum,dram__by
   python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/launches_$TAG.log 2>&1
 LEMGPU_EAGER=1 timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:k_tiles -s 1 -c 1 \
   -o $OUT/ncu_full_$TAG python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
+LEMGPU_EAGER=1 timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:k_recv -s 1 -c 1 \
+  -o $OUT/ncu_recv_$TAG python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $OUT/ncu_recv_$TAG.log 2>&1
 ls -la $OUT | tail -8
