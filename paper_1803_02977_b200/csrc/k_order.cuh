@@ -385,10 +385,12 @@ __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
 // rebuilt for the grid) or the plan is complete; the hand-back point goes to
 // ctl->nr_*.
 constexpr uint32_t kNX = 2048;
-constexpr uint32_t kNXPer = kNX / kTPB;
 struct NarrowSmem {
-  uint32_t cell[2][kNX];
-  uint8_t mask[2][kNX];
+  uint32_t cell[2][kNX];  // frontier / next frontier cells
+  uint8_t mask[2][kNX];   // their donor masks
+  uint16_t par[kNX];      // next frontier: parent index in the frontier
+  uint16_t fco[kNX];      // frontier: offset of its first child in the next frontier
+  uint8_t dir[kNX];       // next frontier: direction parent -> child
   uint32_t scan[kNW + 1];
 };
 
@@ -410,28 +412,67 @@ __device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l,
     for (uint32_t i = i0; i < i1; ++i) cnt += __popc(ns.mask[cur][i]);
     uint32_t total;
     uint32_t out = block_excl_scan(cnt, &total, ns.scan);
-    const bool keep = total <= kNX;  // the next frontier fits in shared memory
-    for (uint32_t i = i0; i < i1; ++i) {
-      a.fc[lo + i] = hi + out;
-      uint32_t m = ns.mask[cur][i];
-      const uint32_t c = ns.cell[cur][i];
-      while (m) {
-        const uint32_t k = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t child = (uint32_t)((int)c + dir_off(k, (int)W));
-        a.order[hi + out] = child;
-        a.ppos[hi + out] = lo + i;
-        a.cdir[hi + out] = (uint8_t)k;
-        if (keep) ns.cell[cur ^ 1u][out] = child;
-        ++out;
+    if (total > kNX) {
+      // the next frontier does not fit: written straight to the queue, and
+      // the run ends after this level
+      for (uint32_t i = i0; i < i1; ++i) {
+        a.fc[lo + i] = hi + out;
+        uint32_t m = ns.mask[cur][i];
+        const uint32_t c = ns.cell[cur][i];
+        while (m) {
+          const uint32_t k = __ffs(m) - 1;
+          m &= m - 1;
+          a.order[hi + out] = (uint32_t)((int)c + dir_off(k, (int)W));
+          a.ppos[hi + out] = lo + i;
+          a.cdir[hi + out] = (uint8_t)k;
+          ++out;
+        }
       }
-    }
-    __syncthreads();
-    for (uint32_t q = tid; q < total; q += kTPB) {
-      const uint32_t child = keep ? ns.cell[cur ^ 1u][q] : __ldcg(a.order + hi + q);
-      const uint32_t m = donor_mask_interior(a, child);
-      a.pdm[hi + q] = (uint8_t)m;
-      if (keep) ns.mask[cur ^ 1u][q] = (uint8_t)m;
+      __syncthreads();
+      for (uint32_t q = tid; q < total; q += kTPB) a.pdm[hi + q] = (uint8_t)donor_mask_interior(a, __ldcg(a.order + hi + q));
+    } else {
+      // children into shared memory only; the queue entries go out coalesced
+      // below, overlapping the donor-mask loads
+      for (uint32_t i = i0; i < i1; ++i) {
+        ns.fco[i] = (uint16_t)out;
+        uint32_t m = ns.mask[cur][i];
+        const uint32_t c = ns.cell[cur][i];
+        while (m) {
+          const uint32_t k = __ffs(m) - 1;
+          m &= m - 1;
+          ns.cell[cur ^ 1u][out] = (uint32_t)((int)c + dir_off(k, (int)W));
+          ns.par[out] = (uint16_t)i;
+          ns.dir[out] = (uint8_t)k;
+          ++out;
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += kTPB) a.fc[lo + i] = hi + ns.fco[i];
+      // donor masks of the children: 4 per thread in flight at once
+      for (uint32_t q0 = tid; q0 < total; q0 += 4 * kTPB) {
+        uint32_t ch[4], mk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ch[u] = q0 + u * kTPB < total ? ns.cell[cur ^ 1u][q0 + u * kTPB] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = q0 + u * kTPB;
+          if (q < total) {
+            a.order[hi + q] = ch[u];
+            a.ppos[hi + q] = lo + ns.par[q];
+            a.cdir[hi + q] = ns.dir[q];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mk[u] = q0 + u * kTPB < total ? donor_mask_interior(a, ch[u]) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = q0 + u * kTPB;
+          if (q < total) {
+            a.pdm[hi + q] = (uint8_t)mk[u];
+            ns.mask[cur ^ 1u][q] = (uint8_t)mk[u];
+          }
+        }
+      }
     }
     __syncthreads();
     if (tid == 0) expand_finish(a, l, hi, total, false, true);
@@ -443,7 +484,7 @@ __device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l,
     hi += total;
     ++l;
     cur ^= 1u;
-    if (!keep) {
+    if (total > kNX) {
       // back to the grid: per-segment child counts of level l for G CTAs,
       // and the next level's count slot cleared
       uint32_t* bins_in = a.bins + (size_t)(l % 3) * G;
