@@ -394,7 +394,7 @@ struct NarrowSmem {
   uint32_t scan[kNW + 1];
 };
 
-__device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l, uint32_t lo, uint32_t hi) {
+__device__ __forceinline__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l, uint32_t lo, uint32_t hi) {
   Ctl* ctl = a.ctl;
   const uint32_t tid = threadIdx.x, G = gridDim.x, W = a.W;
   for (uint32_t i = tid; i < hi - lo; i += kTPB) {
@@ -454,6 +454,8 @@ __device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l,
 #pragma unroll
         for (int u = 0; u < 4; ++u) ch[u] = q0 + u * kTPB < total ? ns.cell[cur ^ 1u][q0 + u * kTPB] : 0u;
 #pragma unroll
+        for (int u = 0; u < 4; ++u) mk[u] = q0 + u * kTPB < total ? donor_mask_interior(a, ch[u]) : 0u;
+#pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t q = q0 + u * kTPB;
           if (q < total) {
@@ -462,8 +464,6 @@ __device__ void expand_narrow_run(const StepArgs& a, NarrowSmem& ns, uint32_t l,
             a.cdir[hi + q] = ns.dir[q];
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) mk[u] = q0 + u * kTPB < total ? donor_mask_interior(a, ch[u]) : 0u;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t q = q0 + u * kTPB;
