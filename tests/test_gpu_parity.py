@@ -520,3 +520,24 @@ def test_filled_terrain_drains_and_steps(oracle):
         assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), s
     with pytest.raises(lem.ConfigError):
         ctx.fill(mode=2, epsilon=0.0)
+
+
+def test_step_host_banded_ensemble(oracle, monkeypatch):
+    """The banded host step on a stacked ensemble (bands cut across member
+    boundaries): every member equals its own oracle run."""
+    M, w, h = 3, 96, 70
+    monkeypatch.setenv("LEMGPU_HOST_BANDS", "5")
+    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M)
+    monkeypatch.delenv("LEMGPU_HOST_BANDS")
+    seeds = [21, 22, 23]
+    host = np.stack([oracle.terrain(w, h, s) for s in seeds])
+    want = [host[m].copy() for m in range(M)]
+    assert _host_register(host)
+    try:
+        for s in range(3):
+            ctx.step_host(host)
+            for m in range(M):
+                oracle.step(want[m], want_donor=False)
+                assert np.array_equal(host[m].view(np.uint64), want[m].view(np.uint64)), (s, m)
+    finally:
+        lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
