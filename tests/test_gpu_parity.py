@@ -541,3 +541,42 @@ def test_step_host_banded_ensemble(oracle, monkeypatch):
                 assert np.array_equal(host[m].view(np.uint64), want[m].view(np.uint64)), (s, m)
     finally:
         lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_configurations(oracle, monkeypatch, seed):
+    """Randomised shapes (3..260 x 3..200, odd and even widths), D4/D8, n = 1/2,
+    spacings, ensembles of 1-3 members and schedule knobs: every step of every
+    member against the oracle (bit-exact for n = 1, 1e-9 relative for n = 2)."""
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(10):
+        w, h = int(rng.integers(3, 261)), int(rng.integers(3, 201))
+        conn = int(rng.choice([4, 8]))
+        n_exp = float(rng.choice([1.0, 1.0, 2.0]))
+        dx = float(rng.choice([1.0, 1.0, 0.5, 2.0]))
+        M = int(rng.integers(1, 4))
+        env = [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_TILE_GRID": "3"},
+               {"LEMGPU_NO_TMA": "1"}, {"LEMGPU_ESC_SMALL": "0", "LEMGPU_FORCE_ESCAPE": "1"}][int(rng.integers(0, 6))]
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        kw = {"n_exp": n_exp, "dx": dx}
+        ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=M)
+        for k in env:
+            monkeypatch.delenv(k)
+        seeds = [int(x) for x in rng.integers(1, 10**6, size=M)]
+        ctx.generate_terrain(seeds)
+        es = [oracle.terrain(w, h, s) for s in seeds]
+        p = make_params(**kw)
+        tag = f"case {case}: {w}x{h} conn={conn} n={n_exp} dx={dx} M={M} env={env}"
+        for s in range(2):
+            ctx.step(1)
+            g = ctx.download().reshape(M, h, w)
+            for m in range(M):
+                oracle.step(es[m], conn=conn, params=p, want_donor=False)
+                if n_exp == 1.0:
+                    assert np.array_equal(g[m].view(np.uint64), es[m].view(np.uint64)), f"{tag} step {s} member {m}"
+                else:
+                    rel = np.abs(g[m] - es[m]) / np.maximum(np.abs(es[m]), 1e-300)
+                    assert rel.max() <= 1e-9, f"{tag} step {s} member {m}: {rel.max()}"
+                    es[m][...] = g[m]
+        ctx.close()
