@@ -1,9 +1,11 @@
-// k_recv_donor.cuh -- receivers (phase 1) + donors (phase 2) in one stencil pass.
+// k_recv_donor.cuh -- the receiver passes: k_recv (tile path: receiver codes +
+// their bit planes) and k_recv_donor (global path / export: receiver codes +
+// donor masks, one stencil pass).
 //
 //   steepest_receiver  proj/include/lem/flow_graph.hpp:44-59
 //   donors_of          proj/include/lem/flow_graph.hpp:64-72
 //
-// One CTA owns a kBY x kBX tile.  h is staged in shared memory with a 2-cell
+// k_recv_donor: one CTA owns a kBY x kBX tile.  h is staged in shared memory with a 2-cell
 // halo (one coalesced HBM read of h), receiver codes are computed for the
 // tile plus a 1-cell ring, and the donor bitmask of every tile cell is then
 // a pull over the neighbours' codes (no atomics).  Outputs: rcode (the D8
@@ -172,10 +174,10 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
 #ifndef LEMGPU_RECV_MINB
 #define LEMGPU_RECV_MINB 5  // measured: 5 CTAs/SM (48 regs) beats 4 (64 regs)
 #endif
-// DONORS: also the donor masks of the tile (the global level path reads
-// them), which needs the receiver codes of the ring around it; the tile path
-// derives donors from the codes and skips the ring.
-template <int CONN, bool DONORS>
+// The global level path's receiver pass (LEMGPU_PATH=global and the parity
+// export): receiver codes AND the donor masks of the tile, which needs the
+// receiver codes of the ring around it.  (The tile path's pass is k_recv below.)
+template <int CONN>
 __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
   __shared__ __align__(4) uint8_t rc[kBY + 2][kBX + 4];
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
   // shared loads per cell); the two ring columns are done separately.
   {
     const int c = 1 + (tid & (kBX - 1));
-    const int ra = DONORS ? 0 : 1, rz = DONORS ? kBY + 2 : kBY + 1;  // receiver-code rows [ra, rz)
+    const int ra = 0, rz = kBY + 2;  // receiver-code rows [ra, rz): the tile and its ring
     const int rbeg = (tid < kBX) ? ra : (ra + rz) / 2;
     const int rend = (tid < kBX) ? (ra + rz) / 2 : rz;
     const int gx = (int)x0 - 1 + c;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
       }
     }
   }
-  if (DONORS && tid < 2 * (kBY + 2)) {  // ring columns c = 0 and c = kBX+1
+  if (tid < 2 * (kBY + 2)) {  // ring columns c = 0 and c = kBX+1
     const int r = tid >> 1, c = (tid & 1) ? kBX + 1 : 0;
     const int gx = (int)x0 - 1 + c;
     uint8_t code = kNoFlowCode;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
     lo[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4]);
     hi[1] = *reinterpret_cast<const uint32_t*>(&rc[r + 1][c4 + 4]);
     uint32_t pm = 0;
-    if (DONORS) {  // materialised donor masks (the global level path reads them)
+    {  // materialised donor masks (the global level path reads them)
       lo[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4]);
       hi[0] = *reinterpret_cast<const uint32_t*>(&rc[r][c4 + 4]);
       lo[2] = *reinterpret_cast<const uint32_t*>(&rc[r + 2][c4]);
@@ -320,33 +322,16 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
       }
     }
     const uint32_t pc = __byte_perm(lo[1], hi[1], 0x4321u);
-    // bit planes of the receiver codes (k_tiles' level discovery): bit b of
-    // code (gx, gy) at planes[b][gy][gx / 32]; columns beyond W read as code
-    // 15 (no receiver, no source).  16 ballots per row, 16 lanes store.
-    if (a.planes) {
-      uint32_t mine = 0;
-#pragma unroll
-      for (int wj = 0; wj < kBX / 32; ++wj) {
-        const uint32_t code = x0 + 32 * wj + lane < W ? (uint32_t)rc[r + 1][32 * wj + lane + 1] : 15u;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const uint32_t v = __ballot_sync(0xffffffffu, (code >> b) & 1u);
-          if (lane == (uint32_t)(4 * wj + b)) mine = v;
-        }
-      }
-      const uint32_t j = x0 / 32 + (lane >> 2);
-      if (lane < 16 && j < a.W32) a.planes[((size_t)(lane & 3) * Ht + gy) * a.W32 + j] = mine;
-    }
     const uint32_t gx = x0 + c4;
     const size_t base = (size_t)gy * W + gx;
     if (gx + 3 < W && (W & 3) == 0) {
       *reinterpret_cast<uint32_t*>(a.rcode + base) = pc;
-      if (DONORS) *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
+      *reinterpret_cast<uint32_t*>(a.dmask + base) = pm;
     } else {
       for (int j = 0; j < 4; ++j)
         if (gx + j < W) {
           a.rcode[base + j] = (uint8_t)(pc >> (8 * j));
-          if (DONORS) a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
+          a.dmask[base + j] = (uint8_t)(pm >> (8 * j));
         }
     }
   }

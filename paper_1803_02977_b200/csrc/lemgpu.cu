@@ -241,7 +241,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   const int nk = a.nkind;
   const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
   const void* fk1 = ctx->use_tiles ? recv_fn(a)
-                                   : (a.conn == 8 ? (const void*)k_recv_donor<8, true> : (const void*)k_recv_donor<4, true>);
+                                   : (a.conn == 8 ? (const void*)k_recv_donor<8> : (const void*)k_recv_donor<4>);
   const void* fes = nk == 1 ? (const void*)k_esc_small<1> : nk == 2 ? (const void*)k_esc_small<2> : (const void*)k_esc_small<0>;
   const void* fch = nk == 1 ? (const void*)k_chunks<1> : nk == 2 ? (const void*)k_chunks<2> : (const void*)k_chunks<0>;
   const void* fde = nk == 1 ? (const void*)k_deep_erode<1> : nk == 2 ? (const void*)k_deep_erode<2> : (const void*)k_deep_erode<0>;
@@ -615,9 +615,9 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     if (a.conn == 8)
-      k_recv_donor<8, true><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     else
-      k_recv_donor<4, true><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
+      k_recv_donor<4><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     k_l0_count<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     k_l0_write<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     const int rc = run_levels_eager(ctx, a);
