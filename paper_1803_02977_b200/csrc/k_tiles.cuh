@@ -36,7 +36,7 @@
 //      each cell reading its receiver's already updated elevation; the new
 //      elevations go to hout.
 // A tree with a cell whose donor lies outside the domain (its cells reach
-// more than 3 cells beyond T; ~0.3% of the cells of a random-noise DEM) or
+// more than 3 cells beyond T; 0.3 % of the cells of a fresh random-noise DEM, ~2.5 % after some steps) or
 // deeper than kTMaxLev ESCAPES: none of its cells is written, its root is
 // appended to a list, and the level-synchronous global path (k_order.cuh +
 // k_physics.cuh) finishes it after this kernel.  h is read-only during the
