@@ -17,9 +17,9 @@
 // queue per worker over a slice of the sources; here the private queue
 // belongs to a CTA and the sources are the level-0 cells of a 64x32 tile.
 //
-// k_recv_donor has already written, for every cell, the receiver code, the
-// donor mask and the four bit planes of the code.  A CTA (persistent,
-// looping over tiles) does, for its tile T:
+// k_recv has already written, for every cell, the receiver code and the four
+// bit planes of the code (donor masks are derived from the codes where
+// needed).  A CTA (persistent, looping over tiles) does, for its tile T:
 //   1. one TMA box brings h for the BFS domain (T grown by kHalo cells); the
 //      codes of the domain and the ring around it are loaded, and the code
 //      bit planes are shifted to the window's word grid;
