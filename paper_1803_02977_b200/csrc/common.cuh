@@ -2,19 +2,23 @@
 //
 // One timestep is a CUDA graph of these kernels:
 //
-//   k_recv_donor        receivers + donor bitmask + code bit planes      (k_recv_donor.cuh)
+//   k_recv              receiver codes + code bit planes                  (k_recv_donor.cuh)
 //   k_tiles             level order, accumulation, uplift and erosion of
 //                       every drainage tree rooted in a 64x32 tile whose
 //                       cells stay within 3 cells of it                  (k_tiles.cuh)
-//   then, for the trees that escape their tile (and for the parity export):
-//   k_l0_count/_write   level 0 of the BFS order: stream compaction       (k_order.cuh)
-//   WHILE { k_expand }  one frontier expansion per level                  (k_order.cuh)
+//   then, for the trees that escape their tile:
+//   k_esc_small         a small escape set in one CTA's shared memory      (k_tiles.cuh)
+//   k_esc_bfs           cooperative: every level of the escaped trees      (k_order.cuh)
 //   k_chunks            accumulation + uplift + erosion per source chunk  (k_physics.cuh)
-//   k_deep_*            the same sweeps level by level for deep plans     (k_physics.cuh)
+//   k_deep_coop         cooperative: the same sweeps level by level for
+//                       deep plans                                        (k_physics.cuh)
 //   k_finalize          per-step diagnostics                              (k_physics.cuh)
 //
-// The number of levels is data dependent; it is discovered on the device and
-// drives graph WHILE nodes (cudaGraphSetConditional), so a step is one
+// The global level path (LEMGPU_PATH=global, and the parity export) runs
+// k_recv_donor (receivers + donor masks), k_l0_count/_write (level 0) and
+// WHILE { k_expand } / WHILE { k_deep_* } graph loops instead.  The number of
+// levels is data dependent and discovered on the device (cooperative loops
+// or graph WHILE nodes set with cudaGraphSetConditional), so a step is one
 // cudaGraphLaunch with no host round trip.
 //
 // Arithmetic is FP64 and never contracted: compiled with --fmad=false and
@@ -48,7 +52,7 @@ constexpr uint8_t kNoFlowCode = 8;  // rcode value for kNoFlow
 constexpr int kTX = 64, kTY = LEMGPU_TILE_Y, kHalo = 3;
 constexpr int kTTPB = LEMGPU_TILE_TPB;
 
-// k_recv_donor tile (output cells): halo of 2 for h, 1 for the receiver codes.
+// k_recv / k_recv_donor tile (output cells): halo of 2 for h, 1 for the receiver codes.
 constexpr int kBX = 128;
 constexpr int kBY = 32;
 // scan tiles
@@ -177,7 +181,7 @@ struct StepArgs {
   uint8_t* rcode;
   uint8_t* dmask;
   int dmask_valid;   // dmask holds this step's donor masks (else derived from rcode where needed)
-  uint32_t* planes;  // 4 bit planes of rcode, [plane][row][W32] words (k_recv_donor -> k_tiles)
+  uint32_t* planes;  // 4 bit planes of rcode, [plane][row][W32] words (k_recv -> k_tiles)
   uint32_t W32;      // words per plane row
   uint32_t* order;
   uint32_t* ppos;     // position-major: queue position of the receiver (levels >= 1)
@@ -193,7 +197,7 @@ struct StepArgs {
   uint32_t* bins;     // 3 x scan_grid per-segment child counts (rotating)
   uint32_t scan_grid;  // CTAs of the scan kernels (segments per level)
   int eager;          // 1: no graph; loop conditions go through ctl->cond
-  int use_tma;        // k_recv_donor stages h with one TMA box per tile
+  int use_tma;        // k_recv / k_recv_donor / k_tiles stage h with one TMA box per tile
   int force_deep;     // testing: use the per-level sweeps even for shallow plans
   int force_escape;   // testing: 1 = every tree of k_tiles escapes, 2 = trees of odd root cells escape
   int tiles;          // 1: the step runs k_tiles + the escape path (else the global level path)

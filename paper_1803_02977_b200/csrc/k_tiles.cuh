@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         s.hw[i] = (gx >= 0 && gx < W && gy >= 0 && gy < Ht) ? __ldg(a.h + (size_t)gy * W + gx) : 0.0;
       }
     }
-    // receiver codes of rows kDY0-1 .. kDY1 from k_recv_donor's output
+    // receiver codes of rows kDY0-1 .. kDY1 from k_recv's output
     // (asynchronous 4-byte copies, cp.async); cells outside the raster read as NoFlow
     for (int i = (int)tid; i < kRN / 4; i += kTTPB) {
       const int y = kDY0 - 1 + (4 * i) / kWP, x = (4 * i) % kWP;
