@@ -364,7 +364,9 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     k_recv(const __grid_constant__ StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
   __shared__ __align__(8) uint64_t bar;
-  if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  // an earlier step of the batch failed: nothing to do (checked once the TMA
+  // box has landed -- a CTA must not exit with a bulk copy in flight)
+  const uint32_t failed = ld_volatile_u32(&a.ctl->err_flag);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t x0 = blockIdx.x * kBX, y0 = (blockIdx.y + a.by0) * kBY;
   const uint32_t W = a.W, Ht = a.Htot;
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     const uint32_t gy = y0 + (uint32_t)t0 + (uint32_t)(lane & 15);
     bool ok = gy < Ht;
     if (ok) {
-      const uint32_t yl = gy % a.H;
+      const uint32_t yl = a.M > 1 ? gy % a.H : gy;  // one member: no division
       ok = yl > 0 && yl < a.H - 1;
     }
     rows = __ballot_sync(0xffffffffu, ok) & 0xFFFFu;
@@ -410,6 +412,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
   if (!(gx > 0 && gx < W - 1)) rows = 0;
   __syncthreads();
   if (a.use_tma) mbar_wait(&bar, 0);
+  if (failed) return;
 
   // ---- pass 1
   const double* col = &sh[t0][cx + 1];  // sh row t0, window column 0
@@ -505,8 +508,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     for (int i = 0; i < 16; ++i)
       if (i < nr) store_row(i);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());
+  if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());  // (no barrier: thread 0's end ~ the CTA's)
 }
 
 }  // namespace lemgpu
