@@ -27,7 +27,7 @@ def run(n, steps):
     ctx.close()
     return {"size": n, "ms_per_step": ms, "cell_steps_per_s": n * n / (ms / 1e3), "nlevels": d[-1].nlevels,
             "escaped_trees": d[-1].escaped_trees,
-            "k_tiles_ms": kt["tiles"] / kt["launches"], "k_recv_donor_ms": kt["recv_donor"] / kt["launches"]}
+            "k_tiles_ms": kt["tiles"] / kt["launches"], "k_recv_ms": kt["recv_donor"] / kt["launches"]}
 
 
 sizes = [int(x) for x in sys.argv[1:]] or [500, 1000, 2000, 2500, 4000, 5000, 8000, 10000, 16000, 20000]
