@@ -142,6 +142,8 @@ struct Ctl {
   uint32_t nesc, tile_cells, n0i, tile_nlev;
   uint32_t gbar_count, gbar_gen;  // grid barrier of the cooperative escape-path kernel
   uint32_t esc_small;             // 1: k_esc_small finished the escaped trees this step
+  uint32_t esc_fail, esc_cells, esc_nlev, esc_misses, esc_done;  // k_esc_small's CTAs: overflow count, totals
+  unsigned long long esc_iters;
   uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles

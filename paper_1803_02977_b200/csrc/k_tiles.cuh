@@ -636,26 +636,32 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
 __global__ void __launch_bounds__(kTPB) k_esc_gather(StepArgs a, uint32_t* cells, double* vals, uint32_t* count,
                                                      uint32_t cap) {
   const Ctl* ctl = a.ctl;
-  const uint32_t n = ctl->nesc && !ctl->err_flag ? a.levels[ctl->nlev] : 0u;
+  // k_esc_small: the compact list of its cells in ppos; else the level path's queue
+  const bool small = ctl->esc_small != 0;
+  const uint32_t n = ctl->nesc && !ctl->err_flag ? (small ? ctl->esc_cells : a.levels[ctl->nlev]) : 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
   if (n > cap) return;
   for (uint32_t i = blockIdx.x * kTPB + threadIdx.x; i < n; i += gridDim.x * kTPB) {
-    const uint32_t c = a.order[i];
+    const uint32_t c = small ? a.ppos[i] : a.order[i];
     cells[i] = c;
     vals[i] = a.hout[c];
   }
 }
 
 // ---------------------------------------------------------------------------
-// Few escaped trees (small rasters): one CTA finishes them in shared memory --
-// the same breadth-first levels (donor masks from the receiver codes), the
-// reference's FP accumulation in slot order, uplift and erosion level by
-// level -- instead of the cooperative global path, whose ~10 us per level
-// dominates a small step.  Too many roots, more than kEscSmallCap cells or
-// kEscSmallLev levels: nothing is written and the cooperative path runs.
+// The escaped trees in shared memory: the roots are split evenly over the
+// CTAs (one per SM) and each CTA finishes its share of trees alone -- the
+// same breadth-first levels (donor masks from the receiver codes), the
+// reference's FP accumulation in slot order, uplift and erosion level by level
+// -- with block barriers only, instead of the cooperative global path whose
+// grid barrier per level dominates a small escape set.  A CTA whose share has
+// more than kEscSmallRoots roots, kEscSmallCap cells or kEscSmallLev levels
+// counts a failure; then the cooperative path runs for every escaped tree (the
+// trees already written get the same bits again) and this kernel's counters
+// are dropped.  Otherwise the last CTA marks the escape work done.
 constexpr int kEscSmallRoots = 1024;
 constexpr int kEscSmallCap = 6144;
-constexpr int kEscSmallLev = 256;
+constexpr int kEscSmallLev = 64;  // deeper shares fail early (deep plans belong to the cooperative path)
 struct EscSmallSmem {
   double h[kEscSmallCap];
   double A[kEscSmallCap];
@@ -666,7 +672,7 @@ struct EscSmallSmem {
   uint8_t nk[kEscSmallCap];    // number of children
   uint32_t lvl[kEscSmallLev + 1];
   uint32_t scan[kNW + 1];
-  uint32_t flag;
+  uint32_t base, flag;
 };
 constexpr size_t kEscSmallSmemBytes = sizeof(EscSmallSmem);
 
@@ -675,118 +681,157 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   EscSmallSmem& s = *reinterpret_cast<EscSmallSmem*>(smraw);
   Ctl* ctl = a.ctl;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t n = ld_volatile_u32(&ctl->nesc);
-  if (ld_volatile_u32(&ctl->err_flag) || n > (uint32_t)kEscSmallRoots || n > (uint32_t)kEscSmallCap) return;
-  for (uint32_t i = tid; i < n; i += kTPB) {
-    s.cell[i] = a.order[i];
-    s.par[i] = 0xFFFFu;
-  }
-  if (tid == 0) {
-    s.lvl[0] = 0;
-    s.lvl[1] = n;
-    s.flag = 0;
-  }
-  __syncthreads();
-  // breadth-first levels
-  uint32_t nl = n ? 1u : 0u;
-  bool ok = true;
-  while (nl > 0) {
-    const uint32_t ls = s.lvl[nl - 1], le = s.lvl[nl];
-    uint32_t carry = le;
-    for (uint32_t b0 = ls; b0 < le; b0 += kTPB) {
-      const uint32_t i = b0 + tid;
-      uint32_t m = 0;
-      if (i < le) m = nl > 1 ? donor_mask_interior(a, s.cell[i]) : donor_mask_at(a, s.cell[i]);
-      uint32_t tot;
-      const uint32_t ex = block_excl_scan((uint32_t)__popc(m), &tot, s.scan);
-      if (carry + tot > (uint32_t)kEscSmallCap) {
-        ok = false;  // uniform: tot and carry are block-wide
+  const uint32_t tid = threadIdx.x, G = gridDim.x;
+  const uint32_t n = ld_volatile_u32(&ctl->nesc);  // 0 when an earlier step failed (k_tiles did not run)
+  const uint32_t r0 = (uint32_t)((uint64_t)n * blockIdx.x / G), r1 = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / G);
+  const uint32_t nr = r1 - r0;
+  bool ok = nr <= (uint32_t)kEscSmallRoots;
+  uint32_t nl = 0;
+  if (ok && nr > 0) {
+    for (uint32_t i = tid; i < nr; i += kTPB) {
+      s.cell[i] = a.order[r0 + i];
+      s.par[i] = 0xFFFFu;
+    }
+    if (tid == 0) {
+      s.lvl[0] = 0;
+      s.lvl[1] = nr;
+    }
+    __syncthreads();
+    // breadth-first levels
+    nl = 1;
+    for (;;) {
+      const uint32_t ls = s.lvl[nl - 1], le = s.lvl[nl];
+      uint32_t carry = le;
+      for (uint32_t b0 = ls; b0 < le; b0 += kTPB) {
+        const uint32_t i = b0 + tid;
+        uint32_t m = 0;
+        if (i < le) m = nl > 1 ? donor_mask_interior(a, s.cell[i]) : donor_mask_at(a, s.cell[i]);
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan((uint32_t)__popc(m), &tot, s.scan);
+        if (carry + tot > (uint32_t)kEscSmallCap) {
+          ok = false;  // uniform: tot and carry are block-wide
+          break;
+        }
+        if (i < le) {
+          uint32_t c = carry + ex;
+          s.fc[i] = (uint16_t)c;
+          s.nk[i] = (uint8_t)__popc(m);
+          const uint32_t cell = s.cell[i];
+          while (m) {
+            const uint32_t k = __ffs(m) - 1;
+            m &= m - 1;
+            s.cell[c] = (uint32_t)((int)cell + dir_off(k, (int)a.W));
+            s.par[c] = (uint16_t)i;
+            s.kd[c] = (uint8_t)k;
+            ++c;
+          }
+        }
+        carry += tot;
+      }
+      if (!ok) break;
+      if (tid == 0) s.flag = ld_volatile_u32(&ctl->esc_fail);
+      __syncthreads();
+      if (carry == le) break;  // the next level is empty
+      if (s.flag) {  // another CTA already failed: the cooperative path will run (uniform: read after the barrier)
+        ok = false;
         break;
       }
-      if (i < le) {
-        uint32_t c = carry + ex;
-        s.fc[i] = (uint16_t)c;
-        s.nk[i] = (uint8_t)__popc(m);
-        const uint32_t cell = s.cell[i];
-        while (m) {
-          const uint32_t k = __ffs(m) - 1;
-          m &= m - 1;
-          s.cell[c] = (uint32_t)((int)cell + dir_off(k, (int)a.W));
-          s.par[c] = (uint16_t)i;
-          s.kd[c] = (uint8_t)k;
-          ++c;
-        }
+      if (nl == (uint32_t)kEscSmallLev) {
+        ok = false;
+        break;
       }
-      carry += tot;
+      if (tid == 0) s.lvl[nl + 1] = carry;
+      ++nl;
+      __syncthreads();
     }
-    if (!ok) break;
-    __syncthreads();
-    if (carry == le) break;  // the next level is empty
-    if (nl == (uint32_t)kEscSmallLev) {
-      ok = false;
-      break;
-    }
-    if (tid == 0) s.lvl[nl + 1] = carry;
-    ++nl;
-    __syncthreads();
   }
-  if (!ok) return;  // leave the trees to the cooperative path (nothing written)
-  const unsigned long long t_bfs = globaltimer();
-  // accumulation, deepest level first: A = w + the children's A in slot order
-  for (int l = (int)nl - 1; l >= 0; --l) {
-    for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
-      double A = a.w0;
-      const uint32_t nk = l + 1 < (int)nl ? s.nk[i] : 0u, c0 = s.fc[i];
-      for (uint32_t q = 0; q < nk; ++q) A = __dadd_rn(A, s.A[c0 + q]);
-      s.A[i] = A;
+  if (!ok) {
+    if (tid == 0) atomicAdd(&ctl->esc_fail, 1u);
+  } else if (nr > 0) {
+    // accumulation, deepest level first: A = w + the children's A in slot order
+    for (int l = (int)nl - 1; l >= 0; --l) {
+      for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
+        double A = a.w0;
+        const uint32_t nk = l + 1 < (int)nl ? s.nk[i] : 0u, c0 = s.fc[i];
+        for (uint32_t q = 0; q < nk; ++q) A = __dadd_rn(A, s.A[c0 + q]);
+        s.A[i] = A;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-  }
-  // uplift (level 0: interior sources only), erosion level by level
-  uint32_t iters = 0, misses = 0;
-  for (uint32_t l = 0; l < nl; ++l) {
-    for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
-      const uint32_t c = s.cell[i];
-      double hv = a.h[c];
-      if (l == 0) {
-        if (is_interior(a, c)) hv = __dadd_rn(hv, a.du);
-      } else {
-        const double h0 = __dadd_rn(hv, a.du);
-        const double hn = s.h[s.par[i]];
-        const uint32_t mem = a.M > 1 ? c / a.MN : 0u;
-        const double F = tile_F(a, mem, dir_class(s.kd[i]), s.A[i], misses);  // class symmetric in k <-> 7-k
-        int itn;
-        bool okn;
-        if (NK == 1)
-          hv = newton_n1(h0, hn, F, a.eps, a.maxit, itn, okn);
-        else
-          hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, okn);
-        if (okn) {
-          iters += (uint32_t)itn;
+    // uplift (level 0: interior sources only), erosion level by level
+    uint32_t iters = 0, misses = 0;
+    for (uint32_t l = 0; l < nl; ++l) {
+      for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
+        const uint32_t c = s.cell[i];
+        double hv = a.h[c];
+        if (l == 0) {
+          if (is_interior(a, c)) hv = __dadd_rn(hv, a.du);
         } else {
-          hv = h0;  // as chunk_in_global: the failed cell keeps its uplifted height
-          atomicMin(&ctl->err_cell, c);
-          ctl->err_slot = ctl->slot;
-          atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+          const double h0 = __dadd_rn(hv, a.du);
+          const double hn = s.h[s.par[i]];
+          const uint32_t mem = a.M > 1 ? c / a.MN : 0u;
+          const double F = tile_F(a, mem, dir_class(s.kd[i]), s.A[i], misses);  // class symmetric in k <-> 7-k
+          int itn;
+          bool okn;
+          if (NK == 1)
+            hv = newton_n1(h0, hn, F, a.eps, a.maxit, itn, okn);
+          else
+            hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, okn);
+          if (okn) {
+            iters += (uint32_t)itn;
+          } else {
+            hv = h0;  // as chunk_in_global: the failed cell keeps its uplifted height
+            atomicMin(&ctl->err_cell, c);
+            ctl->err_slot = ctl->slot;
+            atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+          }
         }
+        s.h[i] = hv;
+        a.hout[c] = hv;
       }
-      s.h[i] = hv;
-      a.hout[c] = hv;
+      __syncthreads();
+    }
+    // counters aside (dropped if another CTA fails); this CTA's cells appended
+    // to the compact list of escaped cells (a.ppos, for the host-step patch)
+    for (int o = 16; o; o >>= 1) {
+      iters += __shfl_down_sync(0xffffffffu, iters, o);
+      misses += __shfl_down_sync(0xffffffffu, misses, o);
+    }
+    if ((tid & 31) == 0) {
+      if (iters) atomicAdd(&ctl->esc_iters, (unsigned long long)iters);
+      if (misses) atomicAdd(&ctl->esc_misses, misses);
+    }
+    const uint32_t cells = s.lvl[nl];
+    if (tid == 0) {
+      s.base = atomicAdd(&ctl->esc_cells, cells);
+      atomicMax(&ctl->esc_nlev, nl);
     }
     __syncthreads();
+    for (uint32_t i = tid; i < cells; i += kTPB) a.ppos[s.base + i] = s.cell[i];
   }
-  flush_counters(ctl, iters, misses);
-  for (uint32_t l = tid; l <= nl; l += kTPB) a.levels[l] = s.lvl[l];
-  for (uint32_t i = tid; i < s.lvl[nl]; i += kTPB) a.order[i] = s.cell[i];
+  // the last CTA decides
+  __shared__ uint32_t s_last;
+  __syncthreads();
   if (tid == 0) {
-    ctl->nlev = nl;
-    ctl->n0 = n;
-    ctl->mode = kModeDone;
-    ctl->esc_small = 1;
-    ctl->t_t_end = max(ctl->t_t_end, t_bfs);
-    ctl->t_order_end = t_bfs;
-    ctl->t_phys_end = globaltimer();
+    __threadfence();
+    s_last = atomicAdd(&ctl->esc_done, 1u) == G - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    ctl->esc_done = 0;
+    if (ld_volatile_u32(&ctl->esc_fail) == 0) {
+      ctl->nlev = ld_volatile_u32(&ctl->esc_nlev);
+      ctl->n0 = n;
+      ctl->mode = kModeDone;
+      ctl->esc_small = 1;
+      ctl->newton += *reinterpret_cast<volatile unsigned long long*>(&ctl->esc_iters);
+      ctl->misses += ld_volatile_u32(&ctl->esc_misses);
+      const unsigned long long t = globaltimer();
+      ctl->t_t_end = max(ctl->t_t_end, t);
+      ctl->t_order_end = t;
+      ctl->t_phys_end = t;
+    }
   }
 }
 

@@ -56,6 +56,7 @@ struct lemgpu_ctx {
   CUtensorMap tmap[2]{};  // ... k_tiles box
   uint32_t* d_levels_esc = nullptr;
   bool esc_small = true;  // k_esc_small ahead of the cooperative escape path
+  int esc_small_grid = 1;  // its CTAs (one per SM)
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> band_ev;
@@ -253,7 +254,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
         (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
         (ctx->esc_small &&
-         (rc = add_kernel(ctx, g, &prev, fes, dim3(1), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
+         (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else {
@@ -458,6 +459,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.eager = 0;
   a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
   if (const char* env = std::getenv("LEMGPU_ESC_SMALL")) ctx->esc_small = std::atoi(env) != 0;
+  ctx->esc_small_grid = nsm;
+  if (const char* env = std::getenv("LEMGPU_ESC_SMALL_GRID")) ctx->esc_small_grid = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("LEMGPU_HOST_BANDS")) ctx->bands = std::atoi(env);
   if (ctx->bands <= 0) {  // measured on 10000^2 (tools/e2e_probe.py): 32 bands of 25 MB beat 16 and 64
     const uint64_t nbands = N64 * 8 / (25ull << 20);
@@ -581,11 +584,11 @@ void set_eager_conds(const StepArgs& a, cudaStream_t st) {
 int enqueue_escape_eager(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
   if (ctx->esc_small) {
     if (a.nkind == 1)
-      k_esc_small<1><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+      k_esc_small<1><<<ctx->esc_small_grid, kTPB, kEscSmallSmemBytes, st>>>(a);
     else if (a.nkind == 2)
-      k_esc_small<2><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+      k_esc_small<2><<<ctx->esc_small_grid, kTPB, kEscSmallSmemBytes, st>>>(a);
     else
-      k_esc_small<0><<<1, kTPB, kEscSmallSmemBytes, st>>>(a);
+      k_esc_small<0><<<ctx->esc_small_grid, kTPB, kEscSmallSmemBytes, st>>>(a);
   }
   void* eargs[] = {&a};
   CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
