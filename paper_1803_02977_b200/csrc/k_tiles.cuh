@@ -827,8 +827,9 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
       ctl->esc_small = 1;
       ctl->newton += *reinterpret_cast<volatile unsigned long long*>(&ctl->esc_iters);
       ctl->misses += ld_volatile_u32(&ctl->esc_misses);
+      // the whole kernel is reported as the escape path's ORDER phase
+      // (k_finalize: ORDER = t_order_end - t_t_end, EROSION = t_phys_end - t_order_end)
       const unsigned long long t = globaltimer();
-      ctl->t_t_end = max(ctl->t_t_end, t);
       ctl->t_order_end = t;
       ctl->t_phys_end = t;
     }
