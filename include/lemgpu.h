@@ -181,6 +181,9 @@ uint32_t lemgpu_abi_version(void);
 uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx);     /* members * width * height */
 void* lemgpu_stream(lemgpu_ctx* ctx);                 /* the context's cudaStream_t */
 int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
+/* Kernel launches of one step's CUDA graph (the pipelined tile path runs the
+ * receiver pass and k_tiles in bands). */
+uint32_t lemgpu_kernels_per_step(const lemgpu_ctx* ctx);
 
 /* Device time accumulated over the steps synced since timing was enabled:
  * ms[0] = whole step (CUDA events around each graph launch on the context

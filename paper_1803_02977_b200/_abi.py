@@ -81,6 +81,7 @@ _SIGS = {
     "lemgpu_num_cells": (C.c_uint64, [_P]),
     "lemgpu_stream": (_P, [_P]),
     "lemgpu_device_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "lemgpu_kernels_per_step": (C.c_uint32, [_P]),
     "lemgpu_kernel_timing": (C.c_int, [_P, C.c_int]),
     "lemgpu_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
     "lemgpu_debug_timeline": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]),

@@ -57,6 +57,8 @@ struct lemgpu_ctx {
   uint32_t* d_levels_esc = nullptr;
   bool esc_small = true;  // k_esc_small ahead of the cooperative escape path
   int esc_small_grid = 1;  // its CTAs (one per SM)
+  int pipe = 0, pipe_tile_grid = 0;  // pipelined receivers / tiles (bands), k_tiles CTAs per band
+  int pipe_chain = 1;                // receiver bands chained (else independent)
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> band_ev;
@@ -181,6 +183,20 @@ int add_kernel(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, const void
   return 0;
 }
 
+// A kernel node with an explicit dependency list (pipelined tile path).
+int add_kernel_deps(lemgpu_ctx* ctx, cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps, cudaGraphNode_t* out,
+                    const void* fn, dim3 grid, dim3 block, size_t smem, StepArgs* sa, CUtensorMap* map) {
+  cudaKernelNodeParams kp{};
+  void* args[] = {sa, map};
+  kp.func = const_cast<void*>(fn);
+  kp.gridDim = grid;
+  kp.blockDim = block;
+  kp.sharedMemBytes = (unsigned)smem;
+  kp.kernelParams = args;
+  CU(ctx, cudaGraphAddKernelNode(out, g, deps.empty() ? nullptr : deps.data(), deps.size(), &kp));
+  return 0;
+}
+
 int add_while(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, cudaGraphConditionalHandle h,
               const void* fn, dim3 grid, size_t smem, StepArgs* sa) {
   cudaGraphNodeParams cp{};
@@ -249,7 +265,44 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
   cudaGraphNode_t prev = nullptr;
   int rc;
   const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-  if (ctx->use_tiles) {
+  if (ctx->use_tiles && ctx->pipe > 1) {
+    // pipelined: the receiver pass in bands of tile rows (a chain), k_tiles of
+    // band b after the receivers of band b+1; k_tiles limited to 4 CTAs per
+    // SM so the next receiver band's CTAs run beside it
+    const uint32_t W = a.W, Ht = a.Htot, ntx = (W + kTX - 1) / kTX, nty = (Ht + kTY - 1) / kTY;
+    const uint32_t R = (nty + (uint32_t)ctx->pipe - 1) / (uint32_t)ctx->pipe, nb = (nty + R - 1) / R;
+    std::vector<cudaGraphNode_t> rn(nb), tn(nb);
+    for (uint32_t b = 0; b < nb; ++b) {
+      StepArgs ab = a;
+      const uint32_t r0 = b * R, r1 = std::min((b + 1) * R, nty);  // tile rows = k_recv row blocks (kBY == kTY)
+      ab.by0 = r0;
+      std::vector<cudaGraphNode_t> d;
+      if (b && ctx->pipe_chain) d.push_back(rn[b - 1]);
+      if ((rc = add_kernel_deps(ctx, g, d, &rn[b], fk1, dim3(g1.x, r1 - r0), dim3(kTPB), 0, &ab, &ctx->hmap[p])))
+        return rc;
+    }
+    for (uint32_t b = 0; b < nb; ++b) {
+      StepArgs ab = a;
+      ab.t_lo = b * R * ntx;
+      ab.t_hi = std::min((b + 1) * R, nty) * ntx;
+      std::vector<cudaGraphNode_t> d{rn[std::min(b + 1, nb - 1)]};
+      if (!ctx->pipe_chain) {  // the receiver bands are independent: depend on the three this band reads
+        if (b + 1 < nb) d.push_back(rn[b]);
+        if (b >= 1) d.push_back(rn[b - 1]);
+      }
+      const uint32_t grid = std::min<uint32_t>((uint32_t)ctx->pipe_tile_grid, ab.t_hi - ab.t_lo);
+      if ((rc = add_kernel_deps(ctx, g, d, &tn[b], tiles_fn(a), dim3(grid), dim3(kTTPB), tiles_smem(a), &ab,
+                                &ctx->tmap[p])))
+        return rc;
+    }
+    cudaGraphNode_t join;
+    CU(ctx, cudaGraphAddEmptyNode(&join, g, tn.data(), tn.size()));
+    prev = join;
+    if ((ctx->esc_small &&
+         (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
+      return rc;
+  } else if (ctx->use_tiles) {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
         (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
@@ -460,6 +513,14 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
   if (const char* env = std::getenv("LEMGPU_ESC_SMALL")) ctx->esc_small = std::atoi(env) != 0;
   ctx->esc_small_grid = nsm;
+  {  // pipelined receivers / tiles for tall rasters: 24 bands (measured best at 10000^2: 2.127 -> 2.061 ms)
+    const uint32_t nty = (H * M + kTY - 1) / kTY;
+    ctx->pipe = nty >= 128 ? 24 : 0;
+  }
+  if (const char* env = std::getenv("LEMGPU_PIPE")) ctx->pipe = std::atoi(env);
+  ctx->pipe_tile_grid = 4 * nsm;
+  if (const char* env = std::getenv("LEMGPU_PIPE_CHAIN")) ctx->pipe_chain = std::atoi(env);
+  if (const char* env = std::getenv("LEMGPU_PIPE_TILE_GRID")) ctx->pipe_tile_grid = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("LEMGPU_ESC_SMALL_GRID")) ctx->esc_small_grid = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("LEMGPU_HOST_BANDS")) ctx->bands = std::atoi(env);
   if (ctx->bands <= 0) {  // measured on 10000^2 (tools/e2e_probe.py): 32 bands of 25 MB beat 16 and 64
@@ -875,6 +936,20 @@ const char* lemgpu_error_message(const lemgpu_ctx* ctx) {
 uint32_t lemgpu_error_cell(const lemgpu_ctx* ctx) { return ctx ? ctx->err_cell : LEMGPU_NOFLOW; }
 uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx) { return ctx ? ctx->a.N : 0; }
 void* lemgpu_stream(lemgpu_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+uint32_t lemgpu_kernels_per_step(const lemgpu_ctx* ctx) {
+  if (!ctx || !ctx->graph[0]) return 0;
+  size_t n = 0;
+  if (cudaGraphGetNodes(ctx->graph[0], nullptr, &n) != cudaSuccess) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(ctx->graph[0], nodes.data(), &n) != cudaSuccess) return 0;
+  uint32_t k = 0;
+  for (cudaGraphNode_t v : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(v, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes) {
   if (!ctx || !bytes) return LEMGPU_ECONFIG;
   *bytes = ctx->device_bytes;

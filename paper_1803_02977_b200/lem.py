@@ -373,6 +373,9 @@ class DeviceContext:
         t = [buf[i] for i in range(n.value)]
         return [(x - t[0]) * 1e-6 for x in t]
 
+    def kernels_per_step(self) -> int:
+        return int(self._L.lemgpu_kernels_per_step(self._h))
+
     def device_bytes(self) -> int:
         b = C.c_uint64(0)
         self._check(self._L.lemgpu_device_bytes(self._h, C.byref(b)))
