@@ -515,7 +515,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->esc_small_grid = nsm;
   {  // pipelined receivers / tiles for tall rasters: 24 bands (measured best at 10000^2: 2.127 -> 2.061 ms)
     const uint32_t nty = (H * M + kTY - 1) / kTY;
-    ctx->pipe = nty >= 128 ? 24 : 0;
+    ctx->pipe = nty >= 256 ? 24 : 0;  // (5000^2: 157 tile rows, banding costs more than it overlaps)
   }
   if (const char* env = std::getenv("LEMGPU_PIPE")) ctx->pipe = std::atoi(env);
   ctx->pipe_tile_grid = 4 * nsm;
