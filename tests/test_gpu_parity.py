@@ -580,3 +580,31 @@ def test_random_configurations(oracle, monkeypatch, seed):
                     assert rel.max() <= 1e-9, f"{tag} step {s} member {m}: {rel.max()}"
                     es[m][...] = g[m]
         ctx.close()
+
+
+def test_pipelined_graph_tall_rasters(oracle):
+    """Rasters of >= 256 tile rows take the pipelined graph (receiver bands
+    chained, k_tiles of band b after the receivers of band b+1): a tall single
+    raster and a stacked ensemble, every member bit-exact against the oracle."""
+    w, h = 150, 8300  # 260 tile rows
+    ctx = device_ctx(w, h)
+    assert ctx.kernels_per_step() > 7  # banded receivers + tiles
+    e = oracle.terrain(w, h, 51)
+    ctx.upload(e)
+    for s in range(2):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, want_donor=False)
+        assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), s
+        assert d.newton_iters == o["newton_iters"] and d.nlevels == o["nlevels"]
+    M, w, h = 8, 96, 1100  # 275 stacked tile rows
+    ens = lem.DeviceContext(w, h, sim_params(), 8, members=M)
+    assert ens.kernels_per_step() > 7
+    seeds = list(range(60, 60 + M))
+    ens.generate_terrain(seeds)
+    want = [oracle.terrain(w, h, sd) for sd in seeds]
+    for s in range(2):
+        ens.step(1)
+        g = ens.download().reshape(M, h, w)
+        for m in range(M):
+            oracle.step(want[m], want_donor=False)
+            assert np.array_equal(g[m].view(np.uint64), want[m].view(np.uint64)), (s, m)
