@@ -11,7 +11,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Iinclude \
            -Xcompiler -fPIC,-ffp-contract=off,-O2 -shared -cudart static
 
-SRCS := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cuh) include/lemgpu.h
+SRCS := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/lemgpu.h
 
 .PHONY: all lib oracle ptxas clean
 all: lib oracle

@@ -366,7 +366,7 @@ def main():
     dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_TILES
     traffic_tbl, traffic_src = traffic_from_profiles(args.workload)
     traffic = traffic_tbl.get(dom, {}).get("dram_bytes_per_launch") if traffic_tbl else None
-    pipelined = ctx.kernels_per_step() > 7
+    pipelined = ctx.pipeline_bands() > 0
     if pipelined:
         # tall rasters: k_recv and k_tiles run in interleaved bands (one graph,
         # receiver band b+1 beside tile band b), so they are measured as one

@@ -181,9 +181,15 @@ uint32_t lemgpu_abi_version(void);
 uint64_t lemgpu_num_cells(const lemgpu_ctx* ctx);     /* members * width * height */
 void* lemgpu_stream(lemgpu_ctx* ctx);                 /* the context's cudaStream_t */
 int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes);
-/* Kernel launches of one step's CUDA graph (the pipelined tile path runs the
- * receiver pass and k_tiles in bands). */
+/* Kernel nodes of one step's CUDA graph (the pipelined tile path runs the
+ * receiver pass and k_tiles in bands).  Top-level nodes only: the bodies of
+ * the global level path's conditional WHILE nodes (k_expand, k_deep_accum,
+ * k_deep_erode; LEMGPU_PATH=global only) run a data-dependent number of times
+ * and are not counted. */
 uint32_t lemgpu_kernels_per_step(const lemgpu_ctx* ctx);
+/* Bands of the receiver / tile pipeline of the step graph (0: not pipelined;
+ * rasters of >= 256 tile rows are). */
+uint32_t lemgpu_pipeline_bands(const lemgpu_ctx* ctx);
 
 /* Device time accumulated over the steps synced since timing was enabled:
  * ms[0] = whole step (CUDA events around each graph launch on the context
@@ -202,6 +208,17 @@ int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t*
  * scratch array of the last step to host memory.  which: 0 = queue (order),
  * 1 = escape-path level bounds, 2 = control block.  Not used by the step. */
 int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes);
+
+/* Which glibc pow the device reproduces (glibc_pow.cuh): 1 = __pow_fma,
+ * 0 = __pow_sse2 -- the variant the HOST libm's ifunc selected, found at
+ * context creation by probing ::pow -- or -1 when neither restatement matches
+ * the host libm (pow(A,m) beyond the table and n != 1 are then not
+ * bit-identical with the reference on this host).  ctx may be NULL. */
+int lemgpu_pow_variant(const lemgpu_ctx* ctx);
+/* Test hook (no reference counterpart): out[i] = pow(x[i], y[i]) computed by
+ * the device restatement of glibc pow (variant as above) on `device`; host
+ * arrays of n doubles.  Lets the tests compare it with the host libm. */
+int lemgpu_debug_pow(int device, int variant, const double* x, const double* y, double* out, uint64_t n);
 
 /* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */
 int lemgpu_host_register(void* ptr, size_t bytes);

@@ -82,10 +82,13 @@ _SIGS = {
     "lemgpu_stream": (_P, [_P]),
     "lemgpu_device_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "lemgpu_kernels_per_step": (C.c_uint32, [_P]),
+    "lemgpu_pipeline_bands": (C.c_uint32, [_P]),
     "lemgpu_kernel_timing": (C.c_int, [_P, C.c_int]),
     "lemgpu_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
     "lemgpu_debug_timeline": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]),
     "lemgpu_debug_copy": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
+    "lemgpu_pow_variant": (C.c_int, [_P]),
+    "lemgpu_debug_pow": (C.c_int, [C.c_int, C.c_int, _P, _P, _P, C.c_uint64]),
     "lemgpu_host_register": (C.c_int, [_P, C.c_size_t]),
     "lemgpu_host_unregister": (C.c_int, [_P]),
 }

@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "glibc_pow.cuh"
 #include "lemgpu.h"
 
 namespace lemgpu {
@@ -112,6 +113,13 @@ __host__ __device__ constexpr bool dir_in(int conn, int k) {
 #else
 #define LG_FMA(x, y, z) std::fma((x), (y), (z))
 #endif
+// pow(x, y) bit-identical with the host glibc (glibc_pow.cuh).  Out of line:
+// its ~60 FP64 operations and two table lookups stay out of the register
+// budget of the kernels that call it on rare paths.
+__device__ __noinline__ double glibc_pow_dev(int pow_fma, double x, double y) {
+  return pow_fma ? glibc_pow<true>(x, y) : glibc_pow<false>(x, y);
+}
+
 // High 32 bits of a double (sign, exponent, top 20 mantissa bits).
 __host__ __device__ __forceinline__ int hi_word(double x) {
 #ifdef __CUDA_ARCH__
@@ -207,6 +215,7 @@ struct StepArgs {
   uint32_t t_lo, t_hi;  // k_tiles: tile range of the launch (t_hi 0: every tile)
   int no_narrow;      // testing: escape expansion / deep sweeps without narrow runs
   int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
+  int pow_fma;        // the host glibc's pow variant the device reproduces: 1 __pow_fma, 0 __pow_sse2
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)

@@ -118,7 +118,8 @@ constexpr uint32_t kWOffHi = woff_b(4) | woff_b(5) << 8 | woff_b(6) << 16 | woff
 __device__ __forceinline__ int woff(uint32_t k) { return (int)(__byte_perm(kWOffLo, kWOffHi, k) & 0xFFu) - 128; }
 
 // F = ((K*dt) * pow(A, m)) / pow(dist, n) (erosion.cpp:38-39) from the host
-// libm table when A is an exact multiple of the cell area.
+// libm table when A is an exact multiple of the cell area, else with the
+// device restatement of the host glibc pow (identical bits).
 __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32_t cls, double A,
                                          uint32_t& misses) {
   const double q = a.w0_is_one ? A : __ddiv_rn(A, a.w0);
@@ -126,7 +127,7 @@ __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32
     return __ldg(a.ftab + ((size_t)mem * 3 + cls) * a.lut_entries + (uint32_t)q);
   ++misses;
   const double pd = cls == 0 ? a.powdist_h : cls == 1 ? a.powdist_v : a.powdist_d;
-  return __ddiv_rn(__dmul_rn(__ldg(a.kdt + mem), pow(A, __ldg(a.mexp + mem))), pd);
+  return __ddiv_rn(__dmul_rn(__ldg(a.kdt + mem), glibc_pow_dev(a.pow_fma, A, __ldg(a.mexp + mem))), pd);
 }
 
 template <int CONN, int NK, bool EX>
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         if (NK == 1)
           hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
         else
-          hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, ok);
+          hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, a.pow_fma, itn, ok);
       }
       const uint32_t gc = gcell(q);
       if (ok) {
@@ -776,7 +777,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
           if (NK == 1)
             hv = newton_n1(h0, hn, F, a.eps, a.maxit, itn, okn);
           else
-            hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, itn, okn);
+            hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, a.pow_fma, itn, okn);
           if (okn) {
             iters += (uint32_t)itn;
           } else {

@@ -59,6 +59,8 @@ struct lemgpu_ctx {
   int esc_small_grid = 1;  // its CTAs (one per SM)
   int pipe = 0, pipe_tile_grid = 0;  // pipelined receivers / tiles (bands), k_tiles CTAs per band
   int pipe_chain = 1;                // receiver bands chained (else independent)
+  int pow_variant = -1;              // host_pow_variant(): the glibc pow the device reproduces
+  uint32_t pipe_bands = 0;           // bands of the pipelined graph (0: not pipelined)
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> band_ev;
@@ -132,6 +134,56 @@ int validate(const lemgpu_params* p, std::string& why) {
   if (p->connectivity != 4 && p->connectivity != 8)
     return why = "connectivity must be 4 or 8, got " + std::to_string(p->connectivity), 1;
   return 0;
+}
+
+// Which glibc pow the host libm runs (its ifunc picks __pow_fma on CPUs with
+// FMA + AVX2, else __pow_sse2): the restatement (glibc_pow.cuh) that agrees
+// with ::pow on a probe set spanning the regimes the step uses -- drainage
+// areas to m, Newton differences to n and n - 1, random bit patterns.  The
+// two variants disagree on ~0.04 % of such inputs, so 20000 probes separate
+// them.  -1: neither matches (the device pow is then not the host's).
+int host_pow_variant() {
+  static int v = -2;
+  if (v != -2) return v;
+  double (*volatile libm_pow)(double, double) = &::pow;  // no constant folding
+  uint64_t st = 0x243F6A8885A308D3ull;
+  auto nx = [&st]() {
+    uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  auto u01 = [&]() { return (double)(nx() >> 11) * 0x1p-53; };
+  bool fma_ok = true, sse_ok = true;
+  for (int i = 0; i < 20000 && (fma_ok || sse_ok); ++i) {
+    double x, y;
+    switch (i % 4) {
+      case 0: x = (double)(1 + nx() % 8000000); y = 0.25 + 0.6 * u01(); break;
+      case 1: x = std::ldexp(u01() + 0.5, -(int)(nx() % 60)); y = 2.0; break;
+      case 2: x = std::ldexp(u01() + 0.5, -(int)(nx() % 60)); y = -0.9 + 2.8 * u01(); break;
+      default: {
+        uint64_t a = nx(), b = nx();
+        std::memcpy(&x, &a, 8);
+        std::memcpy(&y, &b, 8);
+      }
+    }
+    const double w = libm_pow(x, y);
+    auto same = [&](double g) {
+      uint64_t ga, wa;
+      std::memcpy(&ga, &g, 8);
+      std::memcpy(&wa, &w, 8);
+      return ga == wa || (std::isnan(g) && std::isnan(w));
+    };
+    fma_ok = fma_ok && same(glibc_pow<true>(x, y));
+    sse_ok = sse_ok && same(glibc_pow<false>(x, y));
+  }
+  v = fma_ok ? 1 : sse_ok ? 0 : -1;
+  return v;
+}
+
+__global__ void k_debug_pow(int variant, const double* x, const double* y, double* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = glibc_pow_dev(variant, x[i], y[i]);
 }
 
 // True when every sum of k <= nmax copies of w is exactly k*w, i.e. w's
@@ -270,15 +322,21 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
     // band b after the receivers of band b+1; k_tiles limited to 4 CTAs per
     // SM so the next receiver band's CTAs run beside it
     const uint32_t W = a.W, Ht = a.Htot, ntx = (W + kTX - 1) / kTX, nty = (Ht + kTY - 1) / kTY;
-    const uint32_t R = (nty + (uint32_t)ctx->pipe - 1) / (uint32_t)ctx->pipe, nb = (nty + R - 1) / R;
+    // tile rows per band, a multiple of kRq so every band starts on a k_recv
+    // row block (kBY rows) as well as on a tile row (kTY rows)
+    constexpr uint32_t kRq = (uint32_t)(kBY / std::gcd(kBY, kTY));
+    const uint32_t R = ((nty + (uint32_t)ctx->pipe - 1) / (uint32_t)ctx->pipe + kRq - 1) / kRq * kRq;
+    const uint32_t nb = (nty + R - 1) / R;
+    ctx->pipe_bands = nb;
     std::vector<cudaGraphNode_t> rn(nb), tn(nb);
     for (uint32_t b = 0; b < nb; ++b) {
       StepArgs ab = a;
-      const uint32_t r0 = b * R, r1 = std::min((b + 1) * R, nty);  // tile rows = k_recv row blocks (kBY == kTY)
-      ab.by0 = r0;
+      const uint32_t y0 = b * R * (uint32_t)kTY, y1 = std::min((b + 1) * R * (uint32_t)kTY, Ht);  // raster rows
+      ab.by0 = y0 / (uint32_t)kBY;
+      const uint32_t nby = (y1 - y0 + (uint32_t)kBY - 1) / (uint32_t)kBY;
       std::vector<cudaGraphNode_t> d;
       if (b && ctx->pipe_chain) d.push_back(rn[b - 1]);
-      if ((rc = add_kernel_deps(ctx, g, d, &rn[b], fk1, dim3(g1.x, r1 - r0), dim3(kTPB), 0, &ab, &ctx->hmap[p])))
+      if ((rc = add_kernel_deps(ctx, g, d, &rn[b], fk1, dim3(g1.x, nby), dim3(kTPB), 0, &ab, &ctx->hmap[p])))
         return rc;
     }
     for (uint32_t b = 0; b < nb; ++b) {
@@ -407,6 +465,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.powdist_v = std::pow(a.dist[1], p->n_exp);
   a.powdist_d = std::pow(a.dist[0], p->n_exp);
   a.lut_exact = area_sums_exact(a.w0, (uint64_t)a.MN) ? 1 : 0;
+  ctx->pow_variant = host_pow_variant();
+  a.pow_fma = ctx->pow_variant != 0 ? 1 : 0;
   uint32_t lut_entries = a.MN < 65536u ? a.MN + 1 : 65537u;
   if (const char* env = std::getenv("LEMGPU_LUT_ENTRIES")) lut_entries = (uint32_t)std::strtoul(env, nullptr, 10);
   if (lut_entries < 2) lut_entries = 2;
@@ -950,6 +1010,8 @@ uint32_t lemgpu_kernels_per_step(const lemgpu_ctx* ctx) {
   return k;
 }
 
+uint32_t lemgpu_pipeline_bands(const lemgpu_ctx* ctx) { return ctx ? ctx->pipe_bands : 0; }
+
 int lemgpu_device_bytes(const lemgpu_ctx* ctx, uint64_t* bytes) {
   if (!ctx || !bytes) return LEMGPU_ECONFIG;
   *bytes = ctx->device_bytes;
@@ -1297,6 +1359,26 @@ int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes) {
   const uint64_t cap = which == 0 ? (uint64_t)ctx->a.N * 4 : which == 1 ? ((uint64_t)ctx->a.N + 2) * 4 : sizeof(Ctl);
   CU(ctx, cudaMemcpy(host, src, bytes < cap ? bytes : cap, cudaMemcpyDeviceToHost));
   return LEMGPU_OK;
+}
+
+int lemgpu_pow_variant(const lemgpu_ctx* ctx) { return ctx ? ctx->pow_variant : host_pow_variant(); }
+
+int lemgpu_debug_pow(int device, int variant, const double* x, const double* y, double* out, uint64_t n) {
+  if (!x || !y || !out) return LEMGPU_ECONFIG;
+  if (cudaSetDevice(device) != cudaSuccess) return LEMGPU_ECUDA;
+  double* d = nullptr;
+  if (cudaMalloc(&d, 3 * n * sizeof(double) + 8) != cudaSuccess) return LEMGPU_ECUDA;
+  int rc = LEMGPU_OK;
+  if (cudaMemcpy(d, x, n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(d + n, y, n * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = LEMGPU_ECUDA;
+  if (!rc && n) {
+    k_debug_pow<<<1184, kTPB>>>(variant != 0, d, d + n, d + 2 * n, n);
+    if (cudaGetLastError() != cudaSuccess || cudaMemcpy(out, d + 2 * n, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = LEMGPU_ECUDA;
+  }
+  cudaFree(d);
+  return rc;
 }
 
 int lemgpu_host_register(void* ptr, size_t bytes) {

@@ -376,6 +376,14 @@ class DeviceContext:
     def kernels_per_step(self) -> int:
         return int(self._L.lemgpu_kernels_per_step(self._h))
 
+    def pipeline_bands(self) -> int:
+        """Bands of the receiver / tile pipeline (0: the step graph is not pipelined)."""
+        return int(self._L.lemgpu_pipeline_bands(self._h))
+
+    def pow_variant(self) -> int:
+        """The host glibc pow the device reproduces: 1 __pow_fma, 0 __pow_sse2, -1 none."""
+        return int(self._L.lemgpu_pow_variant(self._h))
+
     def device_bytes(self) -> int:
         b = C.c_uint64(0)
         self._check(self._L.lemgpu_device_bytes(self._h, C.byref(b)))

@@ -1,8 +1,9 @@
 """Parity of the sm_100a path (through the C-ABI) with the pinned CPU oracle.
 
-Bar: rec, dnum, donor slots, order, levels, A bit-exact; h
-bit-exact for n = 1; h within 1e-9 relative for n != 1; newton_iters and
-interior_noflow exact."""
+Bar: rec, dnum, donor slots, order, levels, A bit-exact;
+newton_iters and interior_noflow exact; h bit-exact for every n, every cell
+area and every drainage area: pow is the device restatement of the host glibc
+pow (glibc_pow.cuh), so the stated 1e-9 tolerance for n != 1 is met with 0."""
 import json
 
 import numpy as np
@@ -50,12 +51,8 @@ def test_small_golden(path):
     gr = ctx.download_graph(donor=True)
     for k in ARRAYS:
         assert np.array_equal(gr[k], g[k]), k
-    exact = kw.get("n_exp", 1.0) == 1.0
-    if exact:
-        assert np.array_equal(out.view(np.uint64), g["h1"].view(np.uint64))
-    else:
-        assert np.max(np.abs(out - g["h1"]) / np.abs(g["h1"])) <= 1e-9
-    assert d.newton_iters == int(g["newton_iters"]) or not exact
+    assert np.array_equal(out.view(np.uint64), g["h1"].view(np.uint64))
+    assert d.newton_iters == int(g["newton_iters"])
     assert d.interior_noflow == int(g["interior_noflow"])
     assert d.lut_misses == 0 or "m_exp" in kw or "dx" in kw
 
@@ -221,7 +218,10 @@ def test_member_stats():
     assert (s[:, 1] == hh.max(1)).all() and (s[:, 2] == hh.min(1)).all()
 
 
-def test_n2_tolerance_and_drift(oracle):
+def test_n2_bit_exact_120_steps(oracle):
+    """n = 2 (Newton with pow(diff, 2)): bit-identical to the oracle at every
+    one of 120 steps -- the drift after 120 steps is 0 (north_star asks for it
+    to be reported; tools/drift_n2.py reports it at configs[2]'s 4000^2)."""
     w = h = 200
     p = make_params(n_exp=2.0)
     ctx = device_ctx(w, h, n_exp=2.0)
@@ -230,12 +230,42 @@ def test_n2_tolerance_and_drift(oracle):
     d = ctx.step(1)[0]
     o = oracle.step(e, params=p)
     hg = ctx.download()
-    compare_step(ctx, o, hg, e, exact_h=False, tag="n=2 step 1")
-    assert abs(d.newton_iters - o["newton_iters"]) <= max(10, o["newton_iters"] // 10000)
-    ctx.step(119)
-    oracle.run(e, 119, params=p)
-    rel = np.abs(ctx.download() - e) / np.abs(e)
-    assert rel.max() <= 1e-6  # reported drift after 120 steps; per-step bound is 1e-9
+    compare_step(ctx, o, hg, e, tag="n=2 step 1")
+    assert d.newton_iters == o["newton_iters"]
+    ds = ctx.step(119)
+    rc, newton, _ = oracle.run(e, 119, params=p)
+    assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
+    assert sum(x.newton_iters for x in ds) == newton
+
+
+def test_device_pow_matches_host_libm():
+    """The device restatement of glibc pow == the host libm's ::pow bit for bit
+    on 4e5 inputs (drainage areas^m, Newton differences^2 and ^(n-1), random
+    bit patterns), in the variant the context detected."""
+    import ctypes
+
+    L = lem._abi.lib()
+    variant = L.lemgpu_pow_variant(None)
+    assert variant in (0, 1), "neither glibc pow restatement matches this host's libm"
+    libm = ctypes.CDLL("libm.so.6")
+    libm.pow.restype = ctypes.c_double
+    libm.pow.argtypes = [ctypes.c_double, ctypes.c_double]
+    rng = np.random.default_rng(5)
+    n = 100000
+    xs = [rng.integers(1, 70_000_000, n).astype(np.float64),
+          np.ldexp(0.5 + rng.random(n), -rng.integers(0, 60, n)),
+          np.ldexp(0.5 + rng.random(n), -rng.integers(0, 80, n)),
+          rng.integers(0, 2**63, n, dtype=np.int64).view(np.float64)]
+    ys = [0.25 + 0.6 * rng.random(n), np.full(n, 2.0), -0.9 + 2.8 * rng.random(n),
+          rng.integers(0, 2**63, n, dtype=np.int64).view(np.float64)]
+    x = np.ascontiguousarray(np.concatenate(xs))
+    y = np.ascontiguousarray(np.concatenate(ys))
+    got = np.empty_like(x)
+    assert L.lemgpu_debug_pow(0, variant, x.ctypes.data, y.ctypes.data, got.ctypes.data, x.size) == 0
+    want = np.array([libm.pow(a, b) for a, b in zip(x.tolist(), y.tolist())])
+    same = (got.view(np.uint64) == want.view(np.uint64)) | (np.isnan(got) & np.isnan(want))
+    bad = np.nonzero(~same)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. pow({x[bad[0]]!r}, {y[bad[0]]!r})"
 
 
 def test_convergence_error_surfaces_cell():
@@ -314,7 +344,7 @@ def test_per_level_sweeps_match_chunked(oracle, monkeypatch, w, h, seed, kw):
         hd, hc = deep.download(), chunked.download()
         assert np.array_equal(hd.view(np.uint64), hc.view(np.uint64))
         assert dd.newton_iters == dc.newton_iters
-        compare_step(deep, o, hd, e, exact_h=kw.get("n_exp", 1.0) == 1.0, tag="deep")
+        compare_step(deep, o, hd, e, tag="deep")
 
 
 def _ramp(w, h, seed):
@@ -347,16 +377,12 @@ def test_schedules_agree_with_oracle(oracle, monkeypatch, env, w, h, seed, kw, t
     e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
     ctx.upload(e)
     p = make_params(**kw)
-    exact = kw.get("n_exp", 1.0) == 1.0
     for s in range(4):
         d = ctx.step(1)[0]
         o = oracle.step(e, params=p)
         hg = ctx.download()
-        compare_step(ctx, o, hg, e, exact_h=exact, tag=f"{env} step {s}")
-        if not exact:
-            e[...] = hg  # continue from the same state
-        else:
-            assert d.newton_iters == o["newton_iters"]
+        compare_step(ctx, o, hg, e, tag=f"{env} step {s}")
+        assert d.newton_iters == o["newton_iters"]
         assert d.interior_noflow == o["interior_noflow"]
         assert d.nlevels == o["nlevels"]
 
@@ -396,8 +422,8 @@ def test_deep_plan_1000(oracle, monkeypatch, narrow):
 @pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_PATH": "global"}], ids=["tiles", "half-escape", "global"])
 def test_inexact_cell_area(oracle, monkeypatch, env):
     """dx*dy with a full significand: the drainage area is the reference's FP
-    sum in slot order (bit-exact), pow(A, m) is evaluated on the device (lut
-    misses), so elevations agree within the stated tolerance."""
+    sum in slot order (bit-exact) and pow(A, m) is evaluated on the device by
+    the glibc restatement (lut misses) -- elevations bit-exact."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     kw = {"dx": 0.1, "dy": 0.3}
@@ -411,9 +437,8 @@ def test_inexact_cell_area(oracle, monkeypatch, env):
         d = ctx.step(1)[0]
         o = oracle.step(e, params=p)
         hg = ctx.download()
-        compare_step(ctx, o, hg, e, exact_h=False, tag=f"{env} step {s}")
-        assert d.lut_misses > 0 and abs(d.newton_iters - o["newton_iters"]) <= 2
-        e[...] = hg
+        compare_step(ctx, o, hg, e, tag=f"{env} step {s}")
+        assert d.lut_misses > 0 and d.newton_iters == o["newton_iters"]
 
 
 def _host_register(a):
@@ -547,7 +572,7 @@ def test_step_host_banded_ensemble(oracle, monkeypatch):
 def test_random_configurations(oracle, monkeypatch, seed):
     """Randomised shapes (3..260 x 3..200, odd and even widths), D4/D8, n = 1/2,
     spacings, ensembles of 1-3 members and schedule knobs: every step of every
-    member against the oracle (bit-exact for n = 1, 1e-9 relative for n = 2)."""
+    member against the oracle, bit-exact."""
     rng = np.random.default_rng(1000 + seed)
     for case in range(10):
         w, h = int(rng.integers(3, 261)), int(rng.integers(3, 201))
@@ -573,12 +598,7 @@ def test_random_configurations(oracle, monkeypatch, seed):
             g = ctx.download().reshape(M, h, w)
             for m in range(M):
                 oracle.step(es[m], conn=conn, params=p, want_donor=False)
-                if n_exp == 1.0:
-                    assert np.array_equal(g[m].view(np.uint64), es[m].view(np.uint64)), f"{tag} step {s} member {m}"
-                else:
-                    rel = np.abs(g[m] - es[m]) / np.maximum(np.abs(es[m]), 1e-300)
-                    assert rel.max() <= 1e-9, f"{tag} step {s} member {m}: {rel.max()}"
-                    es[m][...] = g[m]
+                assert np.array_equal(g[m].view(np.uint64), es[m].view(np.uint64)), f"{tag} step {s} member {m}"
         ctx.close()
 
 
@@ -588,7 +608,7 @@ def test_pipelined_graph_tall_rasters(oracle):
     raster and a stacked ensemble, every member bit-exact against the oracle."""
     w, h = 150, 8300  # 260 tile rows
     ctx = device_ctx(w, h)
-    assert ctx.kernels_per_step() > 7  # banded receivers + tiles
+    assert ctx.pipeline_bands() > 1 and ctx.kernels_per_step() > 2 * ctx.pipeline_bands()
     e = oracle.terrain(w, h, 51)
     ctx.upload(e)
     for s in range(2):
@@ -598,7 +618,7 @@ def test_pipelined_graph_tall_rasters(oracle):
         assert d.newton_iters == o["newton_iters"] and d.nlevels == o["nlevels"]
     M, w, h = 8, 96, 1100  # 275 stacked tile rows
     ens = lem.DeviceContext(w, h, sim_params(), 8, members=M)
-    assert ens.kernels_per_step() > 7
+    assert ens.pipeline_bands() > 1
     seeds = list(range(60, 60 + M))
     ens.generate_terrain(seeds)
     want = [oracle.terrain(w, h, sd) for sd in seeds]
