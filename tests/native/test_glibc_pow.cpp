@@ -113,6 +113,30 @@ int main(int argc, char** argv) {
     }
     check(x, y);
   }
+  // the n = 2 fast path: glibc_pow_sq(x) == pow(x, 2), on random x and on x
+  // whose square sits near a rounding midpoint (x = sqrt of a midpoint, nudged)
+  uint64_t bad_sq = 0, nsq = 0;
+  for (uint64_t i = 0; i < count / 2; ++i) {
+    double x;
+    if (i & 1) {
+      x = std::ldexp(u01() + 0.5, (int)(next_u64() % 120) - 80);
+    } else {
+      const double m = std::ldexp(1.0 + u01(), (int)(next_u64() % 100) - 70);  // a square
+      const double mid = m + std::ldexp(1.0, std::ilogb(m) - 53);            // the midpoint above it
+      x = std::sqrt(mid);
+      const int nudge = (int)(next_u64() % 7) - 3;
+      for (int k = 0; k < (nudge < 0 ? -nudge : nudge); ++k) x = std::nextafter(x, nudge < 0 ? 0.0 : 1e300);
+    }
+    ++nsq;
+    const double want = libm_pow(x, 2.0);
+    const double got = fma ? lemgpu::glibc_pow_sq<true>(x) : lemgpu::glibc_pow_sq<false>(x);
+    if (asu(want) != asu(got)) {
+      if (bad_sq < 5) std::printf("POW_SQ MISMATCH x = %a: libm %a fast %a\n", x, want, got);
+      ++bad_sq;
+    }
+  }
+  std::printf("glibc_pow_sq: %llu inputs, %llu mismatches\n", (unsigned long long)nsq, (unsigned long long)bad_sq);
+  bad += bad_sq;
   // identities the n = 1 and n = 2 Newton paths rely on (k_physics.cuh):
   // pow(x, 1) == x and pow(x, 0) == 1 for every positive finite x (normal or not)
   uint64_t bad_id = 0;
