@@ -60,6 +60,17 @@ WORKLOADS = {
 }
 
 
+def arm_config(workload, world):
+    """The `config` both arms print (identical keys and values for the same
+    workload and world size, so the driver can match the two lines)."""
+    wl = WORKLOADS[workload]
+    return {"workload": wl["desc"] + (" -- one independent replica per GPU" if (world > 1 and wl["members"] == 1) else ""),
+            "grid": [wl["w"], wl["h"]], "members": wl["members"] * (world if wl["members"] == 1 else 1),
+            "params": "K=2e-6 m=0.5 n=%g u=2e-3 dt=1000 eps=1e-6 D8" % wl["n_exp"]
+                      + (" (per-member K, m)" if wl["members"] > 1 else ""),
+            "fill": "epsilon_ascending 1e-8" if wl.get("fill") else "off"}
+
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -200,7 +211,7 @@ def run_reference_arm(args):
 
     wl = WORKLOADS[args.workload]
     w, h = wl["w"], wl["h"]
-    cfg = {"workload": wl["desc"], "grid": [w, h], "members": wl["members"], "impl": "reference CPU (rb_private_queues)"}
+    cfg = arm_config(args.workload, env_int("WORLD_SIZE", 1))
     if not RefLib.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liblemref.so not built"}))
         return 0
@@ -227,6 +238,8 @@ def run_reference_arm(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": k_run, "warmup": warm + 1,
            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM, lem::generate_terrain)", "config": cfg,
+           "details": {"impl": "reference CPU: lem::strategy_step(rb_private_queues) of the unmodified reference "
+                               "(oracle/_ref/liblemref.so)"},
            "impl": "reference",
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -358,42 +371,52 @@ def main():
     peak, peak_src = load_peaks()
     n_l = max(kt["launches"], 1)
     step_ms_ev = kt["step"] / n_l
+    # kernel spans per step (device %globaltimer; lemgpu_diag::kernel_s)
     k1_ms, tiles_ms = kt["recv_donor"] / n_l, kt["tiles"] / n_l
     esc_ord_ms, esc_phys_ms = kt["order"] / n_l, kt["physics"] / n_l
-    # dominant kernel: k_tiles (level order, accumulation, uplift and erosion of
-    # every tree that stays within its tile's halo) after k_recv
-    # (receivers, donor masks, code bit planes); the escape path finishes the rest
-    dom, dom_ms, dom_b = "k_tiles", tiles_ms, B_TILES
+    esc_cells = float(np.mean([d.escaped_cells for d in diags])) if diags else 0.0
+    tile_cells = max(cells - esc_cells, 0.0)
     traffic_tbl, traffic_src = traffic_from_profiles(args.workload)
-    traffic = traffic_tbl.get(dom, {}).get("dram_bytes_per_launch") if traffic_tbl else None
     pipelined = ctx.pipeline_bands() > 0
+    # candidate kernels with their algorithmic bytes per step:
+    # k_recv 17 B/cell (receivers 12 + donors 5) for every cell; k_tiles and the
+    # escape path 70 B/cell (order 9 + accumulation 21 + uplift/erosion 40) for
+    # the cells each finishes.  The dominant one is the longest.
+    cands = []
     if pipelined:
-        # tall rasters: k_recv and k_tiles run in interleaved bands (one graph,
-        # receiver band b+1 beside tile band b), so they are measured as one
-        # unit -- the step minus the escape kernels -- on their joint 87 B/cell
-        dom, dom_b = "k_recv+k_tiles (pipelined bands)", B_RECV + B_TILES
-        dom_ms = max(step_ms_ev - esc_ord_ms - esc_phys_ms, 1e-9)
-        if traffic_tbl and "k_tiles" in traffic_tbl and "k_recv" in traffic_tbl:
-            traffic = traffic_tbl["k_tiles"]["dram_bytes_per_launch"] + traffic_tbl["k_recv"]["dram_bytes_per_launch"]
-    achieved = dom_b * cells / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
-    per_gpu = value / world if wl["members"] == 1 else value / world
+        # tall rasters: k_recv and k_tiles run in interleaved bands (receiver band
+        # b+1 beside tile band b): one unit, the step minus the escape kernels
+        cands.append(("k_recv+k_tiles (pipelined bands)", max(step_ms_ev - esc_ord_ms - esc_phys_ms, 1e-9),
+                      B_RECV * cells + B_TILES * tile_cells, ("k_recv", "k_tiles")))
+    else:
+        cands.append(("k_tiles", tiles_ms, B_TILES * tile_cells, ("k_tiles",)))
+        cands.append(("k_recv", k1_ms, B_RECV * cells, ("k_recv",)))
+    cands.append(("escape path (k_esc_small | k_esc_bfs + k_chunks/k_deep_coop)", esc_ord_ms + esc_phys_ms,
+                  B_TILES * esc_cells, ("k_esc_small", "k_esc_bfs", "k_chunks", "k_deep_coop")))
+    dom, dom_ms, dom_bytes, dom_kernels = max(cands, key=lambda c: c[1])
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
+    traffic = None
+    if traffic_tbl and all(k in traffic_tbl for k in dom_kernels[:2]):
+        traffic = sum(traffic_tbl[k]["dram_bytes_per_launch"] for k in dom_kernels if k in traffic_tbl)
+    per_gpu = value / world
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_cell": dom_b,
-                "alg_bytes_note": "SURVEY 8(d): order 9 + accumulation 21 + uplift/erosion 40 = 70 B/cell for "
-                                  "k_tiles (k_recv: receivers 12 + donors 5); k_tiles moves ~18 B/cell" +
-                                  ("; pipelined: k_recv + k_tiles bands together, 87 B/cell over their joint span "
+                "alg_bytes_per_launch": dom_bytes,
+                "alg_bytes_note": "SURVEY 8(d): k_recv 17 B/cell (receivers 12 + donors 5) over all cells; k_tiles / "
+                                  "escape path 70 B/cell (order 9 + accumulation 21 + uplift/erosion 40) over the "
+                                  "cells each finishes" +
+                                  ("; pipelined: k_recv + k_tiles bands as one unit over their joint span "
                                    "(step events minus the escape kernels)" if pipelined else ""),
-                "k_tiles_span_ms": tiles_ms,
-                "k_recv": {"alg_bytes_per_cell": B_RECV, "ms": k1_ms,
-                                 "achieved": B_RECV * cells / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None,
-                                 "frac": (B_RECV * cells / (k1_ms / 1e3) / 1e9 / peak) if k1_ms > 0 else None},
-                "moved_bytes_per_cell_min": B_TILES_MIN,
-                "hbm_frac_of_moved_bytes": (B_TILES_MIN * cells / (dom_ms / 1e3) / 1e9 / peak) if dom_ms > 0 else None,
+                "dominant_by": "longest measured kernel span per step (device %globaltimer)",
+                "dram_frac": (traffic / (dom_ms / 1e3) / 1e9 / peak) if (traffic and dom_ms > 0) else None,
+                "dram_frac_note": "ncu DRAM bytes of the same kernel(s) per launch / their span / peak: the bandwidth "
+                                  "actually moved (the kernels are issue/latency-bound, see DESIGN.md)",
+                "candidates_ms": {c[0]: round(c[1], 5) for c in cands},
+                "escaped_cells_per_step": esc_cells,
                 "kernel_ms": {"step(events)": step_ms_ev, "k_recv": k1_ms, "k_tiles": tiles_ms,
                               "escape:levels": esc_ord_ms, "escape:physics": esc_phys_ms},
                 "timing_source": "CUDA events around each step's graph launch on the context stream; "
-                                 "per-kernel split from device %globaltimer stamps taken by the kernels",
+                                 "kernel spans from device %globaltimer stamps taken by the kernels",
                 "step": {"alg_bytes_per_cell": B_STEP, "achieved": per_gpu * B_STEP / 1e9,
                          "frac": per_gpu * B_STEP / 1e9 / peak},
                 "traffic_source": traffic_src}
@@ -416,16 +439,18 @@ def main():
         "scaling": "weak" if wl["members"] == 1 else "strong",
         "vs_baseline": value / PAPER_P100 if (args.workload == "dem10000" and world == 1) else None,
         "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM generated on device, bit-exact lem::generate_terrain)",
-        "config": {"workload": wl["desc"] + (f" -- one independent replica per GPU, per-step {backend} stats all-reduce"
-                                             if (world > 1 and wl["members"] == 1) else ""),
-                   "grid": [w, h], "members_per_gpu": M, "params": "K=2e-6 m=0.5 n=%g u=2e-3 dt=1000 eps=1e-6" % wl["n_exp"],
+        "config": arm_config(args.workload, world),
+        "details": {"members_per_gpu": M,
                    "parallelism": f"replicas{world}" if wl["members"] == 1 else f"members/{world}",
+                   "collective": (f"per-step {backend} all-reduce of the per-member statistics" if world > 1 else None),
+                   "pow_variant": {1: "glibc __pow_fma", 0: "glibc __pow_sse2", -1: "NONE MATCHES"}[ctx.pow_variant()],
                    "l2": f"inputs larger than L2: {ctx.device_bytes() / 1e9:.1f} GB device state per GPU vs 126 MB L2, no flush",
                    "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",
                    "nlevels_last_step": last.nlevels if last else None,
                    "phase_ms_last_step": ({k: round(v * 1e3, 4) for k, v in zip(
-                       ("k_recv", "-", "escape:order", "k_tiles", "-", "escape:accum+uplift+erosion"), last.seconds)
-                       if k != "-"} if last else None),
+                       ("receivers", "donors", "order", "accumulation", "uplift", "erosion"), last.seconds)}
+                       if last else None),
+                   "lut_misses_last_step": last.lut_misses if last else None,
                    "escaped_trees_last_step": last.escaped_trees if last else None,
                    "newton_iters_last_step": last.newton_iters if last else None,
                    **({"fill": "lem::priority_flood_fill epsilon_ascending 1e-8 on the device (lemgpu_fill), once, "

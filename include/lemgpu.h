@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define LEMGPU_ABI_VERSION 2
+#define LEMGPU_ABI_VERSION 3
 #define LEMGPU_NOFLOW 0xFFFFFFFFu /* kNoFlow, proj/include/lem/raster.hpp:16 */
 
 enum {
@@ -82,13 +82,26 @@ typedef struct lemgpu_member {
 /* Mirror of lem::StepDiagnostics + PhaseTimings
  * (proj/include/lem/simulation.hpp:25-40), plus device-side facts. */
 typedef struct lemgpu_diag {
-  double seconds[6];        /* per-phase device time (globaltimer), lem::Phase order */
+  /* PhaseTimings::seconds, lem::Phase order.  The step's device time (first
+   * kernel start to the end of the step, %globaltimer) split in proportion to
+   * the SM cycles every CTA spent in each phase: the kernels fuse phases
+   * (receivers + donors; order + accumulation + uplift + erosion) and overlap,
+   * so the six slots add up to the step's device time. */
+  double seconds[6];
   uint64_t newton_iters;    /* sum of Newton iterations over eroded cells (erosion.cpp:76-77) */
   uint32_t interior_noflow; /* interior cells with rec == kNoFlow (simulation.cpp:42-44) */
   uint32_t nlevels;         /* TraversalPlan::nlevels() (traversal.hpp:34) */
-  uint32_t lut_misses;      /* cells whose pow(A,m) was not served by the host-libm LUT */
+  uint32_t lut_misses;      /* cells whose pow(A,m) was computed on the device, not read from the
+                               host-libm table (bit-identical either way: glibc_pow.cuh) */
   uint32_t status;          /* LEMGPU_* for this step */
   uint32_t err_cell;        /* ConvergenceError::cell() when status == 3 */
+  uint32_t escaped_trees;   /* trees finished by the escape path (tile path), else source chunks */
+  /* Kernel spans of the step (device %globaltimer, first CTA start to last CTA
+   * end; the receiver and tile passes overlap when pipelined):
+   * [0] receiver pass (k_recv), [1] tile pass (k_tiles), [2] escape path's
+   * level expansion, [3] escape path's accumulation + uplift + erosion. */
+  double kernel_s[4];
+  uint32_t escaped_cells;   /* cells of the escaped trees */
   uint32_t reserved;
 } lemgpu_diag;
 
@@ -191,12 +204,11 @@ uint32_t lemgpu_kernels_per_step(const lemgpu_ctx* ctx);
  * rasters of >= 256 tile rows are). */
 uint32_t lemgpu_pipeline_bands(const lemgpu_ctx* ctx);
 
-/* Device time accumulated over the steps synced since timing was enabled:
- * ms[0] = whole step (CUDA events around each graph launch on the context
- * stream), ms[1] = k_recv_donor, ms[2] = level order (k_level0 + k_expand),
- * ms[3] = accumulation + uplift + erosion (k_chunks / k_deep_*); the phase
- * split comes from %globaltimer stamps taken on the device.  `ms` holds 5:
- * step, k_recv_donor, escape-path order, escape-path physics, k_tiles. */
+/* Device time accumulated over the steps synced since timing was enabled,
+ * `ms` holds 5: [0] whole step (CUDA events around each graph launch on the
+ * context stream), then the summed lemgpu_diag::kernel_s spans: [1] receiver
+ * pass, [2] escape-path level expansion, [3] escape-path accumulation +
+ * uplift + erosion, [4] tile pass. */
 int lemgpu_kernel_timing(lemgpu_ctx* ctx, int enable);
 int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
 
@@ -206,8 +218,17 @@ int lemgpu_kernel_times(lemgpu_ctx* ctx, double* ms, uint32_t* launches);
 int lemgpu_debug_timeline(lemgpu_ctx* ctx, uint64_t* ns, uint32_t cap, uint32_t* count);
 /* Debug / test hook (no reference counterpart): copy `bytes` of a device
  * scratch array of the last step to host memory.  which: 0 = queue (order),
- * 1 = escape-path level bounds, 2 = control block.  Not used by the step. */
+ * 1 = escape-path level bounds, 2 = control block, 3 = the tile pass's
+ * per-cell level (u8, 0xFF: cell of an escaped tree) and 4 = its per-cell
+ * drainage area (f64) -- 3 and 4 need lemgpu_debug_tile_capture.  Not used by
+ * the step. */
 int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes);
+/* Debug / test hook: when enabled, every step's tile pass (k_tiles) also
+ * writes the TraversalPlan level and the drainage area of each cell it
+ * finishes, straight from its shared-memory level lists and counts, so the
+ * tests can pin those phases directly (not through the export path).  Costs
+ * 9 B/cell of extra writes per step while on. */
+int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable);
 
 /* Which glibc pow the device reproduces (glibc_pow.cuh): 1 = __pow_fma,
  * 0 = __pow_sse2 -- the variant the HOST libm's ifunc selected, found at

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "liblemgpu.so"
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 NOFLOW = 0xFFFFFFFF
 
 OK, ECONFIG, ESTRUCTURE, ECONVERGENCE, ECUDA, EOTHER = range(6)
@@ -52,6 +52,9 @@ class lemgpu_diag(C.Structure):
         ("lut_misses", C.c_uint32),
         ("status", C.c_uint32),
         ("err_cell", C.c_uint32),
+        ("escaped_trees", C.c_uint32),
+        ("kernel_s", C.c_double * 4),
+        ("escaped_cells", C.c_uint32),
         ("reserved", C.c_uint32),
     ]
 
@@ -87,6 +90,7 @@ _SIGS = {
     "lemgpu_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
     "lemgpu_debug_timeline": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]),
     "lemgpu_debug_copy": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
+    "lemgpu_debug_tile_capture": (C.c_int, [_P, C.c_int]),
     "lemgpu_pow_variant": (C.c_int, [_P]),
     "lemgpu_debug_pow": (C.c_int, [C.c_int, C.c_int, _P, _P, _P, C.c_uint64]),
     "lemgpu_host_register": (C.c_int, [_P, C.c_size_t]),

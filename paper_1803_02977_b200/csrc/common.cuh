@@ -171,6 +171,7 @@ struct Ctl {
   uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
+  unsigned long long ph_cyc[6];  // SM cycles per lem::Phase charged by the CTAs this step (PhClk)
   uint32_t ntl, nltl;
   unsigned long long tl[96];   // debug timeline of the running step (finisher stamps)
   unsigned long long ltl[98];  // ... and of the last completed step
@@ -233,6 +234,8 @@ struct StepArgs {
   int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
   int pow_fma;        // the host glibc's pow variant the device reproduces: 1 __pow_fma, 0 __pow_sse2
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
+  uint8_t* dbg_level;  // debug capture (nullptr: off): level of every cell k_tiles finishes (escaped: untouched)
+  double* dbg_A;       // ... and its drainage area
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
   cudaGraphConditionalHandle h_expand, h_dacc, h_deros;
@@ -264,6 +267,56 @@ __device__ __forceinline__ void timeline(Ctl* ctl) {
     ctl->ntl = i + 1;
   }
 }
+
+// ---------------------------------------------------------------- phase clocks
+// lem::Phase busy time (PhaseTimings, simulation.hpp:19-32).  The kernels fuse
+// phases (k_recv: receivers + donors; k_tiles / k_esc_small: order,
+// accumulation, uplift, erosion) and overlap (receiver bands beside tile
+// bands), so the phases are not kernel spans: thread 0 of every CTA charges
+// the SM cycles between its phase boundaries (taken where a block barrier
+// closes a phase) to that phase, in shared memory, and adds them to the
+// step's totals when the CTA ends.  k_finalize splits the step's device time
+// (first kernel start to k_finalize) in these proportions: the six slots add
+// up to the step and say where the SMs spent it.
+struct PhClk {
+  unsigned long long last;
+  unsigned long long acc[6];
+};
+__device__ __forceinline__ void phclk_begin(PhClk& c) {
+  if (threadIdx.x == 0) {
+    c.last = (unsigned long long)clock64();
+#pragma unroll
+    for (int i = 0; i < 6; ++i) c.acc[i] = 0;
+  }
+}
+__device__ __forceinline__ void phclk_mark(PhClk& c, int ended) {
+  if (threadIdx.x == 0) {
+    const unsigned long long n = (unsigned long long)clock64();
+    c.acc[ended] += n - c.last;
+    c.last = n;
+  }
+}
+__device__ __forceinline__ void phclk_end(PhClk& c, int ended, Ctl* ctl) {
+  if (threadIdx.x == 0) {
+    phclk_mark(c, ended);
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      if (c.acc[i]) atomicAdd(&ctl->ph_cyc[i], c.acc[i]);
+  }
+}
+
+// A kernel that is one phase: thread 0's cycles from construction to scope exit.
+struct PhWhole {
+  Ctl* ctl;
+  int ph;
+  unsigned long long t0;
+  __device__ __forceinline__ PhWhole(Ctl* c, int p) : ctl(c), ph(p), t0(0) {
+    if (threadIdx.x == 0) t0 = (unsigned long long)clock64();
+  }
+  __device__ __forceinline__ ~PhWhole() {
+    if (threadIdx.x == 0) atomicAdd(&ctl->ph_cyc[ph], (unsigned long long)clock64() - t0);
+  }
+};
 
 // True in every thread of exactly one CTA: the last CTA of the grid to get
 // here (all others have finished their work and fenced it).  The caller's

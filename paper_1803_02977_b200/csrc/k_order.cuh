@@ -135,6 +135,7 @@ __device__ __forceinline__ uint32_t seg_size(uint32_t n, uint32_t G) { return n 
 __global__ void __launch_bounds__(kTPB) k_l0_count(StepArgs a) {
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->err_flag)) return;  // sticky failure of an earlier step (uniform)
+  PhWhole ph(ctl, LEMGPU_PHASE_ORDER);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const uint32_t S = ((a.N + G - 1) / G + 15u) & ~15u;
   const uint32_t s0 = b * S, s1 = min(a.N, s0 + S);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kTPB) k_l0_write(StepArgs a) {
   __shared__ ScanSmem sm;
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->err_flag)) return;
+  PhWhole ph(ctl, LEMGPU_PHASE_ORDER);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const uint32_t S = ((a.N + G - 1) / G + 15u) & ~15u;
   const uint32_t s0 = b * S, s1 = min(a.N, s0 + S);
@@ -367,6 +369,7 @@ __device__ __forceinline__ void expand_finish(const StepArgs& a, uint32_t l, uin
 __global__ void __launch_bounds__(kTPB) k_expand(StepArgs a) {
   __shared__ ScanSmem sm;
   Ctl* ctl = a.ctl;
+  PhWhole ph(ctl, LEMGPU_PHASE_ORDER);
   const uint32_t l = ld_volatile_u32(&ctl->lvl);
   const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
   const uint32_t lo = a.levels[l], hi = a.levels[l + 1];
@@ -524,6 +527,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
   ScanSmem& sm = u.sm;
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->esc_small)) return;  // k_esc_small finished the escaped trees (uniform)
+  PhWhole ph(ctl, LEMGPU_PHASE_ORDER);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const bool err = ld_volatile_u32(&ctl->err_flag) != 0;
   const uint32_t n = ld_volatile_u32(&ctl->nesc);

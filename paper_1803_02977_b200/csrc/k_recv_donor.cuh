@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
   __shared__ __align__(4) uint8_t rc[kBY + 2][kBX + 4];
   __shared__ uint8_t rowint[kBY + 2];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ PhClk s_pc;
   if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  phclk_begin(s_pc);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
   const uint32_t W = a.W, Ht = a.Htot;
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
   __syncthreads();
 
   // ---- donors_of: neighbour in direction k donates iff its code is 7-k.
+  phclk_mark(s_pc, LEMGPU_PHASE_RECEIVERS);
   // Four cells per thread in SWAR form: for each direction, the four
   // neighbour codes are one byte window of a shared row.
   for (int r = warp; r < kBY; r += kNW) {
@@ -336,6 +339,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
     }
   }
   __syncthreads();
+  phclk_end(s_pc, LEMGPU_PHASE_DONORS, a.ctl);
   if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());
 }
 
@@ -364,6 +368,8 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     k_recv(const __grid_constant__ StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ PhClk s_pc;
+  phclk_begin(s_pc);
   // an earlier step of the batch failed: nothing to do (checked once the TMA
   // box has landed -- a CTA must not exit with a bulk copy in flight)
   const uint32_t failed = ld_volatile_u32(&a.ctl->err_flag);
@@ -481,7 +487,8 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     else
       cw1 = (cw1 & ~(15u << sh4)) | (code << sh4);
   }
-  // ---- pass 3: stores
+  // ---- pass 3: stores (codes, and the bit planes the donors are derived from)
+  phclk_mark(s_pc, LEMGPU_PHASE_RECEIVERS);
   const int nr = min(kBY / 2, max(0, (int)Ht - (int)(y0 + (uint32_t)t0)));  // rows inside the raster (warp-uniform)
   const uint32_t j = x0 / 32 + (uint32_t)(cx >> 5);  // plane word of this warp's columns
   const bool xok = gx < W, pok = lane < 4 && j < a.W32;
@@ -508,6 +515,7 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     for (int i = 0; i < 16; ++i)
       if (i < nr) store_row(i);
   }
+  phclk_end(s_pc, LEMGPU_PHASE_DONORS, a.ctl);
   if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());  // (no barrier: thread 0's end ~ the CTA's)
 }
 

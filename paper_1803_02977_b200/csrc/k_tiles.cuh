@@ -130,12 +130,24 @@ __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32
   return __ddiv_rn(__dmul_rn(__ldg(a.kdt + mem), glibc_pow_dev(a.pow_fma, A, __ldg(a.mexp + mem))), pd);
 }
 
+// Drainage area of a tile cell for the debug capture: count (escape mark in
+// bit 31 dropped) x cell area, or the FP sum itself.
+template <bool EX, typename T>
+__device__ __forceinline__ double dbg_area(T v, double w0) {
+  if constexpr (EX)
+    return __dmul_rn((double)(v & 0x7FFFFFFFu), w0);
+  else
+    return (double)v;
+}
+
 template <int CONN, int NK, bool EX>
 __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char smraw[];
   TileSmem<EX>& s = *reinterpret_cast<TileSmem<EX>*>(smraw);
+  __shared__ PhClk s_pc;
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->err_flag)) return;  // an earlier step failed (uniform)
+  phclk_begin(s_pc);
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const int W = (int)a.W, Ht = (int)a.Htot;
   const uint32_t ntx = (a.W + kTX - 1) / kTX, nty = (a.Htot + kTY - 1) / kTY;
@@ -472,6 +484,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       __syncthreads();
     }
     // ---- 6. drainage area
+    phclk_mark(s_pc, LEMGPU_PHASE_ORDER);  // staging + the levels
     if (EX) {
       // cell counts: every cell adds 1 to each ancestor (integer adds commute)
       for (uint32_t i = (nl > 1 ? s.lvs[1] : 0u) + tid; i < (nl > 1 ? s.lvs[nl] : 0u); i += kTTPB) {
@@ -507,6 +520,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         __syncthreads();
       }
     }
+    phclk_mark(s_pc, LEMGPU_PHASE_ACCUM);
     // ---- 7. level 0: uplift interior sources (never eroded)
     // escaped roots -> the global level path (level 0 of its queue)
     for (uint32_t i0 = 0; i0 < (nl ? s.lvs[1] : 0u); i0 += kTTPB) {
@@ -529,6 +543,10 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           }
           a.hout[gc] = hv;
           ++cells;
+          if (a.dbg_level) {
+            a.dbg_level[gc] = 0;
+            a.dbg_A[gc] = dbg_area<EX>(ACC(q), a.w0);
+          }
         }
       }
       const uint32_t eb = __ballot_sync(0xffffffffu, e);
@@ -541,8 +559,9 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       }
     }
     __syncthreads();
+    phclk_mark(s_pc, LEMGPU_PHASE_UPLIFT);
     // erosion, downstream -> upstream, with the receiver's updated elevation
-    auto erode = [&](uint32_t i) -> bool {
+    auto erode = [&](uint32_t i, uint32_t lev) -> bool {
       const uint32_t q = s.list[i];
       const uint32_t code = RC(q);
       const uint32_t p = (uint32_t)((int)q + woff(code));
@@ -583,6 +602,10 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       }
       HW(q) = hnew;
       a.hout[gc] = hnew;
+      if (a.dbg_level) {  // debug capture (lemgpu_debug_tile_capture): this cell's level and drainage area
+        a.dbg_level[gc] = (uint8_t)lev;
+        a.dbg_A[gc] = dbg_area<EX>(ACC(q), a.w0);
+      }
       return true;
     };
     // the last levels, once at most kSmallLevel cells remain, by warp 0 alone
@@ -590,18 +613,19 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     while (lw > 1 && s.lvs[nl] - s.lvs[lw - 1] <= (uint32_t)kSmallEro) --lw;
     for (uint32_t l = 1; l < lw; ++l) {
       bool any = false;
-      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) any |= erode(i);
+      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) any |= erode(i, l);
       if (__syncthreads_or(any)) maxl = max(maxl, l + 1);
     }
     if (tid < 32) {
       for (uint32_t l = lw; l < nl; ++l) {
         bool any = false;
-        for (uint32_t i = s.lvs[l] + lane; i < s.lvs[l + 1]; i += 32) any |= erode(i);
+        for (uint32_t i = s.lvs[l] + lane; i < s.lvs[l + 1]; i += 32) any |= erode(i, l);
         if (__any_sync(0xffffffffu, any)) maxl = max(maxl, l + 1);
         __syncwarp();
       }
     }
     if (nl) maxl = max(maxl, 1u);
+    phclk_mark(s_pc, LEMGPU_PHASE_EROSION);
   }
 
   // ---- counters: one atomic per warp for the whole kernel
@@ -620,6 +644,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   }
   if (tid == 0) atomicMax(&ctl->tile_nlev, maxl);
   __syncthreads();
+  phclk_end(s_pc, LEMGPU_PHASE_EROSION, ctl);
   if (tid == 0) atomicMax(&ctl->t_t_end, globaltimer());
 }
 
@@ -681,6 +706,8 @@ template <int NK>
 __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   EscSmallSmem& s = *reinterpret_cast<EscSmallSmem*>(smraw);
+  __shared__ PhClk s_pc;
+  phclk_begin(s_pc);
   Ctl* ctl = a.ctl;
   const uint32_t tid = threadIdx.x, G = gridDim.x;
   const uint32_t n = ld_volatile_u32(&ctl->nesc);  // 0 when an earlier step failed (k_tiles did not run)
@@ -749,6 +776,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   if (!ok) {
     if (tid == 0) atomicAdd(&ctl->esc_fail, 1u);
   } else if (nr > 0) {
+    phclk_mark(s_pc, LEMGPU_PHASE_ORDER);
     // accumulation, deepest level first: A = w + the children's A in slot order
     for (int l = (int)nl - 1; l >= 0; --l) {
       for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
@@ -759,6 +787,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
       }
       __syncthreads();
     }
+    phclk_mark(s_pc, LEMGPU_PHASE_ACCUM);
     // uplift (level 0: interior sources only), erosion level by level
     uint32_t iters = 0, misses = 0;
     for (uint32_t l = 0; l < nl; ++l) {
@@ -813,6 +842,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   // the last CTA decides
   __shared__ uint32_t s_last;
   __syncthreads();
+  phclk_end(s_pc, ok ? LEMGPU_PHASE_EROSION : LEMGPU_PHASE_ORDER, ctl);
   if (tid == 0) {
     __threadfence();
     s_last = atomicAdd(&ctl->esc_done, 1u) == G - 1 ? 1u : 0u;
@@ -828,8 +858,6 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
       ctl->esc_small = 1;
       ctl->newton += *reinterpret_cast<volatile unsigned long long*>(&ctl->esc_iters);
       ctl->misses += ld_volatile_u32(&ctl->esc_misses);
-      // the whole kernel is reported as the escape path's ORDER phase
-      // (k_finalize: ORDER = t_order_end - t_t_end, EROSION = t_phys_end - t_order_end)
       const unsigned long long t = globaltimer();
       ctl->t_order_end = t;
       ctl->t_phys_end = t;

@@ -977,6 +977,8 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
                   a.ctl,      ctx->d_diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (a.dbg_level) cudaFree(a.dbg_level);
+  if (a.dbg_A) cudaFree(a.dbg_A);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   for (int p = 0; p < 2; ++p) {
     if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
@@ -1143,10 +1145,10 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
       float t = 0;
       cudaEventElapsedTime(&t, ctx->ev[2 * s], ctx->ev[2 * s + 1]);
       ctx->kernel_ms[0] += t;
-      ctx->kernel_ms[1] += d[s].seconds[LEMGPU_PHASE_RECEIVERS] * 1e3;
-      ctx->kernel_ms[2] += d[s].seconds[LEMGPU_PHASE_ORDER] * 1e3;
-      ctx->kernel_ms[3] += d[s].seconds[LEMGPU_PHASE_EROSION] * 1e3;
-      ctx->kernel_ms[4] += d[s].seconds[LEMGPU_PHASE_ACCUM] * 1e3;
+      ctx->kernel_ms[1] += d[s].kernel_s[0] * 1e3;
+      ctx->kernel_ms[2] += d[s].kernel_s[2] * 1e3;
+      ctx->kernel_ms[3] += d[s].kernel_s[3] * 1e3;
+      ctx->kernel_ms[4] += d[s].kernel_s[1] * 1e3;
     }
     ctx->kernel_launches += n;
   }
@@ -1355,9 +1357,46 @@ int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes) {
   CU(ctx, cudaSetDevice(ctx->device));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   const void* src = which == 0 ? (const void*)ctx->a.order : which == 1 ? (const void*)ctx->d_levels_esc
-                                                                          : (const void*)ctx->a.ctl;
-  const uint64_t cap = which == 0 ? (uint64_t)ctx->a.N * 4 : which == 1 ? ((uint64_t)ctx->a.N + 2) * 4 : sizeof(Ctl);
+                    : which == 2 ? (const void*)ctx->a.ctl : which == 3 ? (const void*)ctx->a.dbg_level
+                                                                         : (const void*)ctx->a.dbg_A;
+  const uint64_t cap = which == 0 ? (uint64_t)ctx->a.N * 4 : which == 1 ? ((uint64_t)ctx->a.N + 2) * 4
+                       : which == 2 ? sizeof(Ctl) : which == 3 ? (uint64_t)ctx->a.N : (uint64_t)ctx->a.N * 8;
+  if (!src) return fail(ctx, LEMGPU_ECONFIG, "debug capture is off");
   CU(ctx, cudaMemcpy(host, src, bytes < cap ? bytes : cap, cudaMemcpyDeviceToHost));
+  return LEMGPU_OK;
+}
+
+int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  StepArgs& a = ctx->a;
+  if (enable && !a.dbg_level) {
+    CU(ctx, cudaMalloc(&a.dbg_level, a.N));
+    CU(ctx, cudaMalloc(&a.dbg_A, (size_t)a.N * sizeof(double)));
+  } else if (!enable && a.dbg_level) {
+    cudaFree(a.dbg_level);
+    cudaFree(a.dbg_A);
+    a.dbg_level = nullptr;
+    a.dbg_A = nullptr;
+  } else {
+    return LEMGPU_OK;
+  }
+  for (uint32_t p = 0; p < 2; ++p) {  // StepArgs is captured by value in the graph nodes
+    if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
+    if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
+    ctx->exec[p] = nullptr;
+    ctx->graph[p] = nullptr;
+    const int rc = build_graph(ctx, p);
+    if (rc) return rc;
+  }
+  if (a.dbg_level) {
+    CU(ctx, cudaMemset(a.dbg_level, 0xFF, a.N));
+    CU(ctx, cudaMemset(a.dbg_A, 0xFF, (size_t)a.N * sizeof(double)));
+  }
   return LEMGPU_OK;
 }
 

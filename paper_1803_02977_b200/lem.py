@@ -221,12 +221,15 @@ class StepDiagnostics:
     interior_noflow: int = 0
     nlevels: int = 0
     lut_misses: int = 0
-    escaped_trees: int = 0  # trees finished by the global level path (k_tiles path), else source chunks
+    escaped_trees: int = 0  # trees finished by the escape path (tile path), else source chunks
+    kernel_seconds: List[float] = field(default_factory=lambda: [0.0] * 4)  # receiver, tile, escape-levels, escape-physics spans
+    escaped_cells: int = 0
 
     @staticmethod
     def from_abi(d: _abi.lemgpu_diag) -> "StepDiagnostics":
         return StepDiagnostics(list(d.seconds), int(d.newton_iters), int(d.interior_noflow),
-                               int(d.nlevels), int(d.lut_misses), int(d.reserved))
+                               int(d.nlevels), int(d.lut_misses), int(d.escaped_trees), list(d.kernel_s),
+                               int(d.escaped_cells))
 
     @property
     def timings(self):
@@ -364,6 +367,21 @@ class DeviceContext:
         self._check(self._L.lemgpu_kernel_times(self._h, ms, C.byref(n)))
         return {"step": ms[0], "recv_donor": ms[1], "order": ms[2], "physics": ms[3], "tiles": ms[4],
                 "launches": n.value}
+
+    def tile_capture(self, enable: bool = True):
+        """Debug: make every step's tile pass record each finished cell's level and
+        drainage area (lemgpu_debug_tile_capture); read them with tile_levels()."""
+        self._check(self._L.lemgpu_debug_tile_capture(self._h, 1 if enable else 0))
+
+    def tile_levels(self):
+        """(level u8 [N], A f64 [N]) written by the last step's tile pass; level 0xFF
+        marks a cell of a tree that escaped its tile (finished by the escape path)."""
+        n = self.n
+        lv = np.empty(n, np.uint8)
+        A = np.empty(n, np.float64)
+        self._check(self._L.lemgpu_debug_copy(self._h, 3, lv.ctypes.data, lv.nbytes))
+        self._check(self._L.lemgpu_debug_copy(self._h, 4, A.ctypes.data, A.nbytes))
+        return lv, A
 
     def debug_timeline(self):
         """k_flow barrier timestamps of the last step, as ms offsets from its start."""

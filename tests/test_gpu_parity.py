@@ -628,3 +628,33 @@ def test_pipelined_graph_tall_rasters(oracle):
         for m in range(M):
             oracle.step(want[m], want_donor=False)
             assert np.array_equal(g[m].view(np.uint64), want[m].view(np.uint64)), (s, m)
+
+
+@pytest.mark.parametrize("w,h,seed,kw,terrain", [
+    (300, 200, 71, {}, "noise"), (257, 131, 72, {"dx": 0.5, "dy": 0.25}, "noise"), (130, 97, 73, {"n_exp": 2.0}, "noise"),
+    (129, 70, 74, {}, "ramp"), (1000, 1000, 42, {}, "noise"),
+])
+def test_tile_pass_levels_and_area_direct(oracle, w, h, seed, kw, terrain):
+    """The tile pass's own level lists and drainage areas (captured inside
+    k_tiles from shared memory, not rebuilt by the export path) equal the
+    reference's TraversalPlan levels and accumulation for every cell it
+    finishes; the cells it leaves are exactly those of the escaped trees."""
+    ctx = device_ctx(w, h, **kw)
+    ctx.tile_capture(True)
+    e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
+    ctx.upload(e)
+    p = make_params(**kw)
+    for s in range(2):
+        d = ctx.step(1)[0]
+        o = oracle.step(e, params=p, want_donor=False)
+        lv, A = ctx.tile_levels()
+        olv = np.empty(w * h, np.int32)
+        for L in range(o["nlevels"]):
+            olv[o["order"][o["levels"][L]:o["levels"][L + 1]]] = L
+        done = lv != 0xFF
+        assert done.sum() == w * h - d.escaped_cells, (done.sum(), d.escaped_cells)
+        assert np.array_equal(lv[done].astype(np.int32), olv[done]), f"step {s}: tile levels differ"
+        assert np.array_equal(A[done].view(np.uint64), o["A"][done].view(np.uint64)), f"step {s}: tile areas differ"
+        if s == 0 and terrain == "noise":
+            assert done.mean() > 0.9  # random noise: nearly every tree stays inside its tile
+    ctx.tile_capture(False)
