@@ -171,7 +171,7 @@ struct Ctl {
   uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
-  unsigned long long ph_cyc[6];  // SM cycles per lem::Phase charged by the CTAs this step (PhClk)
+  unsigned long long ph_cyc[32][6];  // SM cycles per lem::Phase charged by the CTAs this step (PhClk), 32 spread slots
   uint32_t ntl, nltl;
   unsigned long long tl[96];   // debug timeline of the running step (finisher stamps)
   unsigned long long ltl[98];  // ... and of the last completed step
@@ -279,29 +279,38 @@ __device__ __forceinline__ void timeline(Ctl* ctl) {
 // (first kernel start to k_finalize) in these proportions: the six slots add
 // up to the step and say where the SMs spent it.
 struct PhClk {
-  unsigned long long last;
+  uint32_t last;  // 32-bit SM clock (%clock): deltas between marks are far below 2^32 cycles
+  uint32_t pad;
   unsigned long long acc[6];
 };
+#ifdef LEMGPU_NO_PHCLK
+#define LEMGPU_PHCLK_ON 0
+#else
+#define LEMGPU_PHCLK_ON 1
+#endif
 __device__ __forceinline__ void phclk_begin(PhClk& c) {
-  if (threadIdx.x == 0) {
-    c.last = (unsigned long long)clock64();
+  if (LEMGPU_PHCLK_ON && threadIdx.x == 0) {
+    c.last = (uint32_t)clock();
 #pragma unroll
     for (int i = 0; i < 6; ++i) c.acc[i] = 0;
   }
 }
 __device__ __forceinline__ void phclk_mark(PhClk& c, int ended) {
-  if (threadIdx.x == 0) {
-    const unsigned long long n = (unsigned long long)clock64();
+  if (LEMGPU_PHCLK_ON && threadIdx.x == 0) {
+    const uint32_t n = (uint32_t)clock();
     c.acc[ended] += n - c.last;
     c.last = n;
   }
 }
 __device__ __forceinline__ void phclk_end(PhClk& c, int ended, Ctl* ctl) {
-  if (threadIdx.x == 0) {
+  if (LEMGPU_PHCLK_ON && threadIdx.x == 0) {
     phclk_mark(c, ended);
+    // spread over 32 slots: tens of thousands of CTAs (k_recv) would
+    // otherwise serialise on six addresses
+    unsigned long long* slot = ctl->ph_cyc[(blockIdx.x + blockIdx.y * 7u) & 31u];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
-      if (c.acc[i]) atomicAdd(&ctl->ph_cyc[i], c.acc[i]);
+      if (c.acc[i]) atomicAdd(slot + i, c.acc[i]);
   }
 }
 
@@ -314,7 +323,7 @@ struct PhWhole {
     if (threadIdx.x == 0) t0 = (unsigned long long)clock64();
   }
   __device__ __forceinline__ ~PhWhole() {
-    if (threadIdx.x == 0) atomicAdd(&ctl->ph_cyc[ph], (unsigned long long)clock64() - t0);
+    if (threadIdx.x == 0) atomicAdd(&ctl->ph_cyc[blockIdx.x & 31u][ph], (unsigned long long)clock64() - t0);
   }
 };
 

@@ -543,10 +543,6 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           }
           a.hout[gc] = hv;
           ++cells;
-          if (a.dbg_level) {
-            a.dbg_level[gc] = 0;
-            a.dbg_A[gc] = dbg_area<EX>(ACC(q), a.w0);
-          }
         }
       }
       const uint32_t eb = __ballot_sync(0xffffffffu, e);
@@ -561,7 +557,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     __syncthreads();
     phclk_mark(s_pc, LEMGPU_PHASE_UPLIFT);
     // erosion, downstream -> upstream, with the receiver's updated elevation
-    auto erode = [&](uint32_t i, uint32_t lev) -> bool {
+    auto erode = [&](uint32_t i) -> bool {
       const uint32_t q = s.list[i];
       const uint32_t code = RC(q);
       const uint32_t p = (uint32_t)((int)q + woff(code));
@@ -602,10 +598,6 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       }
       HW(q) = hnew;
       a.hout[gc] = hnew;
-      if (a.dbg_level) {  // debug capture (lemgpu_debug_tile_capture): this cell's level and drainage area
-        a.dbg_level[gc] = (uint8_t)lev;
-        a.dbg_A[gc] = dbg_area<EX>(ACC(q), a.w0);
-      }
       return true;
     };
     // the last levels, once at most kSmallLevel cells remain, by warp 0 alone
@@ -613,18 +605,28 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     while (lw > 1 && s.lvs[nl] - s.lvs[lw - 1] <= (uint32_t)kSmallEro) --lw;
     for (uint32_t l = 1; l < lw; ++l) {
       bool any = false;
-      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) any |= erode(i, l);
+      for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) any |= erode(i);
       if (__syncthreads_or(any)) maxl = max(maxl, l + 1);
     }
     if (tid < 32) {
       for (uint32_t l = lw; l < nl; ++l) {
         bool any = false;
-        for (uint32_t i = s.lvs[l] + lane; i < s.lvs[l + 1]; i += 32) any |= erode(i, l);
+        for (uint32_t i = s.lvs[l] + lane; i < s.lvs[l + 1]; i += 32) any |= erode(i);
         if (__any_sync(0xffffffffu, any)) maxl = max(maxl, l + 1);
         __syncwarp();
       }
     }
     if (nl) maxl = max(maxl, 1u);
+    if (a.dbg_level) {  // debug capture (lemgpu_debug_tile_capture): level and drainage area of the finished cells
+      __syncthreads();  // escape marks are final (inherited during the erosion)
+      for (uint32_t l = 0; l < nl; ++l)
+        for (uint32_t i = s.lvs[l] + tid; i < s.lvs[l + 1]; i += kTTPB) {
+          const uint32_t q = s.list[i];
+          if (ESC_GET(q)) continue;
+          a.dbg_level[gcell(q)] = (uint8_t)l;
+          a.dbg_A[gcell(q)] = dbg_area<EX>(ACC(q), a.w0);
+        }
+    }
     phclk_mark(s_pc, LEMGPU_PHASE_EROSION);
   }
 
