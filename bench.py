@@ -256,6 +256,8 @@ def main():
     ap.add_argument("--workload", default="dem10000", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--options", default=None,
+                    help="JSON dict of lemgpu_options knobs (profiling / tuning), e.g. '{\"eager\": 1}'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -284,8 +286,11 @@ def main():
     ids, seeds, km, members_total = member_table(args.workload, rank, world)
     M = len(ids)
     params = lem.SimParams(n_exp=wl["n_exp"])
+    opts = json.loads(args.options) if args.options else {}
+    if os.environ.get("LEMGPU_EAGER") == "1":  # profiling (tools/profile_round.sh): ncu cannot see graph kernel nodes
+        opts["eager"] = 1
     ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M,
-                            per_member=km if (wl["members"] > 1) else None)
+                            per_member=km if (wl["members"] > 1) else None, options=opts or None)
     ctx.generate_terrain(seeds)
     fill_ms = None
     if wl.get("fill"):  # lem::priority_flood_fill on the device, once, before the timed steps

@@ -105,6 +105,33 @@ typedef struct lemgpu_diag {
   uint32_t reserved;
 } lemgpu_diag;
 
+/* Schedule / tuning / test knobs of a context (no reference counterpart).
+ * Zero-initialised = the production defaults; the library reads no
+ * environment variables.  Every knob gives the same bits (the schedules are
+ * dependency-respecting orders of identical per-cell arithmetic); the tests
+ * use them to force every code path. */
+typedef struct lemgpu_options {
+  int32_t global_path;     /* 1: every tree through the global level path (no tile pass) */
+  int32_t force_escape;    /* 1: every tile tree escapes; 2: trees with an odd root cell escape */
+  int32_t force_deep;      /* 1: per-level sweeps even for shallow plans */
+  int32_t eager;           /* 1: the step's kernels launched one by one, not as a CUDA graph (ncu) */
+  int32_t no_tma;          /* 1: plain loads instead of TMA boxes */
+  int32_t no_narrow;       /* 1: every escape level grid-wide (no narrow runs on one CTA) */
+  int32_t no_esc_small;    /* 1: escaped trees always through the cooperative kernels */
+  int32_t pipe;            /* receiver / tile pipeline bands: 0 default (24 for >= 256 tile rows), -1 off */
+  int32_t pipe_unchained;  /* 1: receiver bands independent (default: chained) */
+  uint32_t tile_grid;      /* CTAs of k_tiles (0: occupancy x SMs) */
+  uint32_t esc_grid;       /* CTAs of the cooperative escape expansion (0: one per SM) */
+  uint32_t esc_small_grid; /* CTAs of k_esc_small (0: one per SM) */
+  uint32_t pipe_tile_grid; /* k_tiles CTAs per pipeline band (0: 4 per SM) */
+  uint32_t lut_entries;    /* size of the host-libm F table per member and class (0: min(W*H + 1, 65537));
+                              raised to cover every tile-tree cell count */
+  uint32_t host_bands;     /* banded host step: bands (0: one per ~25 MB, <= 32; 1..3: unbanded) */
+  uint32_t patch_cap;      /* banded host step: escaped-cell patch capacity (0: max(2^20, N/16)) */
+  int32_t host_profile;    /* 1: banded host step prints its timing to stderr */
+  int32_t reserved[3];
+} lemgpu_options;
+
 typedef struct lemgpu_ctx lemgpu_ctx;
 
 /* ---- lifetime ---------------------------------------------------------- */
@@ -122,6 +149,10 @@ int lemgpu_create(int device, uint32_t width, uint32_t height, const lemgpu_para
 int lemgpu_create_ensemble(int device, uint32_t width, uint32_t height, uint32_t members,
                            const lemgpu_params* params, const lemgpu_member* per_member,
                            lemgpu_ctx** out);
+
+/* lemgpu_create_ensemble with explicit options (NULL: defaults). */
+int lemgpu_create_ex(int device, uint32_t width, uint32_t height, uint32_t members, const lemgpu_params* params,
+                     const lemgpu_member* per_member, const lemgpu_options* options, lemgpu_ctx** out);
 
 void lemgpu_destroy(lemgpu_ctx* ctx);
 

@@ -59,6 +59,16 @@ class lemgpu_diag(C.Structure):
     ]
 
 
+class lemgpu_options(C.Structure):
+    """Schedule / tuning / test knobs (include/lemgpu.h); zero = defaults."""
+
+    _fields_ = [(n, C.c_int32) for n in ("global_path", "force_escape", "force_deep", "eager", "no_tma", "no_narrow",
+                                         "no_esc_small", "pipe", "pipe_unchained")] + \
+               [(n, C.c_uint32) for n in ("tile_grid", "esc_grid", "esc_small_grid", "pipe_tile_grid", "lut_entries",
+                                          "host_bands", "patch_cap")] + \
+               [("host_profile", C.c_int32), ("reserved", C.c_int32 * 3)]
+
+
 # Every symbol include/lemgpu.h declares, with its ctypes signature.
 _P = C.c_void_p
 _SIGS = {
@@ -67,6 +77,11 @@ _SIGS = {
     "lemgpu_create_ensemble": (
         C.c_int,
         [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(lemgpu_params), C.POINTER(lemgpu_member), C.POINTER(_P)],
+    ),
+    "lemgpu_create_ex": (
+        C.c_int,
+        [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(lemgpu_params), C.POINTER(lemgpu_member),
+         C.POINTER(lemgpu_options), C.POINTER(_P)],
     ),
     "lemgpu_destroy": (None, [_P]),
     "lemgpu_upload_elev": (C.c_int, [_P, _P]),

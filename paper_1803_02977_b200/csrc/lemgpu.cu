@@ -61,6 +61,8 @@ struct lemgpu_ctx {
   int pipe_chain = 1;                // receiver bands chained (else independent)
   int pow_variant = -1;              // host_pow_variant(): the glibc pow the device reproduces
   uint32_t pipe_bands = 0;           // bands of the pipelined graph (0: not pipelined)
+  uint32_t opt_patch_cap = 0;        // lemgpu_options::patch_cap
+  bool host_profile = false;         // lemgpu_options::host_profile
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> band_ev;
@@ -391,8 +393,9 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
 }
 
 int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_params* p,
-                const lemgpu_member* per_member, lemgpu_ctx** out) {
+                const lemgpu_member* per_member, const lemgpu_options* opts, lemgpu_ctx** out) {
   *out = nullptr;
+  const lemgpu_options o = opts ? *opts : lemgpu_options{};
   if (!p) return fail(nullptr, LEMGPU_ECONFIG, "params must not be NULL");
   std::string why;
   if (validate(p, why)) return fail(nullptr, LEMGPU_ECONFIG, "%s", why.c_str());
@@ -468,7 +471,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->pow_variant = host_pow_variant();
   a.pow_fma = ctx->pow_variant != 0 ? 1 : 0;
   uint32_t lut_entries = a.MN < 65536u ? a.MN + 1 : 65537u;
-  if (const char* env = std::getenv("LEMGPU_LUT_ENTRIES")) lut_entries = (uint32_t)std::strtoul(env, nullptr, 10);
+  if (o.lut_entries) {
+    // the tile pass indexes the table with tile-tree cell counts unchecked (k_tiles EX path)
+    const uint32_t need = std::min<uint32_t>(a.MN, (uint32_t)(kDW * kDH)) + 1u;
+    lut_entries = std::max(o.lut_entries, need);
+  }
   if (lut_entries < 2) lut_entries = 2;
   a.lut_entries = lut_entries;
 
@@ -554,42 +561,44 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if (ctx->scan_grid > 4096) ctx->scan_grid = 4096;  // part/bins capacity
   ctx->use_tiles = 1;
   ctx->esc_grid = nsm;
-  if (const char* env = std::getenv("LEMGPU_ESC_GRID")) ctx->esc_grid = std::atoi(env);
+  if (o.esc_grid) ctx->esc_grid = (int)o.esc_grid;
   if (ctx->esc_grid < 1 || ctx->esc_grid > ctx->scan_grid) ctx->esc_grid = ctx->scan_grid;
-  if (const char* env = std::getenv("LEMGPU_PATH")) ctx->use_tiles = std::strcmp(env, "global") != 0;
+  if (o.global_path) ctx->use_tiles = 0;
   a.force_escape = 0;
-  if (const char* env = std::getenv("LEMGPU_FORCE_ESCAPE")) a.force_escape = std::atoi(env);
+  a.force_escape = o.force_escape;
   {
     const void* ft = tiles_fn(a);
     CUB(cudaFuncSetAttribute(ft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiles_smem(a)));
     CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ft, kTTPB, tiles_smem(a)));
     const uint32_t ntiles = ((W + kTX - 1) / kTX) * ((H * M + kTY - 1) / kTY);
     uint32_t tg = (uint32_t)(occ > 0 ? occ : 1) * (uint32_t)nsm;
-    if (const char* env = std::getenv("LEMGPU_TILE_GRID")) tg = (uint32_t)std::atoi(env);  // testing: few CTAs, many tiles each
+    if (o.tile_grid) tg = o.tile_grid;  // testing: few CTAs, many tiles each
     if (tg < 1) tg = 1;
     ctx->tile_grid = (int)(tg < ntiles ? tg : ntiles);
   }
   a.eager = 0;
-  a.force_deep = std::getenv("LEMGPU_FORCE_DEEP") ? 1 : 0;
-  if (const char* env = std::getenv("LEMGPU_ESC_SMALL")) ctx->esc_small = std::atoi(env) != 0;
+  a.force_deep = o.force_deep ? 1 : 0;
+  if (o.no_esc_small) ctx->esc_small = false;
   ctx->esc_small_grid = nsm;
   {  // pipelined receivers / tiles for tall rasters: 24 bands (measured best at 10000^2: 2.127 -> 2.061 ms)
     const uint32_t nty = (H * M + kTY - 1) / kTY;
     ctx->pipe = nty >= 256 ? 24 : 0;  // (5000^2: 157 tile rows, banding costs more than it overlaps)
   }
-  if (const char* env = std::getenv("LEMGPU_PIPE")) ctx->pipe = std::atoi(env);
+  if (o.pipe) ctx->pipe = o.pipe < 0 ? 0 : o.pipe;
   ctx->pipe_tile_grid = 4 * nsm;
-  if (const char* env = std::getenv("LEMGPU_PIPE_CHAIN")) ctx->pipe_chain = std::atoi(env);
-  if (const char* env = std::getenv("LEMGPU_PIPE_TILE_GRID")) ctx->pipe_tile_grid = std::max(1, std::atoi(env));
-  if (const char* env = std::getenv("LEMGPU_ESC_SMALL_GRID")) ctx->esc_small_grid = std::max(1, std::atoi(env));
-  if (const char* env = std::getenv("LEMGPU_HOST_BANDS")) ctx->bands = std::atoi(env);
+  if (o.pipe_unchained) ctx->pipe_chain = 0;
+  if (o.pipe_tile_grid) ctx->pipe_tile_grid = (int)o.pipe_tile_grid;
+  if (o.esc_small_grid) ctx->esc_small_grid = (int)o.esc_small_grid;
+  ctx->bands = (int)o.host_bands;
+  ctx->opt_patch_cap = o.patch_cap;
+  ctx->host_profile = o.host_profile != 0;
   if (ctx->bands <= 0) {  // measured on 10000^2 (tools/e2e_probe.py): 32 bands of 25 MB beat 16 and 64
     const uint64_t nbands = N64 * 8 / (25ull << 20);
     ctx->bands = (int)std::min<uint64_t>(32, nbands < 4 ? 1 : nbands);
   }
   if (a.force_deep) ctx->esc_small = false;  // testing the deep sweeps of the escape path
-  a.no_narrow = std::getenv("LEMGPU_NO_NARROW") ? 1 : 0;  // testing: grid-wide sweeps for every level
-  if (const char* env = std::getenv("LEMGPU_EAGER")) a.eager = std::atoi(env) != 0;
+  a.no_narrow = o.no_narrow ? 1 : 0;  // testing: grid-wide sweeps for every level
+  a.eager = o.eager ? 1 : 0;
   for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
     CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEscSmallSmemBytes));
   for (const void* f : {(const void*)k_deep_coop<0>, (const void*)k_deep_coop<1>, (const void*)k_deep_coop<2>})
@@ -611,7 +620,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   // k_recv_donor halo tile and one k_tiles window.  The row pitch must be a
   // multiple of 16 bytes (even W); otherwise the kernels stage h with plain loads.
   a.use_tma = 0;
-  if ((W % 2) == 0 && !std::getenv("LEMGPU_NO_TMA")) {
+  if ((W % 2) == 0 && !o.no_tma) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
@@ -778,7 +787,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     // room for the escaped trees of a typical step (a few % of the cells);
     // more than that and the whole raster is copied down again
     ctx->patch_cap = std::max<uint32_t>(1u << 20, a.N / 16);
-    if (const char* env = std::getenv("LEMGPU_PATCH_CAP")) ctx->patch_cap = (uint32_t)std::atoi(env);  // testing
+    if (ctx->opt_patch_cap) ctx->patch_cap = ctx->opt_patch_cap;  // testing
     ctx->patch_cap = (ctx->patch_cap + 63u) & ~63u;  // the vals after the cells stay 8-byte aligned
     CU(ctx, cudaHostAlloc(&ctx->h_patch, 16 + (size_t)ctx->patch_cap * 12, cudaHostAllocMapped));
   }
@@ -915,7 +924,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     part(0);
     for (auto& th : pool) th.join();
   }
-  if (std::getenv("LEMGPU_HOST_PROFILE")) {
+  if (ctx->host_profile) {
     const auto tq3 = clk::now();
     auto ms = [](clk::duration x) { return std::chrono::duration<double, std::milli>(x).count(); };
     std::fprintf(stderr, "step_host_banded: enqueue %.3f ms, then d2h done %.3f ms, sync %.3f ms, patch of %u cells %.3f ms\n",
@@ -958,13 +967,18 @@ uint32_t lemgpu_abi_version(void) { return LEMGPU_ABI_VERSION; }
 
 int lemgpu_create(int device, uint32_t width, uint32_t height, const lemgpu_params* params,
                   lemgpu_ctx** out) {
-  return create_impl(device, width, height, 1, params, nullptr, out);
+  return create_impl(device, width, height, 1, params, nullptr, nullptr, out);
 }
 
 int lemgpu_create_ensemble(int device, uint32_t width, uint32_t height, uint32_t members,
                            const lemgpu_params* params, const lemgpu_member* per_member,
                            lemgpu_ctx** out) {
-  return create_impl(device, width, height, members, params, per_member, out);
+  return create_impl(device, width, height, members, params, per_member, nullptr, out);
+}
+
+int lemgpu_create_ex(int device, uint32_t width, uint32_t height, uint32_t members, const lemgpu_params* params,
+                     const lemgpu_member* per_member, const lemgpu_options* options, lemgpu_ctx** out) {
+  return create_impl(device, width, height, members, params, per_member, options, out);
 }
 
 void lemgpu_destroy(lemgpu_ctx* ctx) {

@@ -237,23 +237,54 @@ class StepDiagnostics:
 
 
 # ------------------------------------------------------------- device ctx
+# lemgpu_options knobs under the names DESIGN.md's knob table uses
+_KNOB_NAMES = {
+    "LEMGPU_PATH": ("global_path", lambda v: 1 if str(v) == "global" else 0),
+    "LEMGPU_FORCE_ESCAPE": ("force_escape", int), "LEMGPU_FORCE_DEEP": ("force_deep", int),
+    "LEMGPU_EAGER": ("eager", int), "LEMGPU_NO_TMA": ("no_tma", int), "LEMGPU_NO_NARROW": ("no_narrow", int),
+    "LEMGPU_ESC_SMALL": ("no_esc_small", lambda v: 0 if int(v) else 1),
+    "LEMGPU_PIPE": ("pipe", lambda v: int(v) if int(v) > 0 else -1),
+    "LEMGPU_PIPE_CHAIN": ("pipe_unchained", lambda v: 0 if int(v) else 1),
+    "LEMGPU_TILE_GRID": ("tile_grid", int), "LEMGPU_ESC_GRID": ("esc_grid", int),
+    "LEMGPU_ESC_SMALL_GRID": ("esc_small_grid", int), "LEMGPU_PIPE_TILE_GRID": ("pipe_tile_grid", int),
+    "LEMGPU_LUT_ENTRIES": ("lut_entries", int), "LEMGPU_HOST_BANDS": ("host_bands", int),
+    "LEMGPU_PATCH_CAP": ("patch_cap", int), "LEMGPU_HOST_PROFILE": ("host_profile", int),
+}
+
+
+def make_options(options) -> Optional[_abi.lemgpu_options]:
+    """lemgpu_options from a dict of field names (or DESIGN.md knob names)."""
+    if not options:
+        return None
+    o = _abi.lemgpu_options()
+    for k, v in options.items():
+        if k in _KNOB_NAMES:
+            k, conv = _KNOB_NAMES[k]
+            v = conv(v)
+        setattr(o, k, int(v))
+    return o
+
+
 class DeviceContext:
-    """Owner of one ``lemgpu_ctx`` (device buffers + stream)."""
+    """Owner of one ``lemgpu_ctx`` (device buffers + stream).  ``options``:
+    schedule / test knobs (lemgpu_options fields or DESIGN.md knob names)."""
 
     def __init__(self, width: int, height: int, params: SimParams, connectivity: int = 8,
-                 device: int = 0, members: int = 1, per_member=None):
+                 device: int = 0, members: int = 1, per_member=None, options=None):
         L = _abi.lib()
         self.width, self.height, self.members = int(width), int(height), int(members)
         self.connectivity = connectivity
         p = params.to_abi(connectivity)
         h = C.c_void_p()
-        if members == 1 and per_member is None:
+        opts = make_options(options)
+        if members == 1 and per_member is None and opts is None:
             rc = L.lemgpu_create(device, self.width, self.height, C.byref(p), C.byref(h))
         else:
             arr = None
             if per_member is not None:
                 arr = (_abi.lemgpu_member * members)(*[_abi.lemgpu_member(float(k), float(m)) for k, m in per_member])
-            rc = L.lemgpu_create_ensemble(device, self.width, self.height, self.members, C.byref(p), arr, C.byref(h))
+            rc = L.lemgpu_create_ex(device, self.width, self.height, self.members, C.byref(p), arr,
+                                    C.byref(opts) if opts is not None else None, C.byref(h))
         if rc != _abi.OK:
             _raise(rc, L.lemgpu_error_message(None).decode())
         self._h = h

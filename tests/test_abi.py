@@ -48,15 +48,18 @@ def test_struct_layouts_match_header():
     #include <stdio.h>
     #include <stddef.h>
     #include "lemgpu.h"
-    int main(void){ printf("%zu %zu %zu %zu %zu\n", sizeof(lemgpu_params), sizeof(lemgpu_diag),
-        sizeof(lemgpu_member), offsetof(lemgpu_diag, newton_iters), offsetof(lemgpu_params, connectivity)); return 0; }
+    int main(void){ printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(lemgpu_params), sizeof(lemgpu_diag),
+        sizeof(lemgpu_member), offsetof(lemgpu_diag, newton_iters), offsetof(lemgpu_params, connectivity),
+        sizeof(lemgpu_options), offsetof(lemgpu_diag, kernel_s), offsetof(lemgpu_options, host_profile)); return 0; }
     """
     exe = Path("/tmp/lemgpu_layout")
     subprocess.run(["gcc", "-x", "c", "-I", str(ROOT / "include"), "-o", str(exe), "-"], input=src, text=True,
                    check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     assert got == [C.sizeof(_abi.lemgpu_params), C.sizeof(_abi.lemgpu_diag), C.sizeof(_abi.lemgpu_member),
-                   _abi.lemgpu_diag.newton_iters.offset, _abi.lemgpu_params.connectivity.offset]
+                   _abi.lemgpu_diag.newton_iters.offset, _abi.lemgpu_params.connectivity.offset,
+                   C.sizeof(_abi.lemgpu_options), _abi.lemgpu_diag.kernel_s.offset,
+                   _abi.lemgpu_options.host_profile.offset]
 
 
 @pytest.mark.parametrize("field,value,msg", [

@@ -21,8 +21,8 @@ def sim_params(**kw):
     return lem.SimParams(**kw)
 
 
-def device_ctx(w, h, conn=8, **kw):
-    return lem.DeviceContext(w, h, sim_params(**kw), conn)
+def device_ctx(w, h, conn=8, options=None, **kw):
+    return lem.DeviceContext(w, h, sim_params(**kw), conn, options=options)
 
 
 def compare_step(ctx, oracle_out, h_gpu, h_orc, exact_h=True, tag=""):
@@ -329,9 +329,7 @@ def test_cpp_dropin_through_reference_api():
 def test_per_level_sweeps_match_chunked(oracle, monkeypatch, w, h, seed, kw):
     """The deep-plan schedule (one kernel per level, global scratch) forced on a
     shallow plan gives the same bits as the chunked schedule and the oracle."""
-    monkeypatch.setenv("LEMGPU_FORCE_DEEP", "1")
-    deep = device_ctx(w, h, **kw)
-    monkeypatch.delenv("LEMGPU_FORCE_DEEP")
+    deep = device_ctx(w, h, options={"force_deep": 1}, **kw)
     chunked = device_ctx(w, h, **kw)
     e = oracle.terrain(w, h, seed)
     deep.upload(e)
@@ -369,11 +367,7 @@ def test_schedules_agree_with_oracle(oracle, monkeypatch, env, w, h, seed, kw, t
     k_esc_small's shared memory when they fit, <= 6144 cells and <= 256 levels,
     else -- or with LEMGPU_ESC_SMALL=0 -- in the cooperative kernels), the
     global path alone, and its per-level sweeps -- gives the oracle's bits."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    ctx = device_ctx(w, h, **kw)
-    for k in env:
-        monkeypatch.delenv(k)
+    ctx = device_ctx(w, h, options=env, **kw)
     e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
     ctx.upload(e)
     p = make_params(**kw)
@@ -404,10 +398,7 @@ def test_deep_plan_1000(oracle, monkeypatch, narrow):
     escape path runs its cooperative level expansion and deep sweeps (runs of
     narrow levels on one CTA, or -- LEMGPU_NO_NARROW -- every level grid-wide)."""
     e = _ramp(1000, 1000, 5)
-    if not narrow:
-        monkeypatch.setenv("LEMGPU_NO_NARROW", "1")
-    ctx = device_ctx(1000, 1000)
-    monkeypatch.delenv("LEMGPU_NO_NARROW", raising=False)
+    ctx = device_ctx(1000, 1000, options=None if narrow else {"no_narrow": 1})
     ctx.upload(e)
     for s in range(2):
         d = ctx.step(1)[0]
@@ -424,12 +415,8 @@ def test_inexact_cell_area(oracle, monkeypatch, env):
     """dx*dy with a full significand: the drainage area is the reference's FP
     sum in slot order (bit-exact) and pow(A, m) is evaluated on the device by
     the glibc restatement (lut misses) -- elevations bit-exact."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
     kw = {"dx": 0.1, "dy": 0.3}
-    ctx = device_ctx(100, 80, **kw)
-    for k in env:
-        monkeypatch.delenv(k)
+    ctx = device_ctx(100, 80, options=env, **kw)
     e = oracle.terrain(100, 80, 17)
     ctx.upload(e)
     p = make_params(**kw)
@@ -454,13 +441,7 @@ def test_step_host_banded(oracle, monkeypatch, env, w, h, terrain):
     raster goes up and comes down band by band, overlapped with the compute,
     and the escaped trees' cells are patched in afterwards (or, past the patch
     capacity, the whole raster comes down again) -- the oracle's bits."""
-    monkeypatch.setenv("LEMGPU_HOST_BANDS", "4")
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    ctx = device_ctx(w, h)
-    monkeypatch.delenv("LEMGPU_HOST_BANDS")
-    for k in env:
-        monkeypatch.delenv(k)
+    ctx = device_ctx(w, h, options={"LEMGPU_HOST_BANDS": 4, **env})
     e = oracle.terrain(w, h, 41) if terrain == "noise" else _ramp(w, h, 41)
     host = e.copy()
     assert _host_register(host)
@@ -551,9 +532,7 @@ def test_step_host_banded_ensemble(oracle, monkeypatch):
     """The banded host step on a stacked ensemble (bands cut across member
     boundaries): every member equals its own oracle run."""
     M, w, h = 3, 96, 70
-    monkeypatch.setenv("LEMGPU_HOST_BANDS", "5")
-    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M)
-    monkeypatch.delenv("LEMGPU_HOST_BANDS")
+    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M, options={"host_bands": 5})
     seeds = [21, 22, 23]
     host = np.stack([oracle.terrain(w, h, s) for s in seeds])
     want = [host[m].copy() for m in range(M)]
@@ -582,12 +561,8 @@ def test_random_configurations(oracle, monkeypatch, seed):
         M = int(rng.integers(1, 4))
         env = [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_TILE_GRID": "3"},
                {"LEMGPU_NO_TMA": "1"}, {"LEMGPU_ESC_SMALL": "0", "LEMGPU_FORCE_ESCAPE": "1"}][int(rng.integers(0, 6))]
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
         kw = {"n_exp": n_exp, "dx": dx}
-        ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=M)
-        for k in env:
-            monkeypatch.delenv(k)
+        ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=M, options=env)
         seeds = [int(x) for x in rng.integers(1, 10**6, size=M)]
         ctx.generate_terrain(seeds)
         es = [oracle.terrain(w, h, s) for s in seeds]

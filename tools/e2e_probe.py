@@ -42,8 +42,7 @@ print("h2d+d2h concurrent ms", round(timed(both), 2))
 del d1, d2, hq
 torch.cuda.empty_cache()
 for bands in [1, 4, 8, 16, 32, 64]:
-    os.environ["LEMGPU_HOST_BANDS"] = str(bands)
-    ctx = lem.DeviceContext(N, N, lem.SimParams(), 8)
+    ctx = lem.DeviceContext(N, N, lem.SimParams(), 8, options={"host_bands": bands})
     ctx.generate_terrain([42])
     host = hp.numpy().reshape(N, N)
     ctx.download(host)
