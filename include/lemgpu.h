@@ -211,6 +211,38 @@ int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag);
 int lemgpu_download_graph(lemgpu_ctx* ctx, uint32_t* rec, uint8_t* dnum, uint32_t* donor,
                           uint32_t* order, uint32_t* levels, uint32_t* nlevels, double* A);
 
+/* ---- ensemble ------------------------- */
+
+/* Members [first, first + count) of `members_total` owned by `rank` of
+ * `nranks`: contiguous balanced ranges, the reference's partition_sources
+ * rule (proj/src/scheduler.cpp:396-406). */
+int lemgpu_shard_members(uint32_t members_total, int nranks, int rank, uint32_t* first, uint32_t* count);
+
+/* The context of one rank of a sharded ensemble: its member range of
+ * per_member_all[members_total] (NULL: params' K and m for all), batched into
+ * one context, with the per-member statistics enabled at its table rows.  Add
+ * the communicator with lemgpu_stats_comm_init. */
+int lemgpu_create_ensemble_shard(int device, uint32_t width, uint32_t height, uint32_t members_total, int nranks,
+                                 int rank, const lemgpu_params* params, const lemgpu_member* per_member_all,
+                                 const lemgpu_options* options, lemgpu_ctx** out);
+
+/* Per-member statistics every step: table row (member_offset + m) of
+ * [members_total][4] = {mean, max, min, sum} of the elevation the step READS
+ * (the state the previous step left), computed inside the receiver pass from
+ * the h it stages anyway (no extra read of h; members shorter than 32 rows
+ * take a separate pass) in a fixed summation order (deterministic). */
+int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total);
+/* NCCL: rank 0 makes the id (ncclGetUniqueId, 128 bytes), the caller
+ * broadcasts it (torch.distributed, MPI, ...), every rank joins.  From then
+ * on each step's graph ends with ONE ncclAllReduce of the table (every row is
+ * non-zero on exactly one rank, so the SUM is an exact gather).  NCCL is
+ * loaded at run time (libnccl.so.2). */
+int lemgpu_nccl_unique_id(void* id_out, uint32_t bytes);
+int lemgpu_stats_comm_init(lemgpu_ctx* ctx, const void* id, uint32_t bytes, int nranks, int rank);
+/* The table of the last synced step (host copy) / its device address. */
+int lemgpu_stats_table(lemgpu_ctx* ctx, double* host_out);
+const double* lemgpu_stats_table_device(const lemgpu_ctx* ctx);
+
 /* Per-member statistics of the current elevation: out[4*m + {0,1,2,3}] =
  * {mean h, max h, min h, sum h}.  Deterministic (fixed reduction order).
  * `device_out` is a DEVICE pointer written on the context's stream. */

@@ -94,6 +94,17 @@ _SIGS = {
     "lemgpu_step_host": (C.c_int, [_P, _P, C.POINTER(lemgpu_diag)]),
     "lemgpu_download_graph": (C.c_int, [_P, _P, _P, _P, _P, _P, C.POINTER(C.c_uint32), _P]),
     "lemgpu_member_stats_device": (C.c_int, [_P, _P]),
+    "lemgpu_shard_members": (C.c_int, [C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "lemgpu_create_ensemble_shard": (
+        C.c_int,
+        [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(lemgpu_params),
+         C.POINTER(lemgpu_member), C.POINTER(lemgpu_options), C.POINTER(_P)],
+    ),
+    "lemgpu_stats_enable": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "lemgpu_nccl_unique_id": (C.c_int, [_P, C.c_uint32]),
+    "lemgpu_stats_comm_init": (C.c_int, [_P, _P, C.c_uint32, C.c_int, C.c_int]),
+    "lemgpu_stats_table": (C.c_int, [_P, _P]),
+    "lemgpu_stats_table_device": (_P, [_P]),
     "lemgpu_error_message": (C.c_char_p, [_P]),
     "lemgpu_error_cell": (C.c_uint32, [_P]),
     "lemgpu_num_cells": (C.c_uint64, [_P]),

@@ -104,6 +104,80 @@ __global__ void k_stats_partial(const double* h, uint32_t MN, uint32_t chunks, d
   }
 }
 
+// Per-member fold of the receiver pass's block partials (stats_block), in a
+// fixed order: table row st_member0 + m = {mean, max, min, sum}.  One CTA per
+// local member.
+__global__ void __launch_bounds__(kTPB) k_stats_reduce(StepArgs a) {
+  if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  const uint32_t m = blockIdx.x, H = a.H;
+  const uint32_t by0 = (m * H) / kBY, by1 = ((m + 1) * H - 1) / kBY;
+  double su = 0.0, mx = -INFINITY, mn = INFINITY;
+  for (uint32_t by = by0; by <= by1; ++by) {
+    const uint32_t sl = (by * kBY) / H == m ? 0u : 1u;  // slot of member m in this block row
+    for (uint32_t bx = threadIdx.x; bx < a.st_nbx; bx += kTPB) {
+      const double* p = a.st_part + ((size_t)by * a.st_nbx + bx) * 6 + 3 * sl;
+      su = __dadd_rn(su, p[0]);
+      mx = fmax(mx, p[1]);
+      mn = fmin(mn, p[2]);
+    }
+  }
+  __shared__ double ss[kTPB], sx[kTPB], sn[kTPB];
+  ss[threadIdx.x] = su;
+  sx[threadIdx.x] = mx;
+  sn[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = kTPB / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      ss[threadIdx.x] = __dadd_rn(ss[threadIdx.x], ss[threadIdx.x + o]);
+      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + o]);
+      sn[threadIdx.x] = fmin(sn[threadIdx.x], sn[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = a.st_table + (size_t)(a.st_member0 + m) * 4;
+    o[0] = __ddiv_rn(ss[0], (double)a.MN);
+    o[1] = sx[0];
+    o[2] = sn[0];
+    o[3] = ss[0];
+  }
+}
+
+// The same table from a separate pass over the h the step reads, for rasters
+// whose members are shorter than a receiver block (H < kBY).  One CTA per member.
+__global__ void __launch_bounds__(kTPB) k_stats_whole(StepArgs a) {
+  if (ld_volatile_u32(&a.ctl->err_flag)) return;
+  const uint32_t m = blockIdx.x;
+  const double* hm = a.h + (size_t)m * a.MN;
+  double su = 0.0, mx = -INFINITY, mn = INFINITY;
+  for (uint32_t i = threadIdx.x; i < a.MN; i += kTPB) {
+    const double v = hm[i];
+    su = __dadd_rn(su, v);
+    mx = fmax(mx, v);
+    mn = fmin(mn, v);
+  }
+  __shared__ double ss[kTPB], sx[kTPB], sn[kTPB];
+  ss[threadIdx.x] = su;
+  sx[threadIdx.x] = mx;
+  sn[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = kTPB / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      ss[threadIdx.x] = __dadd_rn(ss[threadIdx.x], ss[threadIdx.x + o]);
+      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + o]);
+      sn[threadIdx.x] = fmin(sn[threadIdx.x], sn[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = a.st_table + (size_t)(a.st_member0 + m) * 4;
+    o[0] = __ddiv_rn(ss[0], (double)a.MN);
+    o[1] = sx[0];
+    o[2] = sn[0];
+    o[3] = ss[0];
+  }
+}
+
 __global__ void k_stats_final(const double* part, uint32_t M, uint32_t chunks, uint32_t MN, double* out) {
   for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
     double sum = 0.0, mx = -INFINITY, mn = INFINITY;

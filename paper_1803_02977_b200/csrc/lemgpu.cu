@@ -9,6 +9,8 @@
 // the host libm to be bit-identical with the reference: the stencil
 // distances (neighborhood.hpp:17-23), pow(dist, n) and the pow(A, m) table.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -62,6 +64,14 @@ struct lemgpu_ctx {
   int pow_variant = -1;              // host_pow_variant(): the glibc pow the device reproduces
   uint32_t pipe_bands = 0;           // bands of the pipelined graph (0: not pipelined)
   uint32_t opt_patch_cap = 0;        // lemgpu_options::patch_cap
+  // ensemble statistics (lemgpu_stats_enable) and their NCCL all-reduce
+  double* st_part = nullptr;   // receiver-block partials
+  double* st_local = nullptr;  // [members_total][4]: this rank's rows, zeros elsewhere (all-reduce input)
+  double* st_all = nullptr;    // [members_total][4]: every member (all-reduce output; == st_local without a comm)
+  uint32_t st_total = 0, st_member0 = 0;
+  bool st_on = false;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
   bool host_profile = false;         // lemgpu_options::host_profile
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -251,6 +261,80 @@ int add_kernel_deps(lemgpu_ctx* ctx, cudaGraph_t g, const std::vector<cudaGraphN
   return 0;
 }
 
+// NCCL, loaded on first use (dlopen): the library itself does not depend on
+// it, and a process that already holds torch's libnccl.so.2 shares that copy.
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (tried) return ok;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    allReduce = reinterpret_cast<decltype(allReduce)>(dlsym(h, "ncclAllReduce"));
+    commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    errStr = reinterpret_cast<decltype(errStr)>(dlsym(h, "ncclGetErrorString"));
+    ok = getUniqueId && commInitRank && allReduce && commDestroy && errStr;
+    if (!ok) why = "libnccl.so.2 lacks a needed symbol";
+    return ok;
+  }
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  return api;
+}
+
+// The statistics nodes of a step: the per-member fold of the receiver pass's
+// partials (or, for short members, a separate pass), then ONE all-reduce of
+// the whole table over NCCL (SUM: every member's row is non-zero on exactly
+// one rank, so the sum is an exact copy), captured into the step graph.
+int add_stats_nodes(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, StepArgs* a) {
+  const void* fn = a->st_part ? (const void*)k_stats_reduce : (const void*)k_stats_whole;
+  int rc = add_kernel(ctx, g, prev, fn, dim3(a->M), dim3(kTPB), 0, a, nullptr);
+  if (rc || !ctx->comm) return rc;
+  cudaStream_t cs;
+  CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t child = nullptr;
+  CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const ncclResult_t nr = nccl().allReduce(ctx->st_local, ctx->st_all, (size_t)ctx->st_total * 4, ncclDouble, ncclSum,
+                                           ctx->comm, cs);
+  const cudaError_t ce = cudaStreamEndCapture(cs, &child);
+  cudaStreamDestroy(cs);
+  if (nr != ncclSuccess) return fail(ctx, LEMGPU_ECUDA, "ncclAllReduce capture: %s", nccl().errStr(nr));
+  if (ce != cudaSuccess) return fail(ctx, LEMGPU_ECUDA, "stream capture: %s", cudaGetErrorString(ce));
+  cudaGraphNode_t n;
+  CU(ctx, cudaGraphAddChildGraphNode(&n, g, prev, 1, child));
+  cudaGraphDestroy(child);
+  *prev = n;
+  return 0;
+}
+
+// Eager form of add_stats_nodes (eager steps, banded host steps).
+int enqueue_stats(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
+  if (!ctx->st_on) return 0;
+  if (a.st_part)
+    k_stats_reduce<<<a.M, kTPB, 0, st>>>(a);
+  else
+    k_stats_whole<<<a.M, kTPB, 0, st>>>(a);
+  if (ctx->comm) {
+    const ncclResult_t nr = nccl().allReduce(ctx->st_local, ctx->st_all, (size_t)ctx->st_total * 4, ncclDouble,
+                                             ncclSum, ctx->comm, st);
+    if (nr != ncclSuccess) return fail(ctx, LEMGPU_ECUDA, "ncclAllReduce: %s", nccl().errStr(nr));
+  }
+  return 0;
+}
+
 int add_while(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, cudaGraphConditionalHandle h,
               const void* fn, dim3 grid, size_t smem, StepArgs* sa) {
   cudaGraphNodeParams cp{};
@@ -386,9 +470,24 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
         (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
         (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0, &a)) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)))) ||
+      (ctx->st_on && (rc = add_stats_nodes(ctx, g, &prev, &a))) ||
       (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0, &a, nullptr)))
     return rc;
   CU(ctx, cudaGraphInstantiate(&ctx->exec[p], g, 0));
+  return 0;
+}
+
+// StepArgs is captured by value in the graph nodes: rebuild both step graphs
+// after a change of the context's configuration.
+int rebuild_graphs(lemgpu_ctx* ctx) {
+  for (uint32_t p = 0; p < 2; ++p) {
+    if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
+    if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
+    ctx->exec[p] = nullptr;
+    ctx->graph[p] = nullptr;
+    const int rc = build_graph(ctx, p);
+    if (rc) return rc;
+  }
   return 0;
 }
 
@@ -756,6 +855,7 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     const int rc = run_levels_eager(ctx, a);
     if (rc) return rc;
   }
+  if (const int rcs = enqueue_stats(ctx, a, st)) return rcs;
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
   return LEMGPU_OK;
@@ -885,6 +985,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
                                                  reinterpret_cast<double*>(hp + 16 + (size_t)ctx->patch_cap * 4),
                                                  reinterpret_cast<uint32_t*>(hp), ctx->patch_cap);
   }
+  if ((rc = enqueue_stats(ctx, a, st))) return rc;
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
   if (tev) CU(ctx, cudaEventRecord(tev[1], st));
@@ -993,6 +1094,9 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
     if (p) cudaFree(p);
   if (a.dbg_level) cudaFree(a.dbg_level);
   if (a.dbg_A) cudaFree(a.dbg_A);
+  if (ctx->st_local) cudaFree(ctx->st_local);
+  if (ctx->st_part) cudaFree(ctx->st_part);
+  if (ctx->comm) nccl().commDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   for (int p = 0; p < 2; ++p) {
     if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
@@ -1399,19 +1503,117 @@ int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable) {
   } else {
     return LEMGPU_OK;
   }
-  for (uint32_t p = 0; p < 2; ++p) {  // StepArgs is captured by value in the graph nodes
-    if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
-    if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
-    ctx->exec[p] = nullptr;
-    ctx->graph[p] = nullptr;
-    const int rc = build_graph(ctx, p);
-    if (rc) return rc;
-  }
+  if (const int rc = rebuild_graphs(ctx)) return rc;
   if (a.dbg_level) {
     CU(ctx, cudaMemset(a.dbg_level, 0xFF, a.N));
     CU(ctx, cudaMemset(a.dbg_A, 0xFF, (size_t)a.N * sizeof(double)));
   }
   return LEMGPU_OK;
+}
+
+int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  StepArgs& a = ctx->a;
+  if (members_total < member_offset + a.M)
+    return fail(ctx, LEMGPU_ECONFIG, "members_total %u < member_offset %u + %u local members", members_total,
+                member_offset, a.M);
+  if (ctx->st_on) return fail(ctx, LEMGPU_ECONFIG, "statistics already enabled");
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  const size_t tb = (size_t)members_total * 4 * sizeof(double);
+  CU(ctx, cudaMalloc(&ctx->st_local, 2 * tb));
+  CU(ctx, cudaMemset(ctx->st_local, 0, 2 * tb));
+  ctx->st_all = ctx->st_local;  // no communicator: the local table is the table
+  ctx->st_total = members_total;
+  ctx->st_member0 = member_offset;
+  if (a.H >= (uint32_t)kBY) {  // fused into the receiver pass
+    const uint32_t nbx = (a.W + kBX - 1) / kBX, nby = (a.Htot + kBY - 1) / kBY;
+    CU(ctx, cudaMalloc(&ctx->st_part, (size_t)nbx * nby * 6 * sizeof(double)));
+    a.st_part = ctx->st_part;
+    a.st_nbx = nbx;
+  }
+  a.st_table = ctx->st_local;
+  a.st_member0 = member_offset;
+  ctx->st_on = true;
+  return rebuild_graphs(ctx);
+}
+
+int lemgpu_nccl_unique_id(void* id_out, uint32_t bytes) {
+  if (!id_out || bytes < sizeof(ncclUniqueId)) return LEMGPU_ECONFIG;
+  if (!nccl().load()) return fail(nullptr, LEMGPU_EOTHER, "%s", nccl().why.c_str());
+  ncclUniqueId id;
+  const ncclResult_t r = nccl().getUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, LEMGPU_ECUDA, "ncclGetUniqueId: %s", nccl().errStr(r));
+  std::memcpy(id_out, &id, sizeof id);
+  return LEMGPU_OK;
+}
+
+int lemgpu_stats_comm_init(lemgpu_ctx* ctx, const void* id, uint32_t bytes, int nranks, int rank) {
+  if (!ctx || !id || bytes < sizeof(ncclUniqueId) || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(ctx, LEMGPU_ECONFIG, "bad communicator arguments");
+  if (!ctx->st_on) return fail(ctx, LEMGPU_ECONFIG, "enable the statistics first (lemgpu_stats_enable)");
+  if (ctx->comm) return fail(ctx, LEMGPU_ECONFIG, "communicator already set");
+  if (!nccl().load()) return fail(ctx, LEMGPU_EOTHER, "%s", nccl().why.c_str());
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = nccl().commInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return fail(ctx, LEMGPU_ECUDA, "ncclCommInitRank: %s", nccl().errStr(r));
+  ctx->comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->st_all = ctx->st_local + (size_t)ctx->st_total * 4;  // out-of-place all-reduce
+  return rebuild_graphs(ctx);
+}
+
+int lemgpu_stats_table(lemgpu_ctx* ctx, double* host_out) {
+  if (!ctx || !host_out) return LEMGPU_ECONFIG;
+  if (!ctx->st_on) return fail(ctx, LEMGPU_ECONFIG, "statistics are not enabled");
+  CU(ctx, cudaSetDevice(ctx->device));
+  CU(ctx, cudaMemcpyAsync(host_out, ctx->st_all, (size_t)ctx->st_total * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  return LEMGPU_OK;
+}
+
+const double* lemgpu_stats_table_device(const lemgpu_ctx* ctx) { return ctx && ctx->st_on ? ctx->st_all : nullptr; }
+
+int lemgpu_shard_members(uint32_t members_total, int nranks, int rank, uint32_t* first, uint32_t* count) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !first || !count) return LEMGPU_ECONFIG;
+  // partition_sources (scheduler.cpp:396-406): bounds[w] = total * w / workers
+  const uint64_t b0 = (uint64_t)members_total * (uint64_t)rank / (uint64_t)nranks;
+  const uint64_t b1 = (uint64_t)members_total * (uint64_t)(rank + 1) / (uint64_t)nranks;
+  *first = (uint32_t)b0;
+  *count = (uint32_t)(b1 - b0);
+  return LEMGPU_OK;
+}
+
+int lemgpu_create_ensemble_shard(int device, uint32_t width, uint32_t height, uint32_t members_total, int nranks,
+                                 int rank, const lemgpu_params* params, const lemgpu_member* per_member_all,
+                                 const lemgpu_options* options, lemgpu_ctx** out) {
+  if (!out) return LEMGPU_ECONFIG;
+  *out = nullptr;
+  uint32_t first = 0, count = 0;
+  if (lemgpu_shard_members(members_total, nranks, rank, &first, &count) != LEMGPU_OK || count == 0)
+    return fail(nullptr, LEMGPU_ECONFIG, "rank %d of %d owns no member of %u", rank, nranks, members_total);
+  const int rc = create_impl(device, width, height, count, params, per_member_all ? per_member_all + first : nullptr,
+                             options, out);
+  if (rc) return rc;
+  const int rs = lemgpu_stats_enable(*out, first, members_total);
+  if (rs) {
+    g_create_error = (*out)->msg;
+    lemgpu_destroy(*out);
+    *out = nullptr;
+  }
+  return rs;
 }
 
 int lemgpu_pow_variant(const lemgpu_ctx* ctx) { return ctx ? ctx->pow_variant : host_pow_variant(); }

@@ -33,6 +33,74 @@ def member_params(i: int) -> Tuple[int, float, float]:
     return 1000 + i, 1e-6 * (1 + i % 8), 0.35 + 0.05 * (i // 8)
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (libnccl.so.2 loaded at run time)."""
+    import ctypes as C
+
+    from . import _abi
+
+    buf = C.create_string_buffer(128)
+    rc = _abi.lib().lemgpu_nccl_unique_id(buf, 128)
+    if rc != 0:
+        raise RuntimeError(_abi.lib().lemgpu_error_message(None).decode())
+    return buf.raw
+
+
+class DeviceEnsemble:
+    """One rank's shard of an ensemble of ``members`` realisations (configs[4]):
+    its member range (the reference's partition rule), batched into ONE device
+    context (lemgpu_create_ensemble_shard), with the per-member statistics
+    computed inside every step and -- for world > 1 -- all-reduced by ONE
+    ncclAllReduce captured in the step's CUDA graph.  torch.distributed is
+    only the rendezvous that carries the NCCL id; the per-step data path is
+    C++/CUDA/NCCL on the context's stream."""
+
+    def __init__(self, width: int, height: int, members: int, params=None, member_fn=member_params,
+                 device: int = 0, rank: int = 0, world: int = 1, options=None, group=None):
+        import ctypes as C
+
+        from . import _abi
+        from .lem import DeviceContext, SimParams, make_options
+
+        params = params or SimParams()
+        self.members, self.rank, self.world = int(members), int(rank), int(world)
+        self.ids = member_ids(self.members, self.world, self.rank)
+        table = [member_fn(i) for i in range(self.members)]
+        self.seeds = [t[0] for t in table]
+        L = _abi.lib()
+        arr = (_abi.lemgpu_member * self.members)(*[_abi.lemgpu_member(float(t[1]), float(t[2])) for t in table])
+        p = params.to_abi(8)
+        opts = make_options(options)
+        h = C.c_void_p()
+        rc = L.lemgpu_create_ensemble_shard(device, int(width), int(height), self.members, self.world, self.rank,
+                                            C.byref(p), arr, C.byref(opts) if opts is not None else None, C.byref(h))
+        if rc != _abi.OK:
+            raise RuntimeError(L.lemgpu_error_message(None).decode())
+        # wrap the raw handle in a DeviceContext (same ownership rules)
+        ctx = DeviceContext.__new__(DeviceContext)
+        ctx.width, ctx.height, ctx.members, ctx.connectivity = int(width), int(height), len(self.ids), 8
+        ctx._h, ctx._L = h, L
+        ctx.n = ctx.width * ctx.height * ctx.members
+        ctx.stats_total = self.members
+        self.ctx = ctx
+        if self.world > 1:
+            import torch.distributed as dist
+
+            obj = [nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctx.stats_comm_init(obj[0], self.world, self.rank)
+
+    def generate_terrain(self):
+        self.ctx.generate_terrain([self.seeds[i] for i in self.ids])
+
+    def table(self) -> np.ndarray:
+        """[members, 4] {mean, max, min, sum} of h as the last step read it (all ranks' members)."""
+        return self.ctx.stats_table()
+
+    def close(self):
+        self.ctx.close()
+
+
 def reduce_member_stats(local, ids: List[int], members: int, group=None):
     """Assemble the [members, 4] table {mean, max, min, sum} of h on every rank.
 

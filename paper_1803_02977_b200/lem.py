@@ -399,6 +399,24 @@ class DeviceContext:
         return {"step": ms[0], "recv_donor": ms[1], "order": ms[2], "physics": ms[3], "tiles": ms[4],
                 "launches": n.value}
 
+    # ---- ensemble statistics
+    def stats_enable(self, member_offset: int = 0, members_total: Optional[int] = None):
+        """Per-step {mean, max, min, sum} of every member's elevation (the state each
+        step reads), fused into the receiver pass; rows member_offset.. of a
+        [members_total, 4] table."""
+        total = self.members if members_total is None else int(members_total)
+        self._check(self._L.lemgpu_stats_enable(self._h, int(member_offset), total))
+        self.stats_total = total
+
+    def stats_comm_init(self, nccl_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        self._check(self._L.lemgpu_stats_comm_init(self._h, buf, len(nccl_id), int(nranks), int(rank)))
+
+    def stats_table(self) -> np.ndarray:
+        out = np.empty((self.stats_total, 4), np.float64)
+        self._check(self._L.lemgpu_stats_table(self._h, out.ctypes.data))
+        return out
+
     def tile_capture(self, enable: bool = True):
         """Debug: make every step's tile pass record each finished cell's level and
         drainage area (lemgpu_debug_tile_capture); read them with tile_levels()."""

@@ -57,3 +57,21 @@ def test_stats_allreduce_gloo_world2(M):
     mp.spawn(_worker, args=(world, _free_port(), M, out), nprocs=world, join=True)
     assert sorted(out.keys()) == [0, 1]
     assert all(v == 0.0 for v in out.values())
+
+
+def test_shard_members_c_abi_matches_python_rule():
+    """lemgpu_shard_members (the C-ABI the product ensemble entry uses) and the
+    Python rule agree for every (members, world, rank)."""
+    import ctypes as C
+
+    from paper_1803_02977_b200 import _abi
+
+    L = _abi.lib()
+    for M in (1, 5, 64, 100):
+        for world in (1, 2, 3, 4, 8):
+            for rank in range(world):
+                f, c = C.c_uint32(), C.c_uint32()
+                assert L.lemgpu_shard_members(M, world, rank, C.byref(f), C.byref(c)) == 0
+                ids = ensemble.member_ids(M, world, rank)
+                assert (f.value, c.value) == ((ids[0] if ids else f.value), len(ids))
+    assert L.lemgpu_shard_members(4, 2, 2, C.byref(C.c_uint32()), C.byref(C.c_uint32())) != 0
