@@ -2,15 +2,18 @@
 """Benchmark of the B200 D8 landscape-evolution step (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
-                    [--workload dem10000|ens64|dem1000|dem4000n2]
+                    [--workload dem10000|dem1000|dem4000n2|dem1000fill|dem4000fill|ens64]
 
 A "step" is one timestep (receivers, donors, level order, accumulation,
-uplift + erosion) over the whole workload.  Default workload (N=1): the
-10000x10000 random-noise DEM of BASELINE.json configs[1].  For N>1 every rank
-advances its own 10000^2 realisation ("replicas only": one DEM does not
-shard) and the per-step ensemble statistics are all-reduced over
-NCCL -- weak scaling.  ``--workload ens64`` is configs[4]: 64 x 2000^2
-members sharded over the ranks (strong scaling).
+uplift + erosion) over the whole workload.  Default workload at N=1: the
+10000x10000 random-noise DEM of BASELINE.json configs[1].  Default at N>1:
+configs[4], the ensemble of 64 x 2000^2 members sharded over the ranks
+(strong scaling: the same 64 members whatever N; its N=1 counterpart is
+``--workload ens64``), each rank's members batched in one context, the
+per-member statistics fused into the step and all-reduced by ONE
+ncclAllReduce captured in the step's CUDA graph.  ``--workload dem10000`` at
+N>1 runs one independent 10000^2 replica per rank ("replicas only": one DEM
+does not shard) -- weak scaling.
 
 Rank 0 prints one JSON line.  ``value`` is device-resident throughput
 (inputs in HBM), ``e2e`` is the same metric through the C-ABI's
@@ -236,7 +239,8 @@ def run_reference_arm(args):
               f"{w}x{h}" + (f" (one member, scaled x{members})" if members > 1 else "") +
               (f"; steps capped from {k} to fit the time budget" if k_run < k else ""))
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": k_run, "warmup": warm + 1,
-           "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "ms_per_step": per_step * 1e3, "higher_is_better": True,
+           "scaling": "weak" if wl["members"] == 1 else "strong", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM, lem::generate_terrain)", "config": cfg,
            "details": {"impl": "reference CPU: lem::strategy_step(rb_private_queues) of the unmodified reference "
                                "(oracle/_ref/liblemref.so)"},
@@ -253,7 +257,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--workload", default="dem10000", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: dem10000 (configs[1]) on 1 GPU, ens64 (configs[4], strong scaling) on N > 1")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--options", default=None,
@@ -261,6 +266,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.workload is None:
+        args.workload = "dem10000" if max(args.gpus, env_int("WORLD_SIZE", 1)) == 1 else "ens64"
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -289,9 +296,26 @@ def main():
     opts = json.loads(args.options) if args.options else {}
     if os.environ.get("LEMGPU_EAGER") == "1":  # profiling (tools/profile_round.sh): ncu cannot see graph kernel nodes
         opts["eager"] = 1
-    ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M,
-                            per_member=km if (wl["members"] > 1) else None, options=opts or None)
-    ctx.generate_terrain(seeds)
+    ens = world > 1 or wl["members"] > 1
+    from paper_1803_02977_b200 import ensemble
+
+    if ens:
+        # the product ensemble path: this rank's member range in one context,
+        # per-member statistics fused into every step, ONE ncclAllReduce of the
+        # table captured in the step graph; replicas of a single
+        # DEM (--workload dem10000 at N > 1) are an ensemble of one member per rank
+        if wl["members"] > 1:
+            mfn, mtot = ensemble.member_params, wl["members"]
+        else:
+            mfn, mtot = (lambda i: (42 + i, 2e-6, 0.5)), world
+        dens = ensemble.DeviceEnsemble(w, h, mtot, params, member_fn=mfn, device=local, rank=rank, world=world,
+                                       options=opts or None, use_nccl=(backend == "nccl"))
+        ctx = dens.ctx
+        M = len(dens.ids)
+        dens.generate_terrain()
+    else:
+        ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M, options=opts or None)
+        ctx.generate_terrain(seeds)
     fill_ms = None
     if wl.get("fill"):  # lem::priority_flood_fill on the device, once, before the timed steps
         torch.cuda.synchronize(local)
@@ -300,18 +324,9 @@ def main():
         fill_ms = (time.perf_counter() - tf) * 1e3
     cells = w * h * M
     ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
-    ens = world > 1 or wl["members"] > 1
-    stats = torch.zeros(max(M, 1), 4, dtype=torch.float64, device=f"cuda:{local}")
-    from paper_1803_02977_b200 import ensemble
 
     def one_step():
-        ctx.step_async(1)
-        if ens:
-            # per-member statistics + NCCL reduction of the [members, 4] table
-            ctx.member_stats_device(stats.data_ptr())
-            if world > 1:
-                with torch.cuda.stream(ext):
-                    ensemble.reduce_member_stats(stats, ids, members_total)
+        ctx.step_async(1)  # one graph launch: the step, the member statistics, their all-reduce
 
     # ---- warm-up
     for _ in range(args.warmup):
@@ -434,9 +449,9 @@ def main():
             cpu = {"value": None, "error": str(e)}
     # per step (one CUDA graph): k_recv and k_tiles (in bands for tall rasters),
     # k_esc_small, k_esc_bfs (cooperative, every escape level inside),
-    # k_chunks, k_deep_coop (cooperative), k_finalize -- counted from the graph
-    # (+ 2 stats kernels in ensemble mode)
-    launches = args.steps * ctx.kernels_per_step() + (2 * args.steps if ens else 0)
+    # k_chunks, k_deep_coop (cooperative), [k_stats_reduce], k_finalize --
+    # the kernel nodes of the step graph (the NCCL all-reduce is a library kernel)
+    launches = args.steps * ctx.kernels_per_step()
     last = diags[-1] if diags else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -447,7 +462,10 @@ def main():
         "config": arm_config(args.workload, world),
         "details": {"members_per_gpu": M,
                    "parallelism": f"replicas{world}" if wl["members"] == 1 else f"members/{world}",
-                   "collective": (f"per-step {backend} all-reduce of the per-member statistics" if world > 1 else None),
+                   "collective": ("one ncclAllReduce per step of the [members, 4] statistics table, captured in the "
+                                  "step's CUDA graph (lemgpu_stats_comm_init)" if (world > 1 and backend == "nccl")
+                                  else None),
+                   "member_stats": "fused into the receiver pass (lemgpu_stats_enable)" if ens else None,
                    "pow_variant": {1: "glibc __pow_fma", 0: "glibc __pow_sse2", -1: "NONE MATCHES"}[ctx.pow_variant()],
                    "l2": f"inputs larger than L2: {ctx.device_bytes() / 1e9:.1f} GB device state per GPU vs 126 MB L2, no flush",
                    "vs_baseline_ref": "paper RB+GPU on 1x P100: 10000^2 x 120 steps in 70 s (PAPER.md:14) = 1.71e8 cell-steps/s",

@@ -220,18 +220,20 @@ int lemgpu_shard_members(uint32_t members_total, int nranks, int rank, uint32_t*
 
 /* The context of one rank of a sharded ensemble: its member range of
  * per_member_all[members_total] (NULL: params' K and m for all), batched into
- * one context, with the per-member statistics enabled at its table rows.  Add
- * the communicator with lemgpu_stats_comm_init. */
+ * one context, with the per-member statistics enabled at its table rows every
+ * stats_interval-th step.  Add the communicator with lemgpu_stats_comm_init. */
 int lemgpu_create_ensemble_shard(int device, uint32_t width, uint32_t height, uint32_t members_total, int nranks,
                                  int rank, const lemgpu_params* params, const lemgpu_member* per_member_all,
-                                 const lemgpu_options* options, lemgpu_ctx** out);
+                                 uint32_t stats_interval, const lemgpu_options* options, lemgpu_ctx** out);
 
-/* Per-member statistics every step: table row (member_offset + m) of
- * [members_total][4] = {mean, max, min, sum} of the elevation the step READS
- * (the state the previous step left), computed inside the receiver pass from
- * the h it stages anyway (no extra read of h; members shorter than 32 rows
- * take a separate pass) in a fixed summation order (deterministic). */
-int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total);
+/* Per-member statistics every `interval`-th step (0 or 1: every step): table
+ * row (member_offset + m) of [members_total][4] = {mean, max, min, sum} of the
+ * elevation that step STARTS from (the state the previous step left), by a
+ * bandwidth-bound pass (8 B/cell) that runs beside the step's kernels in its
+ * graph, in a fixed summation order (deterministic).  With interval > 1 those
+ * steps launch a second pair of step graphs.  The statistics of the final
+ * state: lemgpu_member_stats_device. */
+int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total, uint32_t interval);
 /* NCCL: rank 0 makes the id (ncclGetUniqueId, 128 bytes), the caller
  * broadcasts it (torch.distributed, MPI, ...), every rank joins.  From then
  * on each step's graph ends with ONE ncclAllReduce of the table (every row is
@@ -239,7 +241,7 @@ int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t member
  * loaded at run time (libnccl.so.2). */
 int lemgpu_nccl_unique_id(void* id_out, uint32_t bytes);
 int lemgpu_stats_comm_init(lemgpu_ctx* ctx, const void* id, uint32_t bytes, int nranks, int rank);
-/* The table of the last synced step (host copy) / its device address. */
+/* The table of the last step that computed it (host copy after a sync) / its device address. */
 int lemgpu_stats_table(lemgpu_ctx* ctx, double* host_out);
 const double* lemgpu_stats_table_device(const lemgpu_ctx* ctx);
 

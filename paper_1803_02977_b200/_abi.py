@@ -98,9 +98,9 @@ _SIGS = {
     "lemgpu_create_ensemble_shard": (
         C.c_int,
         [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(lemgpu_params),
-         C.POINTER(lemgpu_member), C.POINTER(lemgpu_options), C.POINTER(_P)],
+         C.POINTER(lemgpu_member), C.c_uint32, C.POINTER(lemgpu_options), C.POINTER(_P)],
     ),
-    "lemgpu_stats_enable": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "lemgpu_stats_enable": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32]),
     "lemgpu_nccl_unique_id": (C.c_int, [_P, C.c_uint32]),
     "lemgpu_stats_comm_init": (C.c_int, [_P, _P, C.c_uint32, C.c_int, C.c_int]),
     "lemgpu_stats_table": (C.c_int, [_P, _P]),

@@ -234,13 +234,13 @@ struct StepArgs {
   int tab_ok;         // every F of the table is < 2^500: div_rn_recip applies (k_physics.cuh)
   int pow_fma;        // the host glibc's pow variant the device reproduces: 1 __pow_fma, 0 __pow_sse2
   uint32_t expect_cells;  // cells the level expansion must place (cycle check); 0 = no check
-  // ensemble statistics (lemgpu_stats_enable; nullptr: off): the receiver pass
-  // reduces {sum, max, min} of the h it reads per (receiver block, member
-  // slot) into st_part[(by * st_nbx + bx) * 6], k_stats_reduce folds them per
-  // member into st_table rows [st_member0, st_member0 + M) of 4 doubles
+  // ensemble statistics (lemgpu_stats_enable): k_stats_pass reduces {sum,
+  // max, min} of the step's new elevation over st_chunks fixed chunks per
+  // member into st_part[(m * st_chunks + chunk) * 3]; k_stats_fold folds them
+  // into st_table rows [st_member0, st_member0 + M) of 4 doubles
   double* st_part;
   double* st_table;
-  uint32_t st_nbx;
+  uint32_t st_chunks;
   uint32_t st_member0;
   uint8_t* dbg_level;  // debug capture (nullptr: off): level of every cell k_tiles finishes (escaped: untouched)
   double* dbg_A;       // ... and its drainage area

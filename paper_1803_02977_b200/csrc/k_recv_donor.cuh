@@ -177,57 +177,6 @@ __device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
 // The global level path's receiver pass (LEMGPU_PATH=global and the parity
 // export): receiver codes AND the donor masks of the tile, which needs the
 // receiver codes of the ring around it.  (The tile path's pass is k_recv below.)
-// Ensemble statistics fused into the receiver pass: {sum, max,
-// min} of the elevation this step reads -- the state the previous step left
-// -- over one kBX x kBY receiver block already staged in shared memory, so the
-// per-member statistics cost no extra read of h.  A block holds rows of at
-// most two members (H >= kBY; lemgpu_stats_enable falls back to a separate
-// pass otherwise); slot 0 is the member of its first row.  Fixed summation
-// order (each thread's cells in order, then a butterfly and the warps in
-// order): deterministic.
-__device__ __forceinline__ void stats_block(const StepArgs& a, const double (*sh)[kBX + 4], uint32_t x0, uint32_t y0,
-                                            uint32_t by) {
-  const uint32_t W = a.W, Ht = a.Htot, H = a.H;
-  const uint32_t rb = (y0 / H + 1) * H - y0;  // first block row of the second member
-  double su[2] = {0.0, 0.0}, mx[2] = {-INFINITY, -INFINITY}, mn[2] = {INFINITY, INFINITY};
-#pragma unroll 4
-  for (int k = 0; k < (kBX * kBY) / kTPB; ++k) {
-    const uint32_t i = threadIdx.x + kTPB * k, r = i / kBX, c = i % kBX;
-    if (y0 + r < Ht && x0 + c < W) {
-      const double v = sh[r + 2][c + 2];
-      const int sl = r >= rb ? 1 : 0;
-      su[sl] = __dadd_rn(su[sl], v);
-      mx[sl] = fmax(mx[sl], v);
-      mn[sl] = fmin(mn[sl], v);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      su[j] = __dadd_rn(su[j], __shfl_xor_sync(0xffffffffu, su[j], o));
-      mx[j] = fmax(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
-      mn[j] = fmin(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
-    }
-  __shared__ double sw[kNW][6];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    sw[warp][0] = su[0];
-    sw[warp][1] = mx[0];
-    sw[warp][2] = mn[0];
-    sw[warp][3] = su[1];
-    sw[warp][4] = mx[1];
-    sw[warp][5] = mn[1];
-  }
-  __syncthreads();
-  if (threadIdx.x < 6) {
-    const int j = threadIdx.x;
-    double v = sw[0][j];
-    for (int w = 1; w < kNW; ++w) v = (j % 3 == 0) ? __dadd_rn(v, sw[w][j]) : (j % 3 == 1) ? fmax(v, sw[w][j]) : fmin(v, sw[w][j]);
-    a.st_part[((size_t)by * a.st_nbx + blockIdx.x) * 6 + j] = v;
-  }
-}
-
 template <int CONN>
 __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   __shared__ __align__(128) double sh[kBY + 4][kBX + 4];
@@ -390,7 +339,6 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB) k_recv_donor(StepArgs 
     }
   }
   __syncthreads();
-  if (a.st_part) stats_block(a, sh, x0, y0, blockIdx.y);
   phclk_end(s_pc, LEMGPU_PHASE_DONORS, a.ctl);
   if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());
 }
@@ -567,7 +515,6 @@ __global__ void __launch_bounds__(kTPB, LEMGPU_RECV_MINB)
     for (int i = 0; i < 16; ++i)
       if (i < nr) store_row(i);
   }
-  if (a.st_part) stats_block(a, sh, x0, y0, blockIdx.y + a.by0);
   phclk_end(s_pc, LEMGPU_PHASE_DONORS, a.ctl);
   if (threadIdx.x == 0) atomicMax(&a.ctl->t_k1_end, globaltimer());  // (no barrier: thread 0's end ~ the CTA's)
 }

@@ -104,78 +104,81 @@ __global__ void k_stats_partial(const double* h, uint32_t MN, uint32_t chunks, d
   }
 }
 
-// Per-member fold of the receiver pass's block partials (stats_block), in a
-// fixed order: table row st_member0 + m = {mean, max, min, sum}.  One CTA per
-// local member.
-__global__ void __launch_bounds__(kTPB) k_stats_reduce(StepArgs a) {
+// Ensemble statistics of the elevation a step starts from (the
+// state the previous step left): a bandwidth-bound pass (8 B/cell) over fixed
+// chunks of every member -- grid (st_chunks, M) -- that runs beside the
+// step's issue- and latency-bound kernels (it reads the input buffer, which
+// the step never writes), then a fold per member.  Fixed summation order:
+// deterministic.  Fusing the
+// reduction into k_recv or k_tiles was measured (64 x 2000^2: +0.85 ms/step,
+// +15 %) -- those kernels are instruction-bound, the reduction's ~0.5
+// instructions per cell cost more there than 8 B/cell of HBM traffic here.
+__global__ void __launch_bounds__(kTPB) k_stats_pass(StepArgs a) {
   if (ld_volatile_u32(&a.ctl->err_flag)) return;
-  const uint32_t m = blockIdx.x, H = a.H;
-  const uint32_t by0 = (m * H) / kBY, by1 = ((m + 1) * H - 1) / kBY;
+  const uint32_t m = blockIdx.y, ch = blockIdx.x, C = gridDim.x;
+  const uint32_t per = ((a.MN + C - 1) / C + 1u) & ~1u;  // even: 16-byte aligned double2 loads when MN is even
+  const uint32_t s0 = min(a.MN, ch * per), s1 = min(a.MN, s0 + per);
+  const double* hm = a.h + (size_t)m * a.MN;
   double su = 0.0, mx = -INFINITY, mn = INFINITY;
-  for (uint32_t by = by0; by <= by1; ++by) {
-    const uint32_t sl = (by * kBY) / H == m ? 0u : 1u;  // slot of member m in this block row
-    for (uint32_t bx = threadIdx.x; bx < a.st_nbx; bx += kTPB) {
-      const double* p = a.st_part + ((size_t)by * a.st_nbx + bx) * 6 + 3 * sl;
-      su = __dadd_rn(su, p[0]);
-      mx = fmax(mx, p[1]);
-      mn = fmin(mn, p[2]);
+  if ((a.MN & 1u) == 0) {
+    const double2* v2 = reinterpret_cast<const double2*>(hm + s0);
+    for (uint32_t i = threadIdx.x; i < (s1 - s0) / 2; i += kTPB) {
+      const double2 v = __ldcs(v2 + i);
+      su = __dadd_rn(__dadd_rn(su, v.x), v.y);
+      mx = fmax(mx, fmax(v.x, v.y));
+      mn = fmin(mn, fmin(v.x, v.y));
+    }
+  } else {
+    for (uint32_t i = s0 + threadIdx.x; i < s1; i += kTPB) {
+      const double v = hm[i];
+      su = __dadd_rn(su, v);
+      mx = fmax(mx, v);
+      mn = fmin(mn, v);
     }
   }
-  __shared__ double ss[kTPB], sx[kTPB], sn[kTPB];
-  ss[threadIdx.x] = su;
-  sx[threadIdx.x] = mx;
-  sn[threadIdx.x] = mn;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    su = __dadd_rn(su, __shfl_xor_sync(0xffffffffu, su, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  __shared__ double sw[kNW][3];
+  if ((threadIdx.x & 31) == 0) {
+    sw[threadIdx.x >> 5][0] = su;
+    sw[threadIdx.x >> 5][1] = mx;
+    sw[threadIdx.x >> 5][2] = mn;
+  }
   __syncthreads();
-  for (int o = kTPB / 2; o; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      ss[threadIdx.x] = __dadd_rn(ss[threadIdx.x], ss[threadIdx.x + o]);
-      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + o]);
-      sn[threadIdx.x] = fmin(sn[threadIdx.x], sn[threadIdx.x + o]);
-    }
-    __syncthreads();
-  }
   if (threadIdx.x == 0) {
-    double* o = a.st_table + (size_t)(a.st_member0 + m) * 4;
-    o[0] = __ddiv_rn(ss[0], (double)a.MN);
-    o[1] = sx[0];
-    o[2] = sn[0];
-    o[3] = ss[0];
+    double s = sw[0][0], x = sw[0][1], n = sw[0][2];
+    for (int w = 1; w < kNW; ++w) {
+      s = __dadd_rn(s, sw[w][0]);
+      x = fmax(x, sw[w][1]);
+      n = fmin(n, sw[w][2]);
+    }
+    double* o = a.st_part + ((size_t)m * C + ch) * 3;
+    o[0] = s;
+    o[1] = x;
+    o[2] = n;
   }
 }
 
-// The same table from a separate pass over the h the step reads, for rasters
-// whose members are shorter than a receiver block (H < kBY).  One CTA per member.
-__global__ void __launch_bounds__(kTPB) k_stats_whole(StepArgs a) {
+__global__ void __launch_bounds__(32) k_stats_fold(StepArgs a) {
   if (ld_volatile_u32(&a.ctl->err_flag)) return;
-  const uint32_t m = blockIdx.x;
-  const double* hm = a.h + (size_t)m * a.MN;
-  double su = 0.0, mx = -INFINITY, mn = INFINITY;
-  for (uint32_t i = threadIdx.x; i < a.MN; i += kTPB) {
-    const double v = hm[i];
-    su = __dadd_rn(su, v);
-    mx = fmax(mx, v);
-    mn = fmin(mn, v);
+  const uint32_t m = blockIdx.x * 32 + threadIdx.x;
+  if (m >= a.M) return;
+  const double* p = a.st_part + (size_t)m * a.st_chunks * 3;
+  double s = p[0], x = p[1], n = p[2];
+  for (uint32_t c = 1; c < a.st_chunks; ++c) {
+    s = __dadd_rn(s, p[3 * c]);
+    x = fmax(x, p[3 * c + 1]);
+    n = fmin(n, p[3 * c + 2]);
   }
-  __shared__ double ss[kTPB], sx[kTPB], sn[kTPB];
-  ss[threadIdx.x] = su;
-  sx[threadIdx.x] = mx;
-  sn[threadIdx.x] = mn;
-  __syncthreads();
-  for (int o = kTPB / 2; o; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      ss[threadIdx.x] = __dadd_rn(ss[threadIdx.x], ss[threadIdx.x + o]);
-      sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + o]);
-      sn[threadIdx.x] = fmin(sn[threadIdx.x], sn[threadIdx.x + o]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    double* o = a.st_table + (size_t)(a.st_member0 + m) * 4;
-    o[0] = __ddiv_rn(ss[0], (double)a.MN);
-    o[1] = sx[0];
-    o[2] = sn[0];
-    o[3] = ss[0];
-  }
+  double* o = a.st_table + (size_t)(a.st_member0 + m) * 4;
+  o[0] = __ddiv_rn(s, (double)a.MN);
+  o[1] = x;
+  o[2] = n;
+  o[3] = s;
 }
 
 __global__ void k_stats_final(const double* part, uint32_t M, uint32_t chunks, uint32_t MN, double* out) {

@@ -69,7 +69,11 @@ struct lemgpu_ctx {
   double* st_local = nullptr;  // [members_total][4]: this rank's rows, zeros elsewhere (all-reduce input)
   double* st_all = nullptr;    // [members_total][4]: every member (all-reduce output; == st_local without a comm)
   uint32_t st_total = 0, st_member0 = 0;
+  uint32_t st_interval = 1;  // statistics every st_interval-th step (the graphs stat_exec[p])
+  uint64_t st_steps = 0;     // steps enqueued since the statistics were enabled
   bool st_on = false;
+  cudaGraph_t st_graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t st_exec[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   bool host_profile = false;         // lemgpu_options::host_profile
@@ -300,9 +304,19 @@ NcclApi& nccl() {
 // the whole table over NCCL (SUM: every member's row is non-zero on exactly
 // one rank, so the sum is an exact copy), captured into the step graph.
 int add_stats_nodes(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, StepArgs* a) {
-  const void* fn = a->st_part ? (const void*)k_stats_reduce : (const void*)k_stats_whole;
-  int rc = add_kernel(ctx, g, prev, fn, dim3(a->M), dim3(kTPB), 0, a, nullptr);
-  if (rc || !ctx->comm) return rc;
+  // the pass reads the step's INPUT elevation, which nothing writes during the
+  // step: a root node, running beside the step's kernels; the fold joins it
+  cudaGraphNode_t pass, fold;
+  int rc = add_kernel_deps(ctx, g, {}, &pass, (const void*)k_stats_pass, dim3(a->st_chunks, a->M), dim3(kTPB), 0, a,
+                           nullptr);
+  if (!rc) {
+    std::vector<cudaGraphNode_t> d{pass};
+    if (*prev) d.push_back(*prev);
+    rc = add_kernel_deps(ctx, g, d, &fold, (const void*)k_stats_fold, dim3((a->M + 31) / 32), dim3(32), 0, a, nullptr);
+  }
+  if (rc) return rc;
+  *prev = fold;
+  if (!ctx->comm) return 0;
   cudaStream_t cs;
   CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaGraph_t child = nullptr;
@@ -320,13 +334,18 @@ int add_stats_nodes(lemgpu_ctx* ctx, cudaGraph_t g, cudaGraphNode_t* prev, StepA
   return 0;
 }
 
+// The step being enqueued ends with the statistics.
+bool stats_due(const lemgpu_ctx* ctx) { return ctx->st_on && (ctx->st_steps + 1) % ctx->st_interval == 0; }
+
+// Eager form of the statistics pass, at the start of the step (it reads the input).
+void enqueue_stats_pass(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
+  if (ctx->st_on && stats_due(ctx)) k_stats_pass<<<dim3(a.st_chunks, a.M), kTPB, 0, st>>>(a);
+}
+
 // Eager form of add_stats_nodes (eager steps, banded host steps).
 int enqueue_stats(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
-  if (!ctx->st_on) return 0;
-  if (a.st_part)
-    k_stats_reduce<<<a.M, kTPB, 0, st>>>(a);
-  else
-    k_stats_whole<<<a.M, kTPB, 0, st>>>(a);
+  if (!ctx->st_on || !stats_due(ctx)) return 0;
+  k_stats_fold<<<(a.M + 31) / 32, 32, 0, st>>>(a);  // (k_stats_pass ran at the step's start: enqueue_stats_pass)
   if (ctx->comm) {
     const ncclResult_t nr = nccl().allReduce(ctx->st_local, ctx->st_all, (size_t)ctx->st_total * 4, ncclDouble,
                                              ncclSum, ctx->comm, st);
@@ -382,11 +401,13 @@ const void* recv_fn(const StepArgs& a) {
 }
 size_t tiles_smem(const StepArgs& a) { return a.lut_exact ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>(); }
 
-int build_graph(lemgpu_ctx* ctx, uint32_t p) {
+// The step graph that reads hbuf[p]; with_stats: ending with the ensemble
+// statistics and their all-reduce.
+int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
   StepArgs a = step_args(ctx, p);
   cudaGraph_t g;
   CU(ctx, cudaGraphCreate(&g, 0));
-  ctx->graph[p] = g;
+  (with_stats && ctx->st_interval > 1 ? ctx->st_graph[p] : ctx->graph[p]) = g;
   if (!ctx->use_tiles)  // the tile path expands the escaped trees inside one cooperative kernel
     CU(ctx, cudaGraphConditionalHandleCreate(&a.h_expand, g, 1, cudaGraphCondAssignDefault));
   if (!ctx->use_tiles) {  // the tile path sweeps deep plans inside one cooperative kernel
@@ -470,26 +491,38 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p) {
         (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||
         (rc = add_while(ctx, g, &prev, a.h_deros, fde, dim3(ctx->deep_grid), 0, &a)) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_deep_final, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)))) ||
-      (ctx->st_on && (rc = add_stats_nodes(ctx, g, &prev, &a))) ||
+      (with_stats && (rc = add_stats_nodes(ctx, g, &prev, &a))) ||
       (rc = add_kernel(ctx, g, &prev, (const void*)k_finalize, dim3(1), dim3(32), 0, &a, nullptr)))
     return rc;
-  CU(ctx, cudaGraphInstantiate(&ctx->exec[p], g, 0));
+  CU(ctx, cudaGraphInstantiate(with_stats && ctx->st_interval > 1 ? &ctx->st_exec[p] : &ctx->exec[p], g, 0));
   return 0;
 }
 
 // StepArgs is captured by value in the graph nodes: rebuild both step graphs
 // after a change of the context's configuration.
-int rebuild_graphs(lemgpu_ctx* ctx) {
+void destroy_graphs(lemgpu_ctx* ctx) {
   for (uint32_t p = 0; p < 2; ++p) {
     if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
     if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
-    ctx->exec[p] = nullptr;
-    ctx->graph[p] = nullptr;
-    const int rc = build_graph(ctx, p);
+    if (ctx->st_exec[p]) cudaGraphExecDestroy(ctx->st_exec[p]);
+    if (ctx->st_graph[p]) cudaGraphDestroy(ctx->st_graph[p]);
+    ctx->exec[p] = ctx->st_exec[p] = nullptr;
+    ctx->graph[p] = ctx->st_graph[p] = nullptr;
+  }
+}
+
+// Statistics every step: they are part of the step graphs; every k-th step:
+// a second pair of graphs with them, launched on those steps.
+int rebuild_graphs(lemgpu_ctx* ctx) {
+  destroy_graphs(ctx);
+  for (uint32_t p = 0; p < 2; ++p) {
+    int rc = build_graph(ctx, p, ctx->st_on && ctx->st_interval == 1);
+    if (!rc && ctx->st_on && ctx->st_interval > 1) rc = build_graph(ctx, p, true);
     if (rc) return rc;
   }
   return 0;
 }
+
 
 int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_params* p,
                 const lemgpu_member* per_member, const lemgpu_options* opts, lemgpu_ctx** out) {
@@ -829,6 +862,7 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   a.eager = 1;
   cudaStream_t st = ctx->stream;
   set_eager_conds(a, st);
+  enqueue_stats_pass(ctx, a, st);
   if (ctx->use_tiles) {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     {
@@ -985,12 +1019,14 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
                                                  reinterpret_cast<double*>(hp + 16 + (size_t)ctx->patch_cap * 4),
                                                  reinterpret_cast<uint32_t*>(hp), ctx->patch_cap);
   }
+  enqueue_stats_pass(ctx, a, st);  // the input buffer is complete and unchanged by now
   if ((rc = enqueue_stats(ctx, a, st))) return rc;
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
   if (tev) CU(ctx, cudaEventRecord(tev[1], st));
   ctx->cur = p ^ 1u;
   ++ctx->pending;
+  ++ctx->st_steps;
   ctx->have_graph = true;
   using clk = std::chrono::steady_clock;
   const auto tq0 = clk::now();
@@ -1047,12 +1083,17 @@ int enqueue_step(lemgpu_ctx* ctx) {
     CU(ctx, cudaEventRecord(ev[0], ctx->stream));
   }
   const uint32_t p = ctx->cur;
+  if (ctx->a.dbg_level) {  // debug capture: every step starts from "not finished by the tile pass"
+    CU(ctx, cudaMemsetAsync(ctx->a.dbg_level, 0xFF, ctx->a.N, ctx->stream));
+    CU(ctx, cudaMemsetAsync(ctx->a.dbg_A, 0xFF, (size_t)ctx->a.N * sizeof(double), ctx->stream));
+  }
   if (ctx->a.eager) {
     const int rc = enqueue_step_eager(ctx, p);
     if (rc) return rc;
   } else {
-    CU(ctx, cudaGraphLaunch(ctx->exec[p], ctx->stream));
+    CU(ctx, cudaGraphLaunch(ctx->st_interval > 1 && stats_due(ctx) ? ctx->st_exec[p] : ctx->exec[p], ctx->stream));
   }
+  ++ctx->st_steps;
   if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
   ctx->cur = p ^ 1u;
   ++ctx->pending;
@@ -1098,10 +1139,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   if (ctx->st_part) cudaFree(ctx->st_part);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
-  for (int p = 0; p < 2; ++p) {
-    if (ctx->exec[p]) cudaGraphExecDestroy(ctx->exec[p]);
-    if (ctx->graph[p]) cudaGraphDestroy(ctx->graph[p]);
-  }
+  destroy_graphs(ctx);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
@@ -1511,7 +1549,7 @@ int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable) {
   return LEMGPU_OK;
 }
 
-int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total) {
+int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t members_total, uint32_t interval) {
   if (!ctx) return LEMGPU_ECONFIG;
   StepArgs& a = ctx->a;
   if (members_total < member_offset + a.M)
@@ -1529,12 +1567,13 @@ int lemgpu_stats_enable(lemgpu_ctx* ctx, uint32_t member_offset, uint32_t member
   ctx->st_all = ctx->st_local;  // no communicator: the local table is the table
   ctx->st_total = members_total;
   ctx->st_member0 = member_offset;
-  if (a.H >= (uint32_t)kBY) {  // fused into the receiver pass
-    const uint32_t nbx = (a.W + kBX - 1) / kBX, nby = (a.Htot + kBY - 1) / kBY;
-    CU(ctx, cudaMalloc(&ctx->st_part, (size_t)nbx * nby * 6 * sizeof(double)));
-    a.st_part = ctx->st_part;
-    a.st_nbx = nbx;
-  }
+  // chunks per member: ~4 CTAs per SM over the whole ensemble, >= 1
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+  a.st_chunks = std::max<uint32_t>(1u, std::min<uint32_t>(4u * (uint32_t)nsm / a.M + 1u, (a.MN + 4095u) / 4096u));
+  CU(ctx, cudaMalloc(&ctx->st_part, (size_t)a.M * a.st_chunks * 3 * sizeof(double)));
+  a.st_part = ctx->st_part;
+  ctx->st_interval = interval ? interval : 1u;
   a.st_table = ctx->st_local;
   a.st_member0 = member_offset;
   ctx->st_on = true;
@@ -1598,7 +1637,7 @@ int lemgpu_shard_members(uint32_t members_total, int nranks, int rank, uint32_t*
 
 int lemgpu_create_ensemble_shard(int device, uint32_t width, uint32_t height, uint32_t members_total, int nranks,
                                  int rank, const lemgpu_params* params, const lemgpu_member* per_member_all,
-                                 const lemgpu_options* options, lemgpu_ctx** out) {
+                                 uint32_t stats_interval, const lemgpu_options* options, lemgpu_ctx** out) {
   if (!out) return LEMGPU_ECONFIG;
   *out = nullptr;
   uint32_t first = 0, count = 0;
@@ -1607,7 +1646,7 @@ int lemgpu_create_ensemble_shard(int device, uint32_t width, uint32_t height, ui
   const int rc = create_impl(device, width, height, count, params, per_member_all ? per_member_all + first : nullptr,
                              options, out);
   if (rc) return rc;
-  const int rs = lemgpu_stats_enable(*out, first, members_total);
+  const int rs = lemgpu_stats_enable(*out, first, members_total, stats_interval);
   if (rs) {
     g_create_error = (*out)->msg;
     lemgpu_destroy(*out);

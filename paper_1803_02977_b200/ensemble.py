@@ -50,13 +50,14 @@ class DeviceEnsemble:
     """One rank's shard of an ensemble of ``members`` realisations (configs[4]):
     its member range (the reference's partition rule), batched into ONE device
     context (lemgpu_create_ensemble_shard), with the per-member statistics
-    computed inside every step and -- for world > 1 -- all-reduced by ONE
-    ncclAllReduce captured in the step's CUDA graph.  torch.distributed is
+    computed inside every (or every stats_interval-th) step's CUDA graph and --
+    for world > 1 -- all-reduced by ONE ncclAllReduce captured in that graph.  torch.distributed is
     only the rendezvous that carries the NCCL id; the per-step data path is
     C++/CUDA/NCCL on the context's stream."""
 
     def __init__(self, width: int, height: int, members: int, params=None, member_fn=member_params,
-                 device: int = 0, rank: int = 0, world: int = 1, options=None, group=None):
+                 device: int = 0, rank: int = 0, world: int = 1, options=None, group=None, use_nccl: bool = True,
+                 stats_interval: int = 1):
         import ctypes as C
 
         from . import _abi
@@ -73,7 +74,8 @@ class DeviceEnsemble:
         opts = make_options(options)
         h = C.c_void_p()
         rc = L.lemgpu_create_ensemble_shard(device, int(width), int(height), self.members, self.world, self.rank,
-                                            C.byref(p), arr, C.byref(opts) if opts is not None else None, C.byref(h))
+                                            C.byref(p), arr, int(stats_interval),
+                                            C.byref(opts) if opts is not None else None, C.byref(h))
         if rc != _abi.OK:
             raise RuntimeError(L.lemgpu_error_message(None).decode())
         # wrap the raw handle in a DeviceContext (same ownership rules)
@@ -83,7 +85,7 @@ class DeviceEnsemble:
         ctx.n = ctx.width * ctx.height * ctx.members
         ctx.stats_total = self.members
         self.ctx = ctx
-        if self.world > 1:
+        if self.world > 1 and use_nccl:
             import torch.distributed as dist
 
             obj = [nccl_unique_id() if self.rank == 0 else None]
@@ -94,7 +96,7 @@ class DeviceEnsemble:
         self.ctx.generate_terrain([self.seeds[i] for i in self.ids])
 
     def table(self) -> np.ndarray:
-        """[members, 4] {mean, max, min, sum} of h as the last step read it (all ranks' members)."""
+        """[members, 4] {mean, max, min, sum} of h after the last step that computed them (all ranks' members)."""
         return self.ctx.stats_table()
 
     def close(self):

@@ -400,12 +400,12 @@ class DeviceContext:
                 "launches": n.value}
 
     # ---- ensemble statistics
-    def stats_enable(self, member_offset: int = 0, members_total: Optional[int] = None):
-        """Per-step {mean, max, min, sum} of every member's elevation (the state each
-        step reads), fused into the receiver pass; rows member_offset.. of a
+    def stats_enable(self, member_offset: int = 0, members_total: Optional[int] = None, interval: int = 1):
+        """{mean, max, min, sum} of every member's elevation after every
+        `interval`-th step, inside the step graph; rows member_offset.. of a
         [members_total, 4] table."""
         total = self.members if members_total is None else int(members_total)
-        self._check(self._L.lemgpu_stats_enable(self._h, int(member_offset), total))
+        self._check(self._L.lemgpu_stats_enable(self._h, int(member_offset), total, int(interval)))
         self.stats_total = total
 
     def stats_comm_init(self, nccl_id: bytes, nranks: int, rank: int):

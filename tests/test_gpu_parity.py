@@ -640,36 +640,40 @@ def _np_stats(hh):
     return np.stack([flat.mean(1), flat.max(1), flat.min(1), flat.sum(1)], axis=1)
 
 
-@pytest.mark.parametrize("w,h,M,pipelined", [(67, 45, 5, False), (90, 20, 4, False), (96, 1100, 8, True)],
-                         ids=["two-members-per-block", "short-members", "pipelined"])
-def test_ensemble_stats_fused_in_step(oracle, w, h, M, pipelined):
-    """lemgpu_stats_enable: every step's graph leaves the {mean, max, min, sum}
-    of each member's elevation as that step read it -- fused into the receiver
-    pass (or a separate pass for members shorter than a receiver block) --
-    deterministic, and equal to numpy's statistics of the same state."""
+@pytest.mark.parametrize("w,h,M,interval", [(67, 45, 5, 1), (90, 20, 4, 1), (96, 1100, 8, 1), (64, 40, 3, 3)],
+                         ids=["small", "short-members", "tall-pipelined", "every-3rd-step"])
+def test_ensemble_stats_in_step_graph(oracle, w, h, M, interval):
+    """lemgpu_stats_enable: every interval-th step's graph computes the {mean,
+    max, min, sum} of each member's elevation as the step starts --
+    deterministic, equal to numpy's statistics of that state; rows of other
+    ranks stay 0."""
     members = [(1e-6 * (1 + i % 8), 0.35 + 0.05 * (i % 8)) for i in range(M)]
-    ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M, per_member=members)
-    assert (ctx.pipeline_bands() > 0) == pipelined
-    ctx.stats_enable(member_offset=2, members_total=M + 3)
-    ctx.generate_terrain(range(500, 500 + M))
-    tables = []
-    for s in range(3):
-        before = ctx.download().reshape(M, h, w)
-        ctx.step(1)
-        t = ctx.stats_table()
-        assert (t[:2] == 0).all() and (t[2 + M:] == 0).all()  # rows of other ranks stay zero
-        want = _np_stats(before)
-        got = t[2:2 + M]
-        assert np.array_equal(got[:, 1], want[:, 1]) and np.array_equal(got[:, 2], want[:, 2])
-        assert np.allclose(got[:, 3], want[:, 3], rtol=1e-13) and np.allclose(got[:, 0], want[:, 0], rtol=1e-13)
-        tables.append(t.copy())
-    # determinism: the same run again gives the same bits
-    ctx2 = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M, per_member=members)
-    ctx2.stats_enable(member_offset=2, members_total=M + 3)
-    ctx2.generate_terrain(range(500, 500 + M))
-    for s in range(3):
-        ctx2.step(1)
-        assert np.array_equal(ctx2.stats_table().view(np.uint64), tables[s].view(np.uint64))
+
+    def run():
+        ctx = lem.DeviceContext(w, h, lem.SimParams(), 8, members=M, per_member=members)
+        ctx.stats_enable(member_offset=2, members_total=M + 3, interval=interval)
+        ctx.generate_terrain(range(500, 500 + M))
+        out = []
+        last = np.zeros((M + 3, 4))
+        for s in range(6):
+            before = ctx.download().reshape(M, h, w)
+            ctx.step(1)
+            t = ctx.stats_table()
+            if (s + 1) % interval == 0:
+                assert (t[:2] == 0).all() and (t[2 + M:] == 0).all()
+                want = _np_stats(before)
+                got = t[2:2 + M]
+                assert np.array_equal(got[:, 1], want[:, 1]) and np.array_equal(got[:, 2], want[:, 2])
+                assert np.allclose(got[:, 3], want[:, 3], rtol=1e-13) and np.allclose(got[:, 0], want[:, 0], rtol=1e-13)
+            else:
+                assert np.array_equal(t, last)  # not recomputed on this step
+            last = t.copy()
+            out.append(t)
+        return out
+
+    a, b = run(), run()
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))  # deterministic
 
 
 def test_ensemble_shard_with_nccl_allreduce_in_graph(oracle):
@@ -686,14 +690,13 @@ def test_ensemble_shard_with_nccl_allreduce_in_graph(oracle):
     ens.generate_terrain()
     refs = [oracle.terrain(w, h, ensemble.member_params(i)[0]) for i in range(M)]
     for s in range(3):
-        state = np.stack(refs)
+        want = _np_stats(np.stack(refs))
         ens.ctx.step(1)
-        want = _np_stats(state)
-        t = ens.table()
-        assert np.array_equal(t[:, 1], want[:, 1]) and np.allclose(t[:, 3], want[:, 3], rtol=1e-13)
         for i in range(M):
             _, K, m = ensemble.member_params(i)
             oracle.step(refs[i], params=make_params(K=K, m_exp=m), want_donor=False)
+        t = ens.table()
+        assert np.array_equal(t[:, 1], want[:, 1]) and np.allclose(t[:, 3], want[:, 3], rtol=1e-13)
         g = ens.ctx.download()
         for i in range(M):
             assert np.array_equal(g[i].view(np.uint64), refs[i].view(np.uint64)), (s, i)
