@@ -193,6 +193,18 @@ int lemgpu_step_async(lemgpu_ctx* ctx, uint32_t nsteps);
  * since the last sync (oldest first) and returns the first failing status. */
 int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count);
 
+/* Asynchronous snapshot: after lemgpu_step_async, copy the elevation the last
+ * enqueued step produced (and that step's diagnostics; diag_host nullable)
+ * into host memory on a side stream, returning at once.  The next step runs
+ * beside the copy (it only reads that state); the step after, which writes
+ * the same buffer, waits for the copy on the device.  lemgpu_snapshot_wait
+ * blocks until the copy has landed.  One snapshot in flight per context; pin
+ * the host memory (lemgpu_host_register) for the copy to overlap.  Used by the
+ * C++ shim's run_simulation (StepCallback / `lem run` snapshots,
+ * proj/tools/lem.cpp:143-147). */
+int lemgpu_snapshot_async(lemgpu_ctx* ctx, double* host, lemgpu_diag* diag_host);
+int lemgpu_snapshot_wait(lemgpu_ctx* ctx);
+
 /* One lem::strategy_step on a HOST raster: upload elev, one step, download
  * elev (the drop-in semantics of strategy_step(Raster<double>&, ...)).
  * Replaces: proj/src/scheduler.cpp:408-464 for StrategyKind::kRbGpu. */

@@ -92,6 +92,8 @@ _SIGS = {
     "lemgpu_step_async": (C.c_int, [_P, C.c_uint32]),
     "lemgpu_sync": (C.c_int, [_P, C.POINTER(lemgpu_diag), C.c_uint32, C.POINTER(C.c_uint32)]),
     "lemgpu_step_host": (C.c_int, [_P, _P, C.POINTER(lemgpu_diag)]),
+    "lemgpu_snapshot_async": (C.c_int, [_P, _P, C.POINTER(lemgpu_diag)]),
+    "lemgpu_snapshot_wait": (C.c_int, [_P]),
     "lemgpu_download_graph": (C.c_int, [_P, _P, _P, _P, _P, _P, C.POINTER(C.c_uint32), _P]),
     "lemgpu_member_stats_device": (C.c_int, [_P, _P]),
     "lemgpu_shard_members": (C.c_int, [C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),

@@ -76,6 +76,11 @@ struct lemgpu_ctx {
   cudaGraphExec_t st_exec[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // asynchronous snapshots (lemgpu_snapshot_async): side stream, events, the buffer being copied
+  cudaStream_t s_snap = nullptr;
+  cudaEvent_t ev_snap_step = nullptr, ev_snap_done = nullptr;
+  bool snap_pending = false;
+  uint32_t snap_buf = 0;
   bool host_profile = false;         // lemgpu_options::host_profile
   // banded host steps (lemgpu_step_host): copy streams, per-band events, patch count
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -1083,6 +1088,8 @@ int enqueue_step(lemgpu_ctx* ctx) {
     CU(ctx, cudaEventRecord(ev[0], ctx->stream));
   }
   const uint32_t p = ctx->cur;
+  // a snapshot still copying the buffer this step writes: wait for it (on the device)
+  if (ctx->snap_pending && ctx->snap_buf == (p ^ 1u)) CU(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_done, 0));
   if (ctx->a.dbg_level) {  // debug capture: every step starts from "not finished by the tile pass"
     CU(ctx, cudaMemsetAsync(ctx->a.dbg_level, 0xFF, ctx->a.N, ctx->stream));
     CU(ctx, cudaMemsetAsync(ctx->a.dbg_A, 0xFF, (size_t)ctx->a.N * sizeof(double), ctx->stream));
@@ -1142,6 +1149,9 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   destroy_graphs(ctx);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_snap) cudaStreamDestroy(ctx->s_snap);
+  if (ctx->ev_snap_step) cudaEventDestroy(ctx->ev_snap_step);
+  if (ctx->ev_snap_done) cudaEventDestroy(ctx->ev_snap_done);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
   for (cudaEvent_t e : ctx->band_ev) cudaEventDestroy(e);
   if (ctx->h_patch) cudaFreeHost(ctx->h_patch);
@@ -1293,6 +1303,10 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
   if (!ctx) return fail(ctx, LEMGPU_ECONFIG, "null context");
   CU(ctx, cudaSetDevice(ctx->device));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->snap_pending) {  // the diagnostics ring is reused after a sync: the snapshot copy must be done
+    CU(ctx, cudaEventSynchronize(ctx->ev_snap_done));
+    ctx->snap_pending = false;
+  }
   const uint32_t n = ctx->pending;
   std::vector<lemgpu_diag> d(n);
   if (n) CU(ctx, cudaMemcpy(d.data(), ctx->d_diag, n * sizeof(lemgpu_diag), cudaMemcpyDeviceToHost));
@@ -1361,6 +1375,43 @@ int lemgpu_step(lemgpu_ctx* ctx, uint32_t nsteps, lemgpu_diag* per_step) {
     rc = lemgpu_sync(ctx, per_step ? per_step + done : nullptr, chunk, &cnt);
     if (rc) return rc;
     done += chunk;
+  }
+  return LEMGPU_OK;
+}
+
+int lemgpu_snapshot_async(lemgpu_ctx* ctx, double* host, lemgpu_diag* diag_host) {
+  if (!ctx || !host) return fail(ctx, LEMGPU_ECONFIG, "null argument");
+  if (!ctx->pending) return fail(ctx, LEMGPU_ECONFIG, "no step enqueued since the last sync");
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->snap_pending) {
+    CU(ctx, cudaEventSynchronize(ctx->ev_snap_done));
+    ctx->snap_pending = false;
+  }
+  if (!ctx->s_snap) {
+    CU(ctx, cudaStreamCreateWithFlags(&ctx->s_snap, cudaStreamNonBlocking));
+    CU(ctx, cudaEventCreateWithFlags(&ctx->ev_snap_step, cudaEventDisableTiming));
+    CU(ctx, cudaEventCreateWithFlags(&ctx->ev_snap_done, cudaEventDisableTiming));
+  }
+  // the state after the last enqueued step, and that step's diagnostics slot
+  CU(ctx, cudaEventRecord(ctx->ev_snap_step, ctx->stream));
+  CU(ctx, cudaStreamWaitEvent(ctx->s_snap, ctx->ev_snap_step, 0));
+  CU(ctx, cudaMemcpyAsync(host, ctx->hbuf[ctx->cur], (size_t)ctx->a.N * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->s_snap));
+  if (diag_host)
+    CU(ctx, cudaMemcpyAsync(diag_host, ctx->d_diag + (ctx->pending - 1), sizeof(lemgpu_diag), cudaMemcpyDeviceToHost,
+                            ctx->s_snap));
+  CU(ctx, cudaEventRecord(ctx->ev_snap_done, ctx->s_snap));
+  ctx->snap_buf = ctx->cur;
+  ctx->snap_pending = true;
+  return LEMGPU_OK;
+}
+
+int lemgpu_snapshot_wait(lemgpu_ctx* ctx) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->snap_pending) {
+    CU(ctx, cudaEventSynchronize(ctx->ev_snap_done));
+    ctx->snap_pending = false;
   }
   return LEMGPU_OK;
 }

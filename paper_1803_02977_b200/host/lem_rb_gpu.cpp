@@ -139,14 +139,40 @@ RunResult run_simulation_rb_gpu(Raster<double> initial, const RunConfig& cfg, co
     if (cfg.timesteps) check(c->h, lemgpu_step(c->h, cfg.timesteps, d.data()));
     for (const auto& x : d) res.per_step.push_back(to_diag(x));
   } else {
-    for (std::uint32_t s = 1; s <= cfg.timesteps; ++s) {
-      lemgpu_diag d{};
-      check(c->h, lemgpu_step(c->h, 1, &d));
-      check(c->h, lemgpu_download_elev(c->h, res.elevation.storage().data()));
+    // The callback needs each step's raster (lem run's snapshots,
+    // proj/tools/lem.cpp:143-147).  Pipelined: step s+1 runs on the device
+    // while step s's raster comes down on a side stream (lemgpu_snapshot_async)
+    // into one of two pinned staging rasters and the callback sees it.
+    Raster<double> stage[2] = {Raster<double>(res.elevation.width(), res.elevation.height()),
+                               Raster<double>(res.elevation.width(), res.elevation.height())};
+    const std::size_t bytes = stage[0].size() * sizeof(double);
+    bool pinned[2];
+    for (int i = 0; i < 2; ++i) pinned[i] = lemgpu_host_register(stage[i].storage().data(), bytes) == LEMGPU_OK;
+    lemgpu_diag dg[2]{};
+    auto deliver = [&](std::uint32_t s) {
+      check(c->h, lemgpu_snapshot_wait(c->h));
+      const lemgpu_diag& d = dg[s & 1u];
+      if (d.status != 0) check(c->h, lemgpu_sync(c->h, nullptr, 0, nullptr));  // throws the step's error
       StepDiagnostics sd = to_diag(d);
-      on_step(s, res.elevation, sd);
+      on_step(s, stage[s & 1u], sd);
       res.per_step.push_back(std::move(sd));
+    };
+    try {
+      for (std::uint32_t s = 1; s <= cfg.timesteps; ++s) {
+        check(c->h, lemgpu_step_async(c->h, 1));  // runs beside the previous snapshot's copy and callback
+        if (s > 1) deliver(s - 1);
+        check(c->h, lemgpu_snapshot_async(c->h, stage[s & 1u].storage().data(), &dg[s & 1u]));
+      }
+      if (cfg.timesteps) deliver(cfg.timesteps);
+      check(c->h, lemgpu_sync(c->h, nullptr, 0, nullptr));
+    } catch (...) {
+      lemgpu_snapshot_wait(c->h);
+      for (int i = 0; i < 2; ++i)
+        if (pinned[i]) lemgpu_host_unregister(stage[i].storage().data());
+      throw;
     }
+    for (int i = 0; i < 2; ++i)
+      if (pinned[i]) lemgpu_host_unregister(stage[i].storage().data());
   }
   check(c->h, lemgpu_download_elev(c->h, res.elevation.storage().data()));
   for (const auto& d : res.per_step) {
