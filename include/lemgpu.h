@@ -129,7 +129,9 @@ typedef struct lemgpu_options {
   uint32_t host_bands;     /* banded host step: bands (0: one per ~25 MB, <= 32; 1..3: unbanded) */
   uint32_t patch_cap;      /* banded host step: escaped-cell patch capacity (0: max(2^20, N/16)) */
   int32_t host_profile;    /* 1: banded host step prints its timing to stderr */
-  int32_t reserved[3];
+  int32_t esc_forest;      /* escaped trees by k_esc_forest (exact-area steps): 0 auto (>= 1/4 of the cells
+                              escape), 1 always, -1 never (level path) */
+  int32_t reserved[2];
 } lemgpu_options;
 
 typedef struct lemgpu_ctx lemgpu_ctx;

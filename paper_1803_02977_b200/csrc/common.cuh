@@ -8,6 +8,9 @@
 //                       cells stay within 3 cells of it                  (k_tiles.cuh)
 //   then, for the trees that escape their tile:
 //   k_esc_small         a small escape set in one CTA's shared memory      (k_tiles.cuh)
+//   k_esc_forest        cooperative: most of the raster escaped (filled DEMs): levels by
+//                       pointer jumping, trees split between CTAs, swept with block
+//                       barriers only                                     (k_forest.cuh)
 //   k_esc_bfs           cooperative: every level of the escaped trees      (k_order.cuh)
 //   k_chunks            accumulation + uplift + erosion per source chunk  (k_physics.cuh)
 //   k_deep_coop         cooperative: the same sweeps level by level for
@@ -169,6 +172,9 @@ struct Ctl {
   uint32_t esc_fail, esc_cells, esc_nlev, esc_misses, esc_done;  // k_esc_small's CTAs: overflow count, totals
   unsigned long long esc_iters;
   uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
+  uint32_t fr_flag[3], fr_maxd;          // k_esc_forest: pointer-jumping round flags, deepest escaped level
+  uint32_t fr_rounds, fr_maxcells;       // ... rounds taken, most cells of one CTA
+  unsigned long long fr_t[3];            // ... latest end over the CTAs of the counts, F and erosion sweeps
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
   unsigned long long ph_cyc[32][6];  // SM cycles per lem::Phase charged by the CTAs this step (PhClk), 32 spread slots
@@ -242,6 +248,11 @@ struct StepArgs {
   double* st_table;
   uint32_t st_chunks;
   uint32_t st_member0;
+  // k_esc_forest (k_forest.cuh): 0 off, 1 when >= 1/4 of the cells escape, 2 always (EX only)
+  int esc_forest;
+  uint32_t* fbins;   // [owner CTA][depth] counts / cursors (the global path's levels array, N + 2)
+  uint32_t cb_cap;   // entries of cbound (k_esc_forest: level starts)
+  double* hx;        // position-major elevations (k_esc_forest)
   uint8_t* dbg_level;  // debug capture (nullptr: off): level of every cell k_tiles finishes (escaped: untouched)
   double* dbg_A;       // ... and its drainage area
   Ctl* ctl;

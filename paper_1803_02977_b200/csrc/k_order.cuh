@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(kTPB) k_esc_bfs(StepArgs a) {
   } u;
   ScanSmem& sm = u.sm;
   Ctl* ctl = a.ctl;
-  if (ld_volatile_u32(&ctl->esc_small)) return;  // k_esc_small finished the escaped trees (uniform)
+  if (ld_volatile_u32(&ctl->esc_small) || ld_volatile_u32(&ctl->mode) == kModeDone)
+    return;  // k_esc_small or k_esc_forest finished the escaped trees (uniform)
   PhWhole ph(ctl, LEMGPU_PHASE_ORDER);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const bool err = ld_volatile_u32(&ctl->err_flag) != 0;

@@ -33,6 +33,7 @@
 #include "k_recv_donor.cuh"
 #include "k_fill.cuh"
 #include "k_tiles.cuh"
+#include "k_forest.cuh"
 #include "k_util.cuh"
 
 using namespace lemgpu;
@@ -46,6 +47,7 @@ struct lemgpu_ctx {
   int scan_grid = 0, chunk_grid = 0, deep_grid = 0, tile_grid = 0;
   int esc_grid = 0;  // CTAs of the level expansion of the escaped trees (a small workload)
   int deep_coop_grid = 0;  // CTAs of k_deep_coop (kDeepTPB threads, co-resident)
+  int forest_grid = 0;     // CTAs of k_esc_forest (kFTPB threads, co-resident)
   int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
   // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
   // graph[p] / exec[p] is the step that reads hbuf[p]
@@ -404,6 +406,9 @@ const void* recv_fn(const StepArgs& a) {
   if (a.conn == 4) return (const void*)k_recv<4, false>;
   return a.unit_card ? (const void*)k_recv<8, true> : (const void*)k_recv<8, false>;
 }
+const void* forest_fn(int nk) {
+  return nk == 1 ? (const void*)k_esc_forest<1> : nk == 2 ? (const void*)k_esc_forest<2> : (const void*)k_esc_forest<0>;
+}
 size_t tiles_smem(const StepArgs& a) { return a.lut_exact ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>(); }
 
 // The step graph that reads hbuf[p]; with_stats: ending with the ensemble
@@ -470,6 +475,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
     prev = join;
     if ((ctx->esc_small &&
          (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
+        (a.esc_forest && (rc = add_kernel(ctx, g, &prev, forest_fn(nk), dim3(ctx->forest_grid), dim3(kFTPB),
+                                          kForestSmemBytes, &a, nullptr, true))) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else if (ctx->use_tiles) {
@@ -478,6 +485,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
                          &ctx->tmap[p])) ||
         (ctx->esc_small &&
          (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
+        (a.esc_forest && (rc = add_kernel(ctx, g, &prev, forest_fn(nk), dim3(ctx->forest_grid), dim3(kFTPB),
+                                          kForestSmemBytes, &a, nullptr, true))) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else {
@@ -636,10 +645,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
       (rc = dmalloc(ctx, &ctx->hbuf[1], N)) || (rc = dmalloc(ctx, &ctx->d_levels_esc, (size_t)N + 2)) ||
       (rc = dmalloc(ctx, &a.rcode, (size_t)N + 16)) ||
       (rc = dmalloc(ctx, &a.planes, (size_t)4 * H * M * ((W + 31) / 32))) || (rc = dmalloc(ctx, &a.dmask, (size_t)N + 16)) ||
-      (rc = dmalloc(ctx, &a.order, N)) || (rc = dmalloc(ctx, &a.ppos, N)) || (rc = dmalloc(ctx, &a.cdir, N)) ||
+      (rc = dmalloc(ctx, &a.order, (size_t)N + kFChunk)) || (rc = dmalloc(ctx, &a.ppos, (size_t)N + kFChunk)) ||
+      (rc = dmalloc(ctx, &a.cdir, N)) || (rc = dmalloc(ctx, &a.hx, (size_t)N + kFChunk)) ||
       (rc = dmalloc(ctx, &a.fc, (size_t)N + 1)) ||
       (rc = dmalloc(ctx, &a.cbound, ((size_t)N / kChunkRoots + 2) * kCBS)) ||
-      (rc = dmalloc(ctx, &a.Aq, N)) || (rc = dmalloc(ctx, &a.hq, N)) ||
+      (rc = dmalloc(ctx, &a.Aq, (size_t)N + kFChunk)) || (rc = dmalloc(ctx, &a.hq, (size_t)N + kFChunk)) ||
       (rc = dmalloc(ctx, &a.levels, (size_t)N + 2)) ||
       (rc = dmalloc(ctx, &a.pdm, N)) || (rc = dmalloc(ctx, &a.part, 4096)) ||
       (rc = dmalloc(ctx, &a.bins, 3 * 4096)) || (rc = dmalloc(ctx, &a.ctl, 1)) ||
@@ -654,6 +664,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.ftab = ctx->d_lut;
   a.ftab2 = ctx->d_lut2;
   a.cb_stride = N / kChunkRoots + 2;
+  a.cb_cap = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((uint64_t)N / kChunkRoots + 2) * kCBS);
+  a.fbins = a.levels;  // the global path's level array: unused by the tile path's steps
   a.diag = ctx->d_diag;
 #define CUB(call)                          \
   do {                                     \
@@ -734,12 +746,21 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     ctx->bands = (int)std::min<uint64_t>(32, nbands < 4 ? 1 : nbands);
   }
   if (a.force_deep) ctx->esc_small = false;  // testing the deep sweeps of the escape path
+  // k_esc_forest for exact-area steps (integer drainage counts): auto / always / never
+  a.esc_forest = !a.lut_exact || o.esc_forest < 0 || a.force_deep ? 0 : o.esc_forest > 0 ? 2 : 1;
   a.no_narrow = o.no_narrow ? 1 : 0;  // testing: grid-wide sweeps for every level
   a.eager = o.eager ? 1 : 0;
   for (const void* f : {(const void*)k_esc_small<0>, (const void*)k_esc_small<1>, (const void*)k_esc_small<2>})
     CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEscSmallSmemBytes));
   for (const void* f : {(const void*)k_deep_coop<0>, (const void*)k_deep_coop<1>, (const void*)k_deep_coop<2>})
     CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDeepSmemBytes));
+  for (const void* f : {(const void*)k_esc_forest<0>, (const void*)k_esc_forest<1>, (const void*)k_esc_forest<2>})
+    CUB(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kForestSmemBytes));
+  {
+    int occf = 0;
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, forest_fn(a.nkind), kFTPB, kForestSmemBytes));
+    ctx->forest_grid = (occf > 0 ? occf : 1) * nsm;
+  }
   {
     const void* fdc = a.nkind == 1 ? (const void*)k_deep_coop<1> : a.nkind == 2 ? (const void*)k_deep_coop<2>
                                                                               : (const void*)k_deep_coop<0>;
@@ -858,6 +879,9 @@ int enqueue_escape_eager(lemgpu_ctx* ctx, StepArgs& a, cudaStream_t st) {
       k_esc_small<0><<<ctx->esc_small_grid, kTPB, kEscSmallSmemBytes, st>>>(a);
   }
   void* eargs[] = {&a};
+  if (a.esc_forest)
+    CU(ctx, cudaLaunchCooperativeKernel(forest_fn(a.nkind), dim3(ctx->forest_grid), dim3(kFTPB), eargs,
+                                        kForestSmemBytes, st));
   CU(ctx, cudaLaunchCooperativeKernel((const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), eargs, 0, st));
   return run_levels_eager(ctx, a);
 }
@@ -1137,7 +1161,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   StepArgs& a = ctx->a;
   void* ptrs[] = {ctx->d_kdt, ctx->d_mexp, ctx->d_lut, ctx->d_lut2, ctx->hbuf[0], ctx->hbuf[1], ctx->d_levels_esc, a.rcode, a.planes,  a.dmask, a.order,
                   a.ppos,     a.cdir,      a.fc,        a.cbound,     a.Aq,  a.hq,     a.levels, a.pdm, a.part, a.bins,
-                  a.ctl,      ctx->d_diag};
+                  a.ctl,      ctx->d_diag, a.hx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (a.dbg_level) cudaFree(a.dbg_level);
@@ -1565,9 +1589,10 @@ int lemgpu_debug_copy(lemgpu_ctx* ctx, int which, void* host, uint64_t bytes) {
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   const void* src = which == 0 ? (const void*)ctx->a.order : which == 1 ? (const void*)ctx->d_levels_esc
                     : which == 2 ? (const void*)ctx->a.ctl : which == 3 ? (const void*)ctx->a.dbg_level
-                                                                         : (const void*)ctx->a.dbg_A;
+                    : which == 4 ? (const void*)ctx->a.dbg_A : (const void*)ctx->a.bins;
   const uint64_t cap = which == 0 ? (uint64_t)ctx->a.N * 4 : which == 1 ? ((uint64_t)ctx->a.N + 2) * 4
-                       : which == 2 ? sizeof(Ctl) : which == 3 ? (uint64_t)ctx->a.N : (uint64_t)ctx->a.N * 8;
+                       : which == 2 ? sizeof(Ctl) : which == 3 ? (uint64_t)ctx->a.N : which == 4 ? (uint64_t)ctx->a.N * 8
+                       : 3 * 4096 * 4;
   if (!src) return fail(ctx, LEMGPU_ECONFIG, "debug capture is off");
   CU(ctx, cudaMemcpy(host, src, bytes < cap ? bytes : cap, cudaMemcpyDeviceToHost));
   return LEMGPU_OK;

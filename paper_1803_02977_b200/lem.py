@@ -249,6 +249,7 @@ _KNOB_NAMES = {
     "LEMGPU_ESC_SMALL_GRID": ("esc_small_grid", int), "LEMGPU_PIPE_TILE_GRID": ("pipe_tile_grid", int),
     "LEMGPU_LUT_ENTRIES": ("lut_entries", int), "LEMGPU_HOST_BANDS": ("host_bands", int),
     "LEMGPU_PATCH_CAP": ("patch_cap", int), "LEMGPU_HOST_PROFILE": ("host_profile", int),
+    "LEMGPU_ESC_FOREST": ("esc_forest", int),
 }
 
 

@@ -355,8 +355,11 @@ def _ramp(w, h, seed):
 
 @pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_FORCE_ESCAPE": "2"},
                                  {"LEMGPU_PATH": "global"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_FORCE_DEEP": "1"},
-                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0"}],
-                         ids=["tiles", "all-escape", "half-escape", "global", "all-escape-deep", "all-escape-coop"])
+                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0", "LEMGPU_ESC_FOREST": "-1"},
+                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0", "LEMGPU_ESC_FOREST": "1"},
+                                 {"LEMGPU_FORCE_ESCAPE": "2", "LEMGPU_ESC_SMALL": "0", "LEMGPU_ESC_FOREST": "1"}],
+                         ids=["tiles", "all-escape", "half-escape", "global", "all-escape-deep", "all-escape-coop",
+                              "all-escape-forest", "half-escape-forest"])
 @pytest.mark.parametrize("w,h,seed,kw,terrain", [
     (300, 200, 31, {}, "noise"), (130, 97, 32, {"n_exp": 2.0}, "noise"), (77, 65, 33, {"dx": 0.5}, "noise"),
     (129, 70, 34, {}, "ramp"), (90, 61, 35, {}, "ramp"), (400, 12, 36, {}, "ramp"), (61, 40, 37, {"n_exp": 2.0}, "ramp"),
@@ -365,8 +368,9 @@ def test_schedules_agree_with_oracle(oracle, monkeypatch, env, w, h, seed, kw, t
     """Every schedule -- trees finished inside their tile (k_tiles), trees that
     escape to the global level path (all of them, or every odd-rooted one; in
     k_esc_small's shared memory when they fit, <= 6144 cells and <= 256 levels,
-    else -- or with LEMGPU_ESC_SMALL=0 -- in the cooperative kernels), the
-    global path alone, and its per-level sweeps -- gives the oracle's bits."""
+    else -- or with LEMGPU_ESC_SMALL=0 -- in the cooperative level-path
+    kernels or k_esc_forest's pointer-jumped, per-tree sweeps), the global path
+    alone, and its per-level sweeps -- gives the oracle's bits."""
     ctx = device_ctx(w, h, options=env, **kw)
     e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
     ctx.upload(e)
@@ -392,13 +396,17 @@ def test_failed_step_leaves_elevation_unchanged(oracle):
     assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
 
 
-@pytest.mark.parametrize("narrow", [True, False], ids=["narrow-runs", "grid-only"])
-def test_deep_plan_1000(oracle, monkeypatch, narrow):
-    """A 1000^2 tilted plane: ~1000 levels, every tree escapes its tile, the
-    escape path runs its cooperative level expansion and deep sweeps (runs of
-    narrow levels on one CTA, or -- LEMGPU_NO_NARROW -- every level grid-wide)."""
+@pytest.mark.parametrize("opts", [{"esc_forest": -1}, {"esc_forest": -1, "no_narrow": 1}, None],
+                         ids=["narrow-runs", "grid-only", "forest"])
+def test_deep_plan_1000(oracle, monkeypatch, opts):
+    """A 1000^2 tilted plane: ~1000 levels, every tree escapes its tile.  The
+    escape path's level kernels (cooperative level expansion and deep sweeps:
+    runs of narrow levels on one CTA, or every level grid-wide) and, by
+    default, k_esc_forest (levels by pointer jumping, trees split between
+    CTAs) give the oracle's bits; the export still rebuilds the reference's
+    own TraversalPlan."""
     e = _ramp(1000, 1000, 5)
-    ctx = device_ctx(1000, 1000, options=None if narrow else {"no_narrow": 1})
+    ctx = device_ctx(1000, 1000, options=opts)
     ctx.upload(e)
     for s in range(2):
         d = ctx.step(1)[0]
@@ -432,9 +440,11 @@ def _host_register(a):
     return lem._abi.lib().lemgpu_host_register(a.ctypes.data, a.nbytes) == 0
 
 
-@pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0"},
+@pytest.mark.parametrize("env", [{}, {"LEMGPU_FORCE_ESCAPE": "2"},
+                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0", "LEMGPU_ESC_FOREST": "-1"},
+                                 {"LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_SMALL": "0"},
                                  {"LEMGPU_FORCE_ESCAPE": "2", "LEMGPU_PATCH_CAP": "64"}],
-                         ids=["tiles", "half-escape", "all-escape-coop", "patch-overflow"])
+                         ids=["tiles", "half-escape", "all-escape-coop", "all-escape-forest", "patch-overflow"])
 @pytest.mark.parametrize("w,h,terrain", [(300, 250, "noise"), (200, 170, "ramp"), (131, 97, "noise")])
 def test_step_host_banded(oracle, monkeypatch, env, w, h, terrain):
     """lemgpu_step_host (the strategy_step drop-in) on pinned host memory: the
@@ -560,7 +570,8 @@ def test_random_configurations(oracle, monkeypatch, seed):
         dx = float(rng.choice([1.0, 1.0, 0.5, 2.0]))
         M = int(rng.integers(1, 4))
         env = [{}, {"LEMGPU_FORCE_ESCAPE": "2"}, {"LEMGPU_FORCE_ESCAPE": "1"}, {"LEMGPU_TILE_GRID": "3"},
-               {"LEMGPU_NO_TMA": "1"}, {"LEMGPU_ESC_SMALL": "0", "LEMGPU_FORCE_ESCAPE": "1"}][int(rng.integers(0, 6))]
+               {"LEMGPU_NO_TMA": "1"}, {"LEMGPU_ESC_SMALL": "0", "LEMGPU_FORCE_ESCAPE": "1", "LEMGPU_ESC_FOREST": "-1"},
+               {"LEMGPU_ESC_SMALL": "0", "LEMGPU_FORCE_ESCAPE": "2", "LEMGPU_ESC_FOREST": "1"}][int(rng.integers(0, 7))]
         kw = {"n_exp": n_exp, "dx": dx}
         ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=M, options=env)
         seeds = [int(x) for x in rng.integers(1, 10**6, size=M)]

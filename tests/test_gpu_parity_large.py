@@ -82,16 +82,19 @@ def test_config4_full_ensemble_vs_reference():
     assert sum(d.newton_iters for d in ds) == total
 
 
-@pytest.mark.parametrize("n,steps", [(1000, 3), (4000, 1)], ids=["dem1000fill", "dem4000fill"])
-def test_filled_dem_vs_reference(n, steps):
+@pytest.mark.parametrize("n,steps,opts", [(1000, 3, None), (1000, 2, {"esc_forest": -1}), (4000, 2, None)],
+                         ids=["dem1000fill", "dem1000fill-levelpath", "dem4000fill"])
+def test_filled_dem_vs_reference(n, steps, opts):
     """The deep-level regime: seed-42 terrain, epsilon-filled by lem::priority_flood_fill
     (and, independently, by lemgpu_fill -- identical), then stepped: bit-identical to
     the reference although drainage areas reach ~2e5 (1000^2) / ~5e6 (4000^2) --
-    beyond the F table, pow(A, m) is the device restatement of glibc's pow."""
+    beyond the F table, pow(A, m) is the device restatement of glibc's pow.  By
+    default the escaped forest goes through k_esc_forest (levels by pointer
+    jumping, trees split between CTAs); -levelpath: the cooperative level kernels."""
     ref = _ref()
     e0 = ref.terrain(n, n, 42)
     filled = ref.fill(e0, 2)
-    ctx = lem.DeviceContext(n, n, lem.SimParams(), 8)
+    ctx = lem.DeviceContext(n, n, lem.SimParams(), 8, options=opts)
     ctx.generate_terrain([42])
     ctx.fill(mode=2)
     assert _same(ctx.download(), filled)
