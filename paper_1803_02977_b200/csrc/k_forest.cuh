@@ -40,6 +40,7 @@
 namespace lemgpu {
 
 constexpr int kFTPB = 1024;              // one CTA per SM
+constexpr uint32_t kFNW = kFTPB / 32;    // warps per CTA
 constexpr uint32_t kFRing = 4096;        // cells of one level of a CTA held in a shared-memory ring slot
 constexpr uint32_t kFLv = 8192;          // level starts of a CTA kept in shared memory (deeper: global)
 constexpr uint32_t kFTop = 0x80000000u;  // escaped-root mark in the distance word of J
@@ -69,6 +70,11 @@ struct ForestSmem {
 };
 constexpr size_t kForestSmemBytes = sizeof(ForestSmem);
 
+// Barrier of the first n threads of the CTA (named barrier 1; n a multiple of 32).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // One bulk asynchronous copy global -> shared (16-byte aligned, multiple of 16
 // bytes), completing on the mbarrier's transaction count.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -88,7 +94,7 @@ __device__ __forceinline__ uint32_t forest_block_sum(uint32_t v, uint32_t* red) 
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  uint32_t t = threadIdx.x < 32 ? red[threadIdx.x] : 0u;
+  uint32_t t = threadIdx.x < kFNW ? red[threadIdx.x] : 0u;
   if (threadIdx.x < 32)
     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   __syncthreads();
@@ -252,12 +258,12 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
       if (lane == 31) s.red[tid >> 5] = x;
       __syncthreads();
       if (tid < 32) {
-        uint32_t w = s.red[tid];
+        uint32_t w = tid < kFNW ? s.red[tid] : 0u;
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
           if (lane >= (uint32_t)o) w += y;
         }
-        s.red[tid] = w;
+        if (tid < kFNW) s.red[tid] = w;
       }
       __syncthreads();
       const uint32_t ex = carry + (tid >= 32 ? s.red[(tid >> 5) - 1] : 0u) + x - v;
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
         cur[b * D + d] = ex;
         if (d < kFLv) s.lv[d] = ex;
       }
-      carry += s.red[31];
+      carry += s.red[kFNW - 1];
       __syncthreads();
     }
     if (tid == 0) {
@@ -325,8 +331,14 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
   if (lane == 0) s.red[tid >> 5] = Dl;
   __syncthreads();
   Dl = 0;
-  for (int j = 0; j < 32; ++j) Dl = max(Dl, s.red[j]);
+  for (uint32_t j = 0; j < kFNW; ++j) Dl = max(Dl, s.red[j]);
   __syncthreads();
+  // the warps that sweep the counts: about two cells per thread of an average
+  // level (every idle warp would still pay the per-level bookkeeping and the
+  // barrier); the others skip the sweep
+  const uint32_t avgw = (P1 - P0) / max(Dl, 1u);
+  uint32_t nact = 32u * min(kFNW, max(2u, (avgw + 63u) / 64u));
+  bool act = tid < nact;
   // ---- 6. drainage counts, deepest level first: each cell adds its final
   // count to its receiver's slot (shared-memory ring; global for wide levels).
   // The receiver positions of the coming levels stream into shared memory
@@ -335,27 +347,30 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
   // for the next level's chunks, and the ring slot of level d-2 is reset by
   // the top threads, so a level costs the busy warps one shared-memory round
   // trip and a block barrier.
-  const uint32_t HT = kFTPB - 1, rtid = kFTPB - 1 - tid;
+  uint32_t HT = nact - 1;
+  const uint32_t rtid = nact - 1 - tid;
   auto ring_reset = [&](uint32_t d, uint32_t s0, uint32_t e0) {  // level d = [s0, e0) -> counts 1
     if (e0 - s0 > kFRing) return;
     uint32_t* rb = s.u.a.cnt[d % 3];
-    for (uint32_t i = rtid; i < e0 - s0; i += kFTPB) rb[i] = 1u;
+    for (uint32_t i = rtid; i < e0 - s0; i += nact) rb[i] = 1u;
   };
   if (tid < kFSlotsA) mbar_init(&s.bar[tid], 1);
   // chunk k of the descending sweep = positions [(qa - k) * kFChunk, +kFChunk)
   const uint32_t qa = P1 > P0 ? (P1 - 1) / kFChunk : 0u;
   const uint32_t ka_last = Dl > 1 ? qa - lvl(1) / kFChunk : 0u;
   uint32_t ka_next = 0;
+  uint32_t ka_done = 0;  // helper: chunks [0, ka_done) have landed (waited once each: mbarrier waits are not free)
   auto issue_a = [&](uint32_t limit) {  // helper thread: chunks up to index `limit` of the sweep
     for (; ka_next <= limit && ka_next <= ka_last; ++ka_next) {
       const uint32_t sl = ka_next % kFSlotsA;
-      if (ka_next >= kFSlotsA) mbar_wait(&s.bar[sl], ((ka_next - kFSlotsA) / kFSlotsA) & 1u);
+      if (ka_next >= kFSlotsA && ka_next - kFSlotsA >= ka_done) mbar_wait(&s.bar[sl], ((ka_next - kFSlotsA) / kFSlotsA) & 1u);
       mbar_expect_tx(&s.bar[sl], kFChunk * 4);
       bulk_g2s(s.u.a.pp[sl], a.ppos + (size_t)(qa - ka_next) * kFChunk, kFChunk * 4, &s.bar[sl]);
     }
   };
   auto wait_a = [&](uint32_t kl, uint32_t kh) {
-    for (uint32_t k = kl; k <= kh; ++k) mbar_wait(&s.bar[k % kFSlotsA], (k / kFSlotsA) & 1u);
+    for (uint32_t k = ka_done; k <= kh; ++k) mbar_wait(&s.bar[k % kFSlotsA], (k / kFSlotsA) & 1u);
+    ka_done = max(ka_done, kh + 1);
   };
   const long long ck0 = clock64();
   {
@@ -374,46 +389,73 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
     }
   }
   __syncthreads();
-  for (uint32_t d = Dl; d-- > 1;) {
-    const uint32_t ps = lvl(d - 1);
-    const uint32_t pps = d >= 2 ? lvl(d - 2) : 0u;
-    const bool wide = e0 - s0 > kFRing, pwide = s0 - ps > kFRing;
-    const uint32_t* rc = s.u.a.cnt[d % 3];
-    uint32_t* rp = s.u.a.cnt[(d - 1) % 3];
-    for (uint32_t i = s0 + tid; i < e0; i += kFTPB) {
-      const uint32_t p = staged ? s.u.a.pp[(qa - i / kFChunk) % kFSlotsA][i % kFChunk] : __ldcg(a.ppos + i);
-      uint32_t v;
-      if (wide) {
-        v = __ldcg(cnt + i);
-      } else {
-        v = rc[i - s0];
-        cnt[i] = v;
+  if (act) {
+    uint32_t* rc = s.u.a.cnt[(Dl - 1) % 3];  // ring slots of levels d, d-1, d-2 (rotating)
+    uint32_t* rp = s.u.a.cnt[(Dl + 1) % 3];
+    uint32_t* rq = s.u.a.cnt[Dl % 3];
+    for (uint32_t d = Dl; d-- > 1;) {
+      const uint32_t ps = lvl(d - 1);
+      const uint32_t pps = d >= 2 ? lvl(d - 2) : 0u;
+      const bool wide = e0 - s0 > kFRing, pwide = s0 - ps > kFRing;
+      // two cells per iteration: both loads in flight before the atomics
+      for (uint32_t i = s0 + tid; i < e0; i += 2 * nact) {
+        const uint32_t i2 = i + nact;
+        const bool two = i2 < e0;
+        uint32_t p, p2 = 0, v, v2 = 0;
+        if (staged) {
+          p = s.u.a.pp[(qa - i / kFChunk) % kFSlotsA][i % kFChunk];
+          if (two) p2 = s.u.a.pp[(qa - i2 / kFChunk) % kFSlotsA][i2 % kFChunk];
+        } else {
+          p = __ldcg(a.ppos + i);
+          if (two) p2 = __ldcg(a.ppos + i2);
+        }
+        if (wide) {
+          v = __ldcg(cnt + i);
+          if (two) v2 = __ldcg(cnt + i2);
+        } else {
+          v = rc[i - s0];
+          if (two) v2 = rc[i2 - s0];
+#ifndef LEMGPU_FOREST_EXP
+          cnt[i] = v;
+          if (two) cnt[i2] = v2;
+#endif
+        }
+        if (pwide) {
+          atomicAdd(cnt + p, v);
+          if (two) atomicAdd(cnt + p2, v2);
+        } else {
+          atomicAdd(rp + (p - ps), v);
+          if (two) atomicAdd(rp + (p2 - ps), v2);
+        }
       }
-      if (pwide)
-        atomicAdd(cnt + p, v);
-      else
-        atomicAdd(rp + (p - ps), v);
+      // level d-2 takes the slot level d+1 used
+      if (d >= 2 && ps - pps <= kFRing)
+        for (uint32_t i = rtid; i < ps - pps; i += nact) rq[i] = 1u;
+      // the next level (d-1) is staged when its chunks fit behind this level's first one
+      const uint32_t kl = qa - (e0 - 1) / kFChunk, khn = qa - ps / kFChunk;
+      const bool staged_n = khn <= kl + kFSlotsA - 1;
+      if (tid == HT && d > 1) {
+        issue_a(kl + kFSlotsA - 1);  // slots of chunks before this level's are free
+        if (staged_n) wait_a(qa - (s0 - 1) / kFChunk, khn);
+      }
+      named_bar_sync(1, nact);
+      e0 = s0;
+      s0 = ps;
+      staged = staged_n;
+      uint32_t* t = rc;
+      rc = rp;
+      rp = rq;
+      rq = t;
     }
-    if (d >= 2) ring_reset(d - 2, pps, ps);
-    // the next level (d-1) is staged when its chunks fit behind this level's first one
-    const uint32_t kl = qa - (e0 - 1) / kFChunk, khn = qa - ps / kFChunk;
-    const bool staged_n = khn <= kl + kFSlotsA - 1;
-    if (tid == HT && d > 1) {
-      issue_a(kl + kFSlotsA - 1);  // slots of chunks before this level's are free
-      if (staged_n) wait_a(qa - (s0 - 1) / kFChunk, khn);
-    }
-    __syncthreads();
-    e0 = s0;
-    s0 = ps;
-    staged = staged_n;
   }
+  __syncthreads();
   if (Dl > 0) {  // level 0: the roots' final counts
     const uint32_t w = lvl(1) - P0;
     if (w <= kFRing)
       for (uint32_t i = tid; i < w; i += kFTPB) cnt[P0 + i] = s.u.a.cnt[0][i];
   }
   if (tid == HT)  // every issued copy has landed before the space is reused
-    for (uint32_t k = ka_next > kFSlotsA ? ka_next - kFSlotsA : 0u; k < ka_next; ++k)
+    for (uint32_t k = max(ka_done, ka_next > kFSlotsA ? ka_next - kFSlotsA : 0u); k < ka_next; ++k)
       mbar_wait(&s.bar[k % kFSlotsA], (k / kFSlotsA) & 1u);
   __syncthreads();
   }
@@ -425,6 +467,7 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
     sb[0] = Dl;
     sb[1] = P1 - P0;
     sb[4] = (uint32_t)((clock64() - ck0) >> 10);
+    sb[2] = nact;
   }
   grid_barrier(ctl);  // every CTA's counts are final: F for all positions, grid-wide
   // ---- 7. F and the Newton reciprocal of every cell below level 0, the
@@ -469,6 +512,11 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
   grid_barrier(ctl);
   phclk_mark(s_pc, LEMGPU_PHASE_UPLIFT);
   if (tid == 0) atomicMax(&ctl->fr_t[1], globaltimer());
+  // erosion: every warp (measured faster than a subset sized to the average
+  // level: the widest levels dominate and the Newton solves are latency-bound)
+  nact = kFTPB;
+  act = tid < nact;
+  HT = nact - 1;
   // ---- 8. erosion, level 1 upwards, each cell against its receiver's new h;
   // receiver positions, F, reciprocal and uplifted h of the coming levels
   // stream into shared memory ahead of the sweep (same helper thread)
@@ -482,10 +530,11 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
   uint64_t* bare = s.bar + kFSlotsA;
   const uint32_t qe = Dl > 1 ? lvl(1) / kFChunk : 0u, ke_last = Dl > 1 ? (P1 - 1) / kFChunk - qe : 0u;
   uint32_t ke_next = 0;
+  uint32_t ke_done = 0;
   auto issue_e = [&](uint32_t limit) {
     for (; ke_next <= limit && ke_next <= ke_last; ++ke_next) {
       const uint32_t sl = ke_next % kFSlotsE;
-      if (ke_next >= kFSlotsE) mbar_wait(&bare[sl], ((ke_next - kFSlotsE) / kFSlotsE) & 1u);
+      if (ke_next >= kFSlotsE && ke_next - kFSlotsE >= ke_done) mbar_wait(&bare[sl], ((ke_next - kFSlotsE) / kFSlotsE) & 1u);
       const size_t p0 = (size_t)(qe + ke_next) * kFChunk;
       mbar_expect_tx(&bare[sl], kFChunk * 28);
       bulk_g2s(s.u.e.pp[sl], a.ppos + p0, kFChunk * 4, &bare[sl]);
@@ -495,7 +544,8 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
     }
   };
   auto wait_e = [&](uint32_t kl, uint32_t kh) {
-    for (uint32_t k = kl; k <= kh; ++k) mbar_wait(&bare[k % kFSlotsE], (k / kFSlotsE) & 1u);
+    for (uint32_t k = ke_done; k <= kh; ++k) mbar_wait(&bare[k % kFSlotsE], (k / kFSlotsE) & 1u);
+    ke_done = max(ke_done, kh + 1);
   };
   const long long ck1 = clock64();
   // carried level bounds: level d = [s0, e0), level d-1 = [ps, s0)
@@ -510,62 +560,65 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
     }
   }
   __syncthreads();
-  for (uint32_t d = 1; d < Dl; ++d) {
-    const uint32_t en = d + 1 < Dl ? lvl(d + 2 < Dl ? d + 2 : Dl) : e0;  // end of level d+1
-    const bool wide = e0 - s0 > kFRing, pwide = s0 - ps > kFRing;
-    const double* rp = s.u.e.h[(d - 1) & 1];
-    double* rc = s.u.e.h[d & 1];
-    for (uint32_t i = s0 + tid; i < e0; i += kFTPB) {
-      uint32_t p;
-      double F, y, h0;
-      if (staged) {
-        const uint32_t sl = (i / kFChunk - qe) % kFSlotsE, o = i % kFChunk;
-        p = s.u.e.pp[sl][o];
-        F = s.u.e.f[sl][o];
-        y = s.u.e.y[sl][o];
-        h0 = s.u.e.h0[sl][o];
-      } else {
-        p = __ldcg(a.ppos + i);
-        F = __ldcg(Fq + i);
-        y = __ldcg(Yq + i);
-        h0 = __ldcg(Hq + i);
+  if (act) {
+    for (uint32_t d = 1; d < Dl; ++d) {
+      const uint32_t en = d + 1 < Dl ? lvl(d + 2 < Dl ? d + 2 : Dl) : e0;  // end of level d+1
+      const bool wide = e0 - s0 > kFRing, pwide = s0 - ps > kFRing;
+      const double* rp = s.u.e.h[(d - 1) & 1];
+      double* rc = s.u.e.h[d & 1];
+      for (uint32_t i = s0 + tid; i < e0; i += nact) {
+        uint32_t p;
+        double F, y, h0;
+        if (staged) {
+          const uint32_t sl = (i / kFChunk - qe) % kFSlotsE, o = i % kFChunk;
+          p = s.u.e.pp[sl][o];
+          F = s.u.e.f[sl][o];
+          y = s.u.e.y[sl][o];
+          h0 = s.u.e.h0[sl][o];
+        } else {
+          p = __ldcg(a.ppos + i);
+          F = __ldcg(Fq + i);
+          y = __ldcg(Yq + i);
+          h0 = __ldcg(Hq + i);
+        }
+        const double hn = pwide ? __ldcg(Hq + p) : rp[p - ps];
+        int itn;
+        bool ok;
+        double hnew;
+        if (tab && F < 0x1p500)
+          hnew = newton_n1_tab(h0, hn, F, y, a.eps, a.maxit, itn, ok);
+        else if (NK == 1)
+          hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
+        else
+          hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, a.pow_fma, itn, ok);
+        if (ok) {
+          iters += (unsigned long long)itn;
+        } else {
+          hnew = h0;
+          atomicMin(&ctl->err_cell, __ldcg(a.order + i));
+          ctl->err_slot = ctl->slot;
+          atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+        }
+        __stcg(Hq + i, hnew);
+        if (!wide) rc[i - s0] = hnew;
       }
-      const double hn = pwide ? __ldcg(Hq + p) : rp[p - ps];
-      int itn;
-      bool ok;
-      double hnew;
-      if (tab && F < 0x1p500)
-        hnew = newton_n1_tab(h0, hn, F, y, a.eps, a.maxit, itn, ok);
-      else if (NK == 1)
-        hnew = newton_n1(h0, hn, F, a.eps, a.maxit, itn, ok);
-      else
-        hnew = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, a.pow_fma, itn, ok);
-      if (ok) {
-        iters += (unsigned long long)itn;
-      } else {
-        hnew = h0;
-        atomicMin(&ctl->err_cell, __ldcg(a.order + i));
-        ctl->err_slot = ctl->slot;
-        atomicMax(&ctl->err_flag, (uint32_t)LEMGPU_ECONVERGENCE);
+      // the next level (d+1) is staged when its chunks fit behind this level's first one
+      const uint32_t kl = s0 / kFChunk - qe, khn = (en - 1) / kFChunk - qe;
+      const bool staged_n = khn <= kl + kFSlotsE - 1;
+      if (tid == HT && d + 1 < Dl) {
+        issue_e(kl + kFSlotsE - 1);
+        if (staged_n) wait_e(e0 / kFChunk - qe, khn);
       }
-      __stcg(Hq + i, hnew);
-      if (!wide) rc[i - s0] = hnew;
+      named_bar_sync(1, nact);
+      ps = s0;
+      s0 = e0;
+      e0 = en;
+      staged = staged_n;
     }
-    // the next level (d+1) is staged when its chunks fit behind this level's first one
-    const uint32_t kl = s0 / kFChunk - qe, khn = (en - 1) / kFChunk - qe;
-    const bool staged_n = khn <= kl + kFSlotsE - 1;
-    if (tid == HT && d + 1 < Dl) {
-      issue_e(kl + kFSlotsE - 1);
-      if (staged_n) wait_e(e0 / kFChunk - qe, khn);
-    }
-    __syncthreads();
-    ps = s0;
-    s0 = e0;
-    e0 = en;
-    staged = staged_n;
   }
+  __syncthreads();
   if (tid == HT)
-    for (uint32_t k = ke_next > kFSlotsE ? ke_next - kFSlotsE : 0u; k < ke_next; ++k)
+    for (uint32_t k = max(ke_done, ke_next > kFSlotsE ? ke_next - kFSlotsE : 0u); k < ke_next; ++k)
       mbar_wait(&bare[k % kFSlotsE], (k / kFSlotsE) & 1u);
   flush_counters(ctl, iters, misses);
   if (tid == 0) {

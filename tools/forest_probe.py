@@ -25,6 +25,6 @@ buf = np.zeros(3 * 4096, np.uint32)
 ctx._check(ctx._L.lemgpu_debug_copy(ctx._h, 5, buf.ctypes.data, buf.nbytes))
 st = buf[4096:4096 + 8 * 148].reshape(148, 8).astype(np.int64)
 top = np.argsort(-(st[:, 4] + st[:, 7]))[:6]
-print("CTA: levels cells acc_unstaged acc_wide acc_kcyc ero_unstaged ero_wide ero_kcyc")
+print("CTA: levels cells acc_threads - acc_kcyc - - ero_kcyc")
 for b in top:
     print(b, list(st[b]), f"acc {st[b,4]*1024/1.965e3/max(st[b,0],1):.3f} us/level, ero {st[b,7]*1024/1.965e3/max(st[b,0],1):.3f} us/level")
