@@ -316,6 +316,184 @@ int lo_step(double* elev, int w, int h, int connectivity, const lo_params* p,
   return rc;
 }
 
+/* src/mfd.cpp:33-64 compute_mfd: every strictly lower in-bounds neighbour of
+ * an interior cell (stencil order) gets weight pow((e[c] - e[nb]) / dist,
+ * exponent), normalised by their sum (accumulated in stencil order). */
+void lo_compute_mfd(const double* elev, int w, int h, const lo_nbh* nbh, double exponent,
+                    uint32_t* recs, double* alpha, uint8_t* rnum) {
+  const size_t n = (size_t)w * h;
+  const int dmax = nbh->connectivity;
+  for (size_t c = 0; c < n; ++c) {
+    const size_t base = (size_t)dmax * c;
+    for (int i = 0; i < dmax; ++i) {
+      recs[base + i] = LO_NOFLOW;
+      alpha[base + i] = 0.0;
+    }
+    rnum[c] = 0;
+    if (is_perimeter(c, w, h)) continue;
+    const int x = (int)(c % (size_t)w), y = (int)(c / (size_t)w);
+    double wsum = 0.0;
+    int k = 0;
+    for (int i = 0; i < nbh->connectivity; ++i) {
+      const int nx = x + nbh->ox[i], ny = y + nbh->oy[i];
+      if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
+      const uint32_t nb = (uint32_t)ny * (uint32_t)w + (uint32_t)nx;
+      if (elev[nb] >= elev[c]) continue;  /* receivers must be strictly lower */
+      const double slope = (elev[c] - elev[nb]) / nbh->dist[i];
+      const double wt = pow(slope, exponent);
+      recs[base + k] = nb;
+      alpha[base + k] = wt;
+      wsum += wt;
+      ++k;
+    }
+    rnum[c] = (uint8_t)k;
+    for (int i = 0; i < k; ++i) alpha[base + i] /= wsum;
+  }
+}
+
+/* src/mfd.cpp:8-31 build_mfd_donor_table: donors of each cell in ascending
+ * donor order (cells visited in ascending order). */
+static void lo_mfd_donors(size_t n, int dmax, const uint32_t* recs, const double* alpha,
+                          const uint8_t* rnum, uint32_t* donors, double* dalpha, uint8_t* dnum) {
+  memset(dnum, 0, n);
+  for (size_t c = 0; c < n; ++c) {
+    const size_t base = (size_t)dmax * c;
+    for (int k = 0; k < rnum[c]; ++k) {
+      const uint32_t r = recs[base + k];
+      const size_t slot = (size_t)dmax * r + dnum[r];
+      donors[slot] = (uint32_t)c;
+      dalpha[slot] = alpha[base + k];
+      ++dnum[r];
+    }
+  }
+}
+
+static int lo_u32_less(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* src/mfd.cpp:66-104 generate_mfd_order: level 0 = cells without receivers
+ * (ascending); a cell joins the wave after its last receiver is placed; each
+ * level sorted ascending. */
+int lo_mfd_order(size_t n, int dmax, const uint32_t* recs, const uint8_t* rnum, uint32_t* order,
+                 uint32_t* levels, uint32_t* nlevels) {
+  uint32_t* donors = (uint32_t*)malloc(n * dmax * sizeof(uint32_t));
+  double* dalpha = (double*)malloc(n * dmax * sizeof(double));
+  uint8_t* dnum = (uint8_t*)malloc(n);
+  uint8_t* remaining = (uint8_t*)malloc(n);
+  double* zero = (double*)calloc(n * dmax, sizeof(double));
+  lo_mfd_donors(n, dmax, recs, zero, rnum, donors, dalpha, dnum);
+  memcpy(remaining, rnum, n);
+  size_t len = 0;
+  uint32_t nl = 0;
+  levels[nl++] = 0;
+  for (size_t c = 0; c < n; ++c)
+    if (remaining[c] == 0) order[len++] = (uint32_t)c;
+  levels[nl++] = (uint32_t)len;
+  size_t lo = 0, hi = len;
+  while (lo < hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      const uint32_t c = order[i];
+      for (int k = 0; k < dnum[c]; ++k) {
+        const uint32_t d = donors[(size_t)dmax * c + k];
+        if (--remaining[d] == 0) order[len++] = d;
+      }
+    }
+    qsort(order + hi, len - hi, sizeof(uint32_t), lo_u32_less);
+    lo = hi;
+    hi = len;
+    if (hi > lo) levels[nl++] = (uint32_t)hi;
+  }
+  *nlevels = nl - 1;
+  free(donors);
+  free(dalpha);
+  free(dnum);
+  free(remaining);
+  free(zero);
+  return len == n ? LO_OK : LO_ESTRUCTURE;
+}
+
+/* src/mfd.cpp:106-132 accumulate_mfd_into / accumulate_mfd and
+ * include/lem/mfd.hpp:62-69 add_mfd_donor_flow. */
+void lo_accumulate_mfd(size_t n, int dmax, const uint32_t* recs, const double* alpha,
+                       const uint8_t* rnum, const uint32_t* order, const uint32_t* levels,
+                       uint32_t nlevels, double w0, double* A) {
+  uint32_t* donors = (uint32_t*)malloc(n * dmax * sizeof(uint32_t));
+  double* dalpha = (double*)malloc(n * dmax * sizeof(double));
+  uint8_t* dnum = (uint8_t*)malloc(n);
+  lo_mfd_donors(n, dmax, recs, alpha, rnum, donors, dalpha, dnum);
+  for (size_t c = 0; c < n; ++c) A[c] = w0;
+  for (uint32_t l = nlevels; l-- > 0;) {
+    for (uint32_t i = levels[l]; i < levels[l + 1]; ++i) {
+      const uint32_t c = order[i];
+      const size_t base = (size_t)dmax * c;
+      double a = A[c];
+      for (int k = 0; k < dnum[c]; ++k) a += dalpha[base + k] * A[donors[base + k]];
+      A[c] = a;
+    }
+  }
+  free(donors);
+  free(dalpha);
+  free(dnum);
+}
+
+/* src/simulation.cpp:31-89 with Routing::kMfd: D8 receivers, donors and
+ * queue (erosion follows the D8 receiver), MFD graph on the pre-uplift
+ * elevation, MFD plan and accumulation, uplift, erosion. */
+int lo_step_mfd(double* elev, int w, int h, int connectivity, const lo_params* p, double exponent,
+                lo_step_out* out, uint32_t* mfd_order, uint32_t* mfd_levels, uint32_t* mfd_nlevels) {
+  lo_nbh nbh;
+  if (lo_make_nbh(connectivity, p->dx, p->dy, &nbh) != LO_OK) return LO_ECONFIG;
+  const size_t n = (size_t)w * h;
+  const int dmax = connectivity;
+  uint32_t* rec = out->rec ? out->rec : (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* donor = out->donor ? out->donor : (uint32_t*)malloc(n * dmax * sizeof(uint32_t));
+  uint8_t* dnum = out->dnum ? out->dnum : (uint8_t*)malloc(n);
+  uint32_t* order = out->order ? out->order : (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* levels = out->levels ? out->levels : (uint32_t*)malloc((n + 2) * sizeof(uint32_t));
+  double* A = out->A ? out->A : (double*)malloc(n * sizeof(double));
+  uint32_t* recs = (uint32_t*)malloc(n * dmax * sizeof(uint32_t));
+  double* alpha = (double*)malloc(n * dmax * sizeof(double));
+  uint8_t* rnum = (uint8_t*)malloc(n);
+  uint32_t* morder = mfd_order ? mfd_order : (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* mlevels = mfd_levels ? mfd_levels : (uint32_t*)malloc((n + 2) * sizeof(uint32_t));
+  uint32_t mnl = 0;
+  int rc = LO_OK;
+
+  lo_receivers(elev, w, h, &nbh, rec);
+  uint32_t pits = 0;
+  for (size_t c = 0; c < n; ++c)
+    if (rec[c] == LO_NOFLOW && !is_perimeter(c, w, h)) ++pits;
+  out->interior_noflow = pits;
+  lo_donors(rec, w, h, &nbh, donor, dnum);
+  rc = lo_generate_queue(n, rec, donor, dnum, dmax, order, levels, &out->nlevels);
+  if (rc == LO_OK) {
+    lo_compute_mfd(elev, w, h, &nbh, exponent, recs, alpha, rnum);
+    rc = lo_mfd_order(n, dmax, recs, rnum, morder, mlevels, &mnl);
+  }
+  if (rc == LO_OK) {
+    lo_accumulate_mfd(n, dmax, recs, alpha, rnum, morder, mlevels, mnl, p->dx * p->dy, A);
+    lo_uplift(elev, w, h, p->uplift_rate * p->dt);
+    out->err_cell = LO_NOFLOW;
+    rc = lo_erode(elev, w, h, &nbh, order, levels, out->nlevels, rec, A, p, &out->newton_iters,
+                  &out->err_cell);
+  }
+  if (mfd_nlevels) *mfd_nlevels = mnl;
+  if (!out->rec) free(rec);
+  if (!out->donor) free(donor);
+  if (!out->dnum) free(dnum);
+  if (!out->order) free(order);
+  if (!out->levels) free(levels);
+  if (!out->A) free(A);
+  if (!mfd_order) free(morder);
+  if (!mfd_levels) free(mlevels);
+  free(recs);
+  free(alpha);
+  free(rnum);
+  return rc;
+}
+
 /* src/scheduler.cpp:466-500 -- run_simulation loop (rb_serial strategy). */
 int lo_run(double* elev, int w, int h, int connectivity, const lo_params* p, uint32_t steps,
            uint64_t* newton_total, uint32_t* err_cell) {

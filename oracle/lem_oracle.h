@@ -93,6 +93,25 @@ int lo_step(double* elev, int w, int h, int connectivity, const lo_params* p,
 int lo_run(double* elev, int w, int h, int connectivity, const lo_params* p, uint32_t steps,
            uint64_t* newton_total, uint32_t* err_cell);
 
+/* Multiple-flow-direction routing (src/mfd.cpp, include/lem/mfd.hpp).
+ * recs / alpha: N*dmax receiver slots (stencil order) and their normalised
+ * weights; rnum: receivers per cell.  dmax = connectivity. */
+void lo_compute_mfd(const double* elev, int w, int h, const lo_nbh* nbh, double exponent,
+                    uint32_t* recs, double* alpha, uint8_t* rnum);
+/* Dependency-counting level order; levels needs n+2 entries. LO_ESTRUCTURE on a cycle. */
+int lo_mfd_order(size_t n, int dmax, const uint32_t* recs, const uint8_t* rnum, uint32_t* order,
+                 uint32_t* levels, uint32_t* nlevels);
+/* A = w0 + alpha-weighted donor pulls in ascending donor order, last level first. */
+void lo_accumulate_mfd(size_t n, int dmax, const uint32_t* recs, const double* alpha,
+                       const uint8_t* rnum, const uint32_t* order, const uint32_t* levels,
+                       uint32_t nlevels, double w0, double* A);
+/* simulate_step with StepSetup::routing = kMfd (src/simulation.cpp:31-89):
+ * the D8 plan erodes, the MFD accumulation feeds it.  out as lo_step (A = the
+ * MFD drainage area); mfd_order / mfd_levels (N, N+2; may be NULL) receive
+ * the MFD plan. */
+int lo_step_mfd(double* elev, int w, int h, int connectivity, const lo_params* p, double exponent,
+                lo_step_out* out, uint32_t* mfd_order, uint32_t* mfd_levels, uint32_t* mfd_nlevels);
+
 /* Priority-Flood depression filling (src/depressions.cpp:26-68,
  * include/lem/depressions.hpp:8-27): mode 0 off, 1 exact (raise to the spill
  * elevation), 2 epsilon ascending (spill + eps).  A binary min-heap over

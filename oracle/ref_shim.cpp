@@ -128,6 +128,66 @@ int lr_simulate_step(int w, int h, int connectivity, const LrParams* p, double* 
       err_cell);
 }
 
+// One lem::simulate_step with StepSetup::routing = kMfd (src/simulation.cpp:
+// 31-89): h, the MFD drainage area (ws.accum) and the MFD plan (ws.mfd_plan).
+int lr_simulate_step_mfd(int w, int h, int connectivity, const LrParams* p, double exponent, double* elev,
+                         double* A, std::uint32_t* mfd_order, std::uint32_t* mfd_levels,
+                         std::uint32_t* mfd_nlevels, std::uint64_t* newton, std::uint32_t* err_cell) {
+  return guarded(
+      [&] {
+        const std::size_t n = static_cast<std::size_t>(w) * h;
+        lem::Raster<double> r(w, h, std::vector<double>(elev, elev + n));
+        const lem::Neighborhood nbh = lem::Neighborhood::make(connectivity, p->dx, p->dy);
+        const lem::GridGraph g(w, h, nbh);
+        lem::SimParams sp = to_params(p);
+        sp.validate();
+        lem::SimWorkspace ws;
+        lem::StepSetup setup;
+        setup.routing = lem::Routing::kMfd;
+        setup.mfd_exponent = exponent;
+        lem::StepDiagnostics d;
+        try {
+          d = lem::simulate_step(r, g, sp, setup, ws);
+        } catch (...) {
+          std::memcpy(elev, r.storage().data(), n * sizeof(double));
+          throw;
+        }
+        std::memcpy(elev, r.storage().data(), n * sizeof(double));
+        if (A) std::memcpy(A, ws.accum.values.storage().data(), n * sizeof(double));
+        if (mfd_order) std::memcpy(mfd_order, ws.mfd_plan.order.data(), n * 4);
+        if (mfd_levels) std::memcpy(mfd_levels, ws.mfd_plan.levels.data(), ws.mfd_plan.levels.size() * 4);
+        if (mfd_nlevels) *mfd_nlevels = static_cast<std::uint32_t>(ws.mfd_plan.nlevels());
+        if (newton) *newton = d.newton_iters;
+      },
+      err_cell);
+}
+
+// run_simulation with a routing choice (0 d8, 1 mfd) and MFD exponent.
+int lr_run_routing(int w, int h, int connectivity, const LrParams* p, const char* strategy,
+                   std::uint32_t workers, std::uint32_t steps, int routing, double exponent, double* elev,
+                   std::uint64_t* newton, std::uint32_t* err_cell) {
+  return guarded(
+      [&] {
+        const std::size_t n = static_cast<std::size_t>(w) * h;
+        auto kind = lem::strategy_from_string(strategy);
+        if (!kind) throw lem::ConfigError(std::string("unknown strategy ") + strategy);
+        lem::RunConfig cfg;
+        cfg.width = static_cast<std::uint32_t>(w);
+        cfg.height = static_cast<std::uint32_t>(h);
+        cfg.timesteps = steps;
+        cfg.strategy = {*kind, workers};
+        cfg.params = to_params(p);
+        cfg.connectivity = connectivity;
+        cfg.routing = routing ? lem::Routing::kMfd : lem::Routing::kD8;
+        cfg.mfd_exponent = exponent;
+        lem::Raster<double> r(w, h, std::vector<double>(elev, elev + n));
+        lem::RunResult res = lem::run_simulation(std::move(r), cfg);
+        std::memcpy(elev, res.elevation.storage().data(), n * sizeof(double));
+        if (newton) *newton = res.newton_iters;
+      },
+      err_cell);
+}
+
 // lem::run_simulation(Raster initial, cfg) under a named strategy.
 // seconds_out receives the wall time of the stepping loop.
 int lr_run(int w, int h, int connectivity, const LrParams* p, const char* strategy,
@@ -159,9 +219,21 @@ int lr_run(int w, int h, int connectivity, const LrParams* p, const char* strate
 // including the per-step FlowGraph::resize the phase timers miss.
 // fill_mode: 0 off, 1 exact, 2 epsilon ascending (run_simulation's
 // generate_terrain + priority_flood_fill, scheduler.cpp:503-506)
+int lr_bench_routing(int w, int h, int connectivity, const LrParams* p, const char* strategy,
+                     std::uint32_t workers, std::uint64_t seed, std::uint32_t warmup, std::uint32_t steps,
+                     double* seconds, std::uint64_t* newton, int fill_mode, double fill_eps, int routing,
+                     double exponent);
 int lr_bench(int w, int h, int connectivity, const LrParams* p, const char* strategy,
              std::uint32_t workers, std::uint64_t seed, std::uint32_t warmup, std::uint32_t steps,
              double* seconds, std::uint64_t* newton, int fill_mode, double fill_eps) {
+  return lr_bench_routing(w, h, connectivity, p, strategy, workers, seed, warmup, steps, seconds, newton, fill_mode,
+                          fill_eps, 0, 1.0);
+}
+// ... with StepSetup::routing (0 d8, 1 mfd) and the MFD exponent
+int lr_bench_routing(int w, int h, int connectivity, const LrParams* p, const char* strategy,
+                     std::uint32_t workers, std::uint64_t seed, std::uint32_t warmup, std::uint32_t steps,
+                     double* seconds, std::uint64_t* newton, int fill_mode, double fill_eps, int routing,
+                     double exponent) {
   return guarded(
       [&] {
         auto kind = lem::strategy_from_string(strategy);
@@ -178,6 +250,8 @@ int lr_bench(int w, int h, int connectivity, const LrParams* p, const char* stra
         const lem::SimParams sp = to_params(p);
         lem::StepSetup setup;
         setup.order = lem::uses_stack_order(*kind) ? lem::OrderKind::kStack : lem::OrderKind::kQueue;
+        setup.routing = routing ? lem::Routing::kMfd : lem::Routing::kD8;
+        setup.mfd_exponent = exponent;
         const lem::Strategy st{*kind, workers};
         lem::SimWorkspace ws;
         std::uint64_t it = 0;

@@ -81,6 +81,8 @@ class Oracle:
                                             C.c_void_p, C.c_void_p]
         L.lo_donors_explicit.argtypes = [C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p]
+        L.lo_step_mfd.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_double,
+                                  C.POINTER(lo_step_out), C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32)]
         self.L = L
 
     @classmethod
@@ -130,6 +132,25 @@ class Oracle:
         out["err_cell"] = so.err_cell
         return out
 
+    def step_mfd(self, elev: np.ndarray, exponent=1.0, conn=8, params=None):
+        """One reference step with StepSetup::routing = kMfd (simulation.cpp:31-89):
+        A is the MFD drainage area; mfd_order / mfd_levels the MFD plan."""
+        h, w = elev.shape
+        n = w * h
+        p = params or make_params()
+        out = {"rec": np.empty(n, np.uint32), "order": np.empty(n, np.uint32), "levels": np.empty(n + 2, np.uint32),
+               "A": np.empty(n, np.float64), "mfd_order": np.empty(n, np.uint32),
+               "mfd_levels": np.empty(n + 2, np.uint32)}
+        so = lo_step_out(_p(out["rec"]), None, None, _p(out["order"]), _p(out["levels"]), 0, _p(out["A"]), 0, 0, NOFLOW)
+        mnl = C.c_uint32(0)
+        rc = self.L.lo_step_mfd(elev.ctypes.data, w, h, conn, C.byref(p), exponent, C.byref(so),
+                                _p(out["mfd_order"]), _p(out["mfd_levels"]), C.byref(mnl))
+        out.update(status=rc, nlevels=so.nlevels, newton_iters=so.newton_iters, interior_noflow=so.interior_noflow,
+                   err_cell=so.err_cell, mfd_nlevels=mnl.value)
+        out["levels"] = out["levels"][: so.nlevels + 1].copy()
+        out["mfd_levels"] = out["mfd_levels"][: mnl.value + 1].copy()
+        return out
+
     def run(self, elev: np.ndarray, steps: int, conn=8, params=None):
         h, w = elev.shape
         p = params or make_params()
@@ -161,6 +182,13 @@ class RefLib:
         L.lr_fill.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_void_p]
         L.lr_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32, C.c_uint64,
                                C.c_uint32, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.c_double]
+        L.lr_bench_routing.argtypes = L.lr_bench.argtypes + [C.c_int, C.c_double]
+        L.lr_simulate_step_mfd.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_double, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32),
+                                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
+        L.lr_run_routing.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(lo_params), C.c_char_p, C.c_uint32,
+                                     C.c_uint32, C.c_int, C.c_double, C.c_void_p, C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_uint32)]
         self.L = L
 
     @classmethod
@@ -192,25 +220,45 @@ class RefLib:
         out["levels"] = out["levels"][: nl.value + 1].copy()
         return out
 
-    def run(self, elev: np.ndarray, steps: int, strategy="rb_serial", workers=1, conn=8, params=None):
+    def step_mfd(self, elev: np.ndarray, exponent=1.0, conn=8, params=None):
+        """lem::simulate_step with routing = kMfd: h, MFD A and the MFD plan."""
+        h, w = elev.shape
+        n = w * h
+        p = params or make_params()
+        out = {"A": np.empty(n, np.float64), "mfd_order": np.empty(n, np.uint32), "mfd_levels": np.empty(n + 2, np.uint32)}
+        nl, nt, ec = C.c_uint32(0), C.c_uint64(0), C.c_uint32(NOFLOW)
+        rc = self.L.lr_simulate_step_mfd(w, h, conn, C.byref(p), exponent, elev.ctypes.data, _p(out["A"]),
+                                         _p(out["mfd_order"]), _p(out["mfd_levels"]), C.byref(nl), C.byref(nt),
+                                         C.byref(ec))
+        out.update(status=rc, mfd_nlevels=nl.value, newton_iters=nt.value, err_cell=ec.value)
+        out["mfd_levels"] = out["mfd_levels"][: nl.value + 1].copy()
+        return out
+
+    def run(self, elev: np.ndarray, steps: int, strategy="rb_serial", workers=1, conn=8, params=None, routing=0,
+            mfd_exponent=1.0):
         h, w = elev.shape
         p = params or make_params()
         nt, ec = C.c_uint64(0), C.c_uint32(NOFLOW)
-        rc = self.L.lr_run(w, h, conn, C.byref(p), strategy.encode(), workers, steps, elev.ctypes.data,
-                           C.byref(nt), C.byref(ec))
+        if routing:
+            rc = self.L.lr_run_routing(w, h, conn, C.byref(p), strategy.encode(), workers, steps, int(routing),
+                                       float(mfd_exponent), elev.ctypes.data, C.byref(nt), C.byref(ec))
+        else:
+            rc = self.L.lr_run(w, h, conn, C.byref(p), strategy.encode(), workers, steps, elev.ctypes.data,
+                               C.byref(nt), C.byref(ec))
         if rc not in (0, 3):
             raise RuntimeError(self.L.lr_last_error().decode())
         return rc, nt.value, ec.value
 
     def bench(self, w, h, steps, warmup=0, strategy="rb_private_queues", workers=None, seed=42, conn=8, params=None,
-              fill=0, fill_eps=1e-8):
+              fill=0, fill_eps=1e-8, routing=0, mfd_exponent=1.0):
         """Per-step wall seconds of lem::strategy_step on a persistent workspace
         (fill: 0 off, 1 exact, 2 epsilon -- lem::priority_flood_fill first)."""
         p = params or make_params()
         secs = np.zeros(max(1, steps), np.float64)
         nt = C.c_uint64(0)
-        rc = self.L.lr_bench(w, h, conn, C.byref(p), strategy.encode(), workers or self.max_threads(), seed, warmup,
-                             steps, secs.ctypes.data, C.byref(nt), int(fill), float(fill_eps))
+        rc = self.L.lr_bench_routing(w, h, conn, C.byref(p), strategy.encode(), workers or self.max_threads(), seed,
+                                     warmup, steps, secs.ctypes.data, C.byref(nt), int(fill), float(fill_eps),
+                                     int(routing), float(mfd_exponent))
         if rc != 0:
             raise RuntimeError(self.L.lr_last_error().decode())
         return secs[:steps], nt.value

@@ -9,10 +9,13 @@ writes:
   small_*.npz         complete step-1 outputs of small rasters (every array)
   fill_*.npz          lem::priority_flood_fill of small rasters (exact and
                       epsilon-ascending modes)
+  mfd_*.npz           lem::simulate_step with StepSetup::routing = kMfd:
+                      h after the step, the MFD drainage area and MFD plan
 
 Usage:  python tests/golden/make_golden.py [--big] [--big120] [--fill-only]
   --big     add the 10000^2 step-1 anchors (~1 min, 6 GB RAM)
   --big120  add the 10000^2 120-step anchor (rb_private_queues, ~10 min)
+  --mfd-only  only the mfd_*.npz fixtures
 """
 from __future__ import annotations
 
@@ -79,13 +82,41 @@ def fill_goldens(ref: RefLib):
         np.savez_compressed(HERE / f"{name}.npz", w=w, h=h, seed=seed, mode=mode, eps=eps, h0=e0, f=f)
 
 
+MFD = [
+    # name, w, h, seed, conn, exponent, params
+    ("d8_e1_40x30_s3", 40, 30, 3, 8, 1.0, {}),
+    ("d8_e1_64x48_s42", 64, 48, 42, 8, 1.0, {}),
+    ("d8_e11_33x29_s5", 33, 29, 5, 8, 1.1, {}),
+    ("d8_e2_25x25_s2", 25, 25, 2, 8, 2.0, {}),
+    ("d4_e1_30x22_s5", 30, 22, 5, 4, 1.0, {}),
+    ("d8_aniso_e1_33x21_s7", 33, 21, 7, 8, 1.0, {"dx": 0.5, "dy": 2.0}),
+    ("d8_n2_e1_48x36_s13", 48, 36, 13, 8, 1.0, {"n_exp": 2.0}),
+]
+
+
+def mfd_goldens(ref: RefLib):
+    for name, w, h, seed, conn, ex, kw in MFD:
+        p = make_params(**kw)
+        e0 = ref.terrain(w, h, seed)
+        e = e0.copy()
+        s = ref.step_mfd(e, exponent=ex, conn=conn, params=p)
+        assert s["status"] == 0, name
+        np.savez_compressed(
+            HERE / f"mfd_{name}.npz", w=w, h=h, seed=seed, conn=conn, exponent=ex, params=json.dumps(kw), h0=e0,
+            h1=e, A=s["A"], mfd_order=s["mfd_order"], mfd_levels=s["mfd_levels"], newton_iters=s["newton_iters"])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--big120", action="store_true")
     ap.add_argument("--fill-only", action="store_true")
+    ap.add_argument("--mfd-only", action="store_true")
     args = ap.parse_args()
     ref = RefLib.get()
+    mfd_goldens(ref)
+    if args.mfd_only:
+        return
     fill_goldens(ref)
     if args.fill_only:
         return

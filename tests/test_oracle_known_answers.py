@@ -241,3 +241,97 @@ def test_terrain_splitmix_canary(oracle):
     assert a.min() >= 0.0 and a.max() < 1.0
     z = oracle.L.lo_splitmix64(42)
     assert a.ravel()[0] == (z >> 11) * 2.0 ** -53
+
+
+# ---- MFD (proj/tests/test_mfd.cpp, acceptance.cpp:283-327) -------------------
+
+def _mfd(oracle, r, exponent=1.0):
+    import ctypes as C
+    h, w = r.shape
+    n = w * h
+    nbh = _nbh(oracle, 8)
+    recs = np.empty(n * 8, np.uint32)
+    alpha = np.empty(n * 8, np.float64)
+    rnum = np.empty(n, np.uint8)
+    oracle.L.lo_compute_mfd.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+    oracle.L.lo_compute_mfd(np.ascontiguousarray(r).ctypes.data, w, h, C.addressof(nbh), exponent,
+                            recs.ctypes.data, alpha.ctypes.data, rnum.ctypes.data)
+    return recs.reshape(n, 8), alpha.reshape(n, 8), rnum
+
+
+def _nbh(oracle, conn, dx=1.0, dy=1.0):
+    import ctypes as C
+
+    class lo_nbh(C.Structure):
+        _fields_ = [("connectivity", C.c_int), ("ox", C.c_int * 8), ("oy", C.c_int * 8), ("dist", C.c_double * 8),
+                    ("dx", C.c_double), ("dy", C.c_double)]
+
+    nb = lo_nbh()
+    oracle.L.lo_make_nbh.argtypes = [C.c_int, C.c_double, C.c_double, C.c_void_p]
+    assert oracle.L.lo_make_nbh(conn, dx, dy, C.addressof(nb)) == 0
+    return nb
+
+
+def test_mfd_single_downslope_neighbor(oracle):
+    """test_mfd.cpp 'single downslope neighbor gets the whole weight'."""
+    r = np.full((3, 3), 5.0)
+    r[1, 1] = 3.0
+    r[0, 1] = 1.0
+    recs, alpha, rnum = _mfd(oracle, r)
+    assert rnum[4] == 1 and recs[4, 0] == 1 and alpha[4, 0] == 1.0
+
+
+def test_mfd_two_cardinals_split(oracle):
+    """test_mfd.cpp 'two downslope cardinals split 1/3 and 2/3 at exponent 1' (1/5, 4/5 at 2)."""
+    r = np.full((3, 3), 9.0)
+    r[1, 1] = 2.0
+    r[0, 1] = 1.0  # north, slope 1
+    r[1, 0] = 0.0  # west, slope 2
+    recs, alpha, rnum = _mfd(oracle, r, 1.0)
+    assert rnum[4] == 2 and recs[4, 0] == 1 and recs[4, 1] == 3  # stencil order: (0,-1) before (-1,0)
+    assert abs(alpha[4, 0] - 1 / 3) < 1e-15 and abs(alpha[4, 1] - 2 / 3) < 1e-15
+    recs, alpha, rnum = _mfd(oracle, r, 2.0)
+    assert abs(alpha[4, 0] - 0.2) < 1e-15 and abs(alpha[4, 1] - 0.8) < 1e-15
+
+
+def test_mfd_pits_and_perimeter_have_no_receivers(oracle):
+    r = np.full((5, 5), 4.0)
+    r[2, 2] = 1.0
+    recs, alpha, rnum = _mfd(oracle, r)
+    assert rnum[12] == 0
+    per = np.ones((5, 5), bool)
+    per[1:-1, 1:-1] = False
+    assert (rnum[per.ravel()] == 0).all()
+
+
+def test_mfd_weights_sum_to_one_receivers_lower(oracle):
+    r = oracle.terrain(30, 30, 21)
+    recs, alpha, rnum = _mfd(oracle, r, 1.1)
+    e = r.ravel()
+    for c in range(900):
+        k = rnum[c]
+        assert all(e[recs[c, i]] < e[c] for i in range(k))
+        if k:
+            assert abs(alpha[c, :k].sum() - 1.0) < 1e-12
+
+
+def test_mfd_plan_is_a_level_order_and_mass_conserving(oracle):
+    """acceptance.cpp:283-300 criterion 8 (first half): every cell sits strictly
+    above all of its receivers in the MFD level order; the MFD drainage area
+    reaching level 0 is the whole raster's area."""
+    for seed in range(1, 6):
+        e = oracle.terrain(50, 50, seed)
+        r0 = e.copy()
+        s = oracle.step_mfd(e)
+        assert s["status"] == 0
+        lvl = np.empty(2500, np.int64)
+        lv = s["mfd_levels"]
+        for l in range(len(lv) - 1):
+            lvl[s["mfd_order"][lv[l]:lv[l + 1]]] = l
+        recs, alpha, rnum = _mfd(oracle, r0)
+        for c in range(2500):
+            for i in range(rnum[c]):
+                assert lvl[c] > lvl[recs[c, i]], (seed, c)
+        sinks = s["mfd_order"][lv[0]:lv[1]]
+        assert abs(s["A"][sinks].sum() - 2500.0) < 1e-8

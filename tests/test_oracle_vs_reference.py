@@ -100,3 +100,42 @@ def test_fill_vs_reference_live(oracle, mode):
         assert np.array_equal(oracle.fill(e, mode).view(np.uint64), ref.fill(e, mode).view(np.uint64)), seed
     e = ref.terrain(400, 300, 77)
     assert np.array_equal(oracle.fill(e, mode).view(np.uint64), ref.fill(e, mode).view(np.uint64))
+
+
+def test_mfd_golden_fixtures(oracle, golden_dir):
+    """The oracle's MFD restatement (compute_mfd / generate_mfd_order /
+    accumulate_mfd, src/mfd.cpp:33-132, inside simulate_step with
+    Routing::kMfd) against fixtures made by the unmodified reference: h,
+    the MFD drainage area and the MFD plan bit for bit."""
+    cases = sorted(golden_dir.glob("mfd_*.npz"))
+    assert len(cases) >= 7
+    for path in cases:
+        g = np.load(path)
+        kw = json.loads(str(g["params"]))
+        e = g["h0"].copy()
+        s = oracle.step_mfd(e, exponent=float(g["exponent"]), conn=int(g["conn"]), params=make_params(**kw))
+        assert s["status"] == 0, path.name
+        assert np.array_equal(s["A"].view(np.uint64), g["A"].view(np.uint64)), path.name
+        assert np.array_equal(s["mfd_order"], g["mfd_order"]) and np.array_equal(s["mfd_levels"], g["mfd_levels"])
+        assert np.array_equal(e.view(np.uint64), g["h1"].view(np.uint64)), path.name
+        assert s["newton_iters"] == int(g["newton_iters"]), path.name
+
+
+@pytest.mark.skipif(not RefLib.available(), reason="reference library not built")
+@pytest.mark.parametrize("w,h,seed,conn,ex,kw", [
+    (90, 70, 21, 8, 1.0, {}), (61, 47, 22, 8, 1.3, {"m_exp": 0.4}), (50, 50, 23, 4, 1.0, {}),
+    (40, 64, 24, 8, 0.7, {"dx": 2.0, "dy": 0.5}), (120, 33, 25, 8, 1.0, {"n_exp": 2.0}),
+])
+def test_mfd_live_vs_reference(oracle, w, h, seed, conn, ex, kw):
+    ref = RefLib.get()
+    p = make_params(**kw)
+    e1 = ref.terrain(w, h, seed)
+    e2 = e1.copy()
+    for _ in range(3):
+        r = ref.step_mfd(e1, exponent=ex, conn=conn, params=p)
+        o = oracle.step_mfd(e2, exponent=ex, conn=conn, params=p)
+        assert r["status"] == o["status"] == 0
+        assert np.array_equal(r["A"].view(np.uint64), o["A"].view(np.uint64))
+        assert np.array_equal(r["mfd_order"], o["mfd_order"]) and np.array_equal(r["mfd_levels"], o["mfd_levels"])
+        assert np.array_equal(e1.view(np.uint64), e2.view(np.uint64))
+        assert r["newton_iters"] == o["newton_iters"]
