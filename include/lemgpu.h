@@ -179,6 +179,21 @@ int lemgpu_generate_terrain(lemgpu_ctx* ctx, const uint64_t* seeds);
 enum { LEMGPU_FILL_OFF = 0, LEMGPU_FILL_EXACT = 1, LEMGPU_FILL_EPSILON = 2 };
 int lemgpu_fill(lemgpu_ctx* ctx, int mode, double epsilon);
 
+/* StepSetup::routing / mfd_exponent (proj/include/lem/simulation.hpp:55-60,
+ * config.hpp:14-32): routing 0 = d8/d4 (the receiver of the neighbourhood),
+ * 1 = kMfd -- the drainage area that feeds the erosion is the slope-weighted
+ * multiple-flow accumulation (compute_mfd / generate_mfd_order /
+ * accumulate_mfd, proj/src/mfd.cpp:33-132) while the erosion still follows
+ * the D8 receiver.  mfd_exponent must be > 0 (config.cpp:166) -> ECONFIG.
+ * Replaces: the Routing::kMfd branch of simulate_front (simulation.cpp:53-60)
+ * and step_rb_par_all (scheduler.cpp:248-254). */
+int lemgpu_set_routing(lemgpu_ctx* ctx, int routing, double mfd_exponent);
+
+/* The MFD drainage area and plan of the last step (routing = 1): A[N] =
+ * ws.accum, order[N] / levels[nlevels + 1] = ws.mfd_plan (level-major,
+ * ascending within a level, mfd.cpp:66-104).  Any pointer may be NULL. */
+int lemgpu_download_mfd(lemgpu_ctx* ctx, double* A, uint32_t* order, uint32_t* levels, uint32_t* nlevels);
+
 /* ---- stepping ---------------------------------------------------------- */
 
 /* Run nsteps timesteps with the elevation device-resident, then synchronise.

@@ -95,6 +95,8 @@ _SIGS = {
     "lemgpu_snapshot_async": (C.c_int, [_P, _P, C.POINTER(lemgpu_diag)]),
     "lemgpu_snapshot_wait": (C.c_int, [_P]),
     "lemgpu_download_graph": (C.c_int, [_P, _P, _P, _P, _P, _P, C.POINTER(C.c_uint32), _P]),
+    "lemgpu_set_routing": (C.c_int, [_P, C.c_int, C.c_double]),
+    "lemgpu_download_mfd": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_uint32)]),
     "lemgpu_member_stats_device": (C.c_int, [_P, _P]),
     "lemgpu_shard_members": (C.c_int, [C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "lemgpu_create_ensemble_shard": (

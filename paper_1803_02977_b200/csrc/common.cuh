@@ -174,6 +174,7 @@ struct Ctl {
   uint32_t nr_l, nr_lo, nr_hi, nr_done;  // k_esc_bfs: where a narrow run handed back to the grid
   uint32_t fr_flag[3], fr_maxd;          // k_esc_forest: pointer-jumping round flags, deepest escaped level
   uint32_t fr_rounds, fr_maxcells;       // ... rounds taken, most cells of one CTA
+  uint32_t mfd_cnt[3], mfd_nlev;         // k_mfd_levels: per-level append counters, MFD plan levels
   unsigned long long fr_t[3];            // ... latest end over the CTAs of the counts, F and erosion sweeps
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
@@ -253,6 +254,15 @@ struct StepArgs {
   uint32_t* fbins;   // [owner CTA][depth] counts / cursors (the global path's levels array, N + 2)
   uint32_t cb_cap;   // entries of cbound (k_esc_forest: level starts)
   double* hx;        // position-major elevations (k_esc_forest)
+  // MFD routing (k_mfd.cuh; mfd_A != nullptr: the erosion reads this drainage area)
+  double* mfd_A;      // cell-major MFD drainage area
+  double* mfd_wsum;   // cell-major sum of the receiver weights
+  uint8_t* mfd_lm;    // cell-major mask of strictly lower neighbours (the MFD receivers)
+  uint32_t* mfd_rem;  // receiver countdown of the dependency-counting plan
+  uint32_t* mfd_ord;  // the MFD plan, level-major (any order within a level)
+  uint32_t* mfd_lv;   // its level starts
+  uint32_t* mfd_lev;  // cell-major level (for the export)
+  double mfd_exp;     // StepSetup::mfd_exponent
   uint8_t* dbg_level;  // debug capture (nullptr: off): level of every cell k_tiles finishes (escaped: untouched)
   double* dbg_A;       // ... and its drainage area
   Ctl* ctl;

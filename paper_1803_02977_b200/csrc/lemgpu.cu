@@ -34,6 +34,7 @@
 #include "k_fill.cuh"
 #include "k_tiles.cuh"
 #include "k_forest.cuh"
+#include "k_mfd.cuh"
 #include "k_util.cuh"
 
 using namespace lemgpu;
@@ -48,7 +49,10 @@ struct lemgpu_ctx {
   int esc_grid = 0;  // CTAs of the level expansion of the escaped trees (a small workload)
   int deep_coop_grid = 0;  // CTAs of k_deep_coop (kDeepTPB threads, co-resident)
   int forest_grid = 0;     // CTAs of k_esc_forest (kFTPB threads, co-resident)
+  int mfd_grid = 0;        // CTAs of k_mfd_levels (co-resident)
   int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
+  bool opt_global = false;  // lemgpu_options::global_path (the tile path stays off after routing = d8 again)
+  int routing = 0;          // 0 d8 / d4 (StepSetup::routing kD8), 1 kMfd (lemgpu_set_routing)
   // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
   // graph[p] / exec[p] is the step that reads hbuf[p]
   double* hbuf[2] = {nullptr, nullptr};
@@ -490,7 +494,11 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
         (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
       return rc;
   } else {
-    if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
+    if ((a.mfd_A &&  // routing = kMfd: the MFD graph, plan and drainage area first (they read only h)
+         ((rc = add_kernel(ctx, g, &prev, (const void*)k_mfd_graph, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
+          (rc = add_kernel(ctx, g, &prev, (const void*)k_mfd_levels, dim3(ctx->mfd_grid), dim3(kTPB), 0, &a, nullptr,
+                           true)))) ||
+        (rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_count, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)) ||
         (rc = add_kernel(ctx, g, &prev, (const void*)k_l0_write, dim3(ctx->scan_grid), dim3(kTPB), 0, &a, nullptr)))
       return rc;
@@ -713,6 +721,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if (o.esc_grid) ctx->esc_grid = (int)o.esc_grid;
   if (ctx->esc_grid < 1 || ctx->esc_grid > ctx->scan_grid) ctx->esc_grid = ctx->scan_grid;
   if (o.global_path) ctx->use_tiles = 0;
+  ctx->opt_global = o.global_path != 0;
   a.force_escape = 0;
   a.force_escape = o.force_escape;
   {
@@ -760,6 +769,8 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     int occf = 0;
     CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, forest_fn(a.nkind), kFTPB, kForestSmemBytes));
     ctx->forest_grid = (occf > 0 ? occf : 1) * nsm;
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_mfd_levels, kTPB, 0));
+    ctx->mfd_grid = std::min(ctx->scan_grid, (occf > 0 ? occf : 1) * nsm);
   }
   {
     const void* fdc = a.nkind == 1 ? (const void*)k_deep_coop<1> : a.nkind == 2 ? (const void*)k_deep_coop<2>
@@ -909,6 +920,11 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     if (rc) return rc;
   } else {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+    if (a.mfd_A) {
+      k_mfd_graph<<<ctx->deep_grid, kTPB, 0, st>>>(a);
+      void* margs[] = {&a};
+      CU(ctx, cudaLaunchCooperativeKernel((const void*)k_mfd_levels, dim3(ctx->mfd_grid), dim3(kTPB), margs, 0, st));
+    }
     if (a.conn == 8)
       k_recv_donor<8><<<g1, kTPB, 0, st>>>(a, ctx->hmap[p]);
     else
@@ -1166,6 +1182,9 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
     if (p) cudaFree(p);
   if (a.dbg_level) cudaFree(a.dbg_level);
   if (a.dbg_A) cudaFree(a.dbg_A);
+  for (void* q : {(void*)a.mfd_A, (void*)a.mfd_wsum, (void*)a.mfd_lm, (void*)a.mfd_rem, (void*)a.mfd_ord,
+                  (void*)a.mfd_lv, (void*)a.mfd_lev})
+    if (q) cudaFree(q);
   if (ctx->st_local) cudaFree(ctx->st_local);
   if (ctx->st_part) cudaFree(ctx->st_part);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
@@ -1621,6 +1640,72 @@ int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable) {
   if (a.dbg_level) {
     CU(ctx, cudaMemset(a.dbg_level, 0xFF, a.N));
     CU(ctx, cudaMemset(a.dbg_A, 0xFF, (size_t)a.N * sizeof(double)));
+  }
+  return LEMGPU_OK;
+}
+
+int lemgpu_set_routing(lemgpu_ctx* ctx, int routing, double mfd_exponent) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  if (routing != 0 && routing != 1) return fail(ctx, LEMGPU_ECONFIG, "routing must be 0 (d8) or 1 (mfd)");
+  if (!(mfd_exponent > 0.0) || !std::isfinite(mfd_exponent))
+    return fail(ctx, LEMGPU_ECONFIG, "mfd_exponent must be > 0");  // config.cpp:166
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  StepArgs& a = ctx->a;
+  const size_t N = a.N;
+  if (routing == 1 && !a.mfd_A) {
+    if ((dmalloc(ctx, &a.mfd_A, N)) || (dmalloc(ctx, &a.mfd_wsum, N)) || (dmalloc(ctx, &a.mfd_lm, N)) ||
+        (dmalloc(ctx, &a.mfd_rem, N)) || (dmalloc(ctx, &a.mfd_ord, N)) || (dmalloc(ctx, &a.mfd_lv, N + 2)) ||
+        (dmalloc(ctx, &a.mfd_lev, N)))
+      return LEMGPU_ECUDA;
+  } else if (routing == 0 && a.mfd_A) {
+    for (void* q : {(void*)a.mfd_A, (void*)a.mfd_wsum, (void*)a.mfd_lm, (void*)a.mfd_rem, (void*)a.mfd_ord,
+                    (void*)a.mfd_lv, (void*)a.mfd_lev})
+      cudaFree(q);
+    a.mfd_A = a.mfd_wsum = nullptr;
+    a.mfd_lm = nullptr;
+    a.mfd_rem = a.mfd_ord = a.mfd_lv = a.mfd_lev = nullptr;
+  }
+  a.mfd_exp = mfd_exponent;
+  ctx->routing = routing;
+  // the MFD area feeds the global level path's physics (the tile kernels
+  // accumulate their own trees); d8 again: back to the configured path
+  ctx->use_tiles = routing == 1 || ctx->opt_global ? 0 : 1;
+  return rebuild_graphs(ctx);
+}
+
+int lemgpu_download_mfd(lemgpu_ctx* ctx, double* A, uint32_t* order, uint32_t* levels, uint32_t* nlevels) {
+  if (!ctx) return LEMGPU_ECONFIG;
+  if (!ctx->a.mfd_A) return fail(ctx, LEMGPU_ECONFIG, "routing is not mfd (lemgpu_set_routing)");
+  CU(ctx, cudaSetDevice(ctx->device));
+  if (ctx->pending) {
+    const int rc = lemgpu_sync(ctx, nullptr, 0, nullptr);
+    if (rc) return rc;
+  }
+  const StepArgs& a = ctx->a;
+  const size_t N = a.N;
+  if (A) CU(ctx, cudaMemcpy(A, a.mfd_A, N * sizeof(double), cudaMemcpyDeviceToHost));
+  if (order || levels || nlevels) {
+    // the reference's TraversalPlan (mfd.cpp:66-104): level-major, ascending
+    // within a level -- a counting sort of the cell-major levels
+    Ctl c{};
+    CU(ctx, cudaMemcpy(&c, a.ctl, sizeof c, cudaMemcpyDeviceToHost));
+    const uint32_t nl = c.mfd_nlev;
+    std::vector<uint32_t> lev(N), start(nl + 1, 0);
+    CU(ctx, cudaMemcpy(lev.data(), a.mfd_lev, N * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < N; ++i) {
+      if (lev[i] >= nl) return fail(ctx, LEMGPU_ESTRUCTURE, "MFD plan incomplete (cell %zu)", i);
+      ++start[lev[i] + 1];
+    }
+    for (uint32_t l = 0; l < nl; ++l) start[l + 1] += start[l];
+    if (levels)
+      for (uint32_t l = 0; l <= nl; ++l) levels[l] = start[l];
+    if (order)
+      for (size_t i = 0; i < N; ++i) order[start[lev[i]]++] = (uint32_t)i;
+    if (nlevels) *nlevels = nl;
   }
   return LEMGPU_OK;
 }

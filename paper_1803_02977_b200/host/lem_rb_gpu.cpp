@@ -18,6 +18,8 @@ namespace {
 struct Ctx {
   lemgpu_ctx* h = nullptr;
   int w = 0, hgt = 0, conn = 0, device = 0;
+  int routing = 0;            // lemgpu_set_routing state (0 d8, 1 mfd)
+  double mfd_exponent = 1.0;
   SimParams params{};
   ~Ctx() {
     if (h) lemgpu_destroy(h);
@@ -101,10 +103,21 @@ StepDiagnostics to_diag(const lemgpu_diag& d) {
 }
 
 void check_setup(const StepSetup& setup) {
-  // the device path is the D8/D4 queue plan (like rb_private_queues'
-  // routing restriction, scheduler.cpp:413-416)
-  if (setup.routing == Routing::kMfd) throw ConfigError("rb_gpu requires single-receiver (d8/d4) routing");
+  // the device path is the breadth-first queue plan; Routing::kMfd feeds it the
+  // multiple-flow drainage area (simulation.cpp:53-60), like rb_par_all
+  if (setup.routing == Routing::kMfd && !(setup.mfd_exponent > 0.0))
+    throw ConfigError("mfd_exponent must be > 0");  // config.cpp:166
   if (setup.order == OrderKind::kStack) throw ConfigError("rb_gpu uses the breadth-first queue order");
+}
+
+// StepSetup::routing / mfd_exponent onto the context (graphs rebuilt only on a change)
+void apply_routing(Ctx& c, const StepSetup& setup) {
+  const int r = setup.routing == Routing::kMfd ? 1 : 0;
+  const double e = r ? setup.mfd_exponent : 1.0;
+  if (r == c.routing && e == c.mfd_exponent) return;
+  check(c.h, lemgpu_set_routing(c.h, r, e));
+  c.routing = r;
+  c.mfd_exponent = e;
 }
 
 }  // namespace
@@ -114,6 +127,7 @@ StepDiagnostics strategy_step_rb_gpu(Raster<double>& elev, const GridGraph& grid
   check_setup(setup);
   params.validate();
   Ctx& c = ctx_for(ws, grid, params, device);
+  apply_routing(c, setup);
   lemgpu_diag d{};
   check(c.h, lemgpu_step_host(c.h, elev.storage().data(), &d));
   return to_diag(d);
@@ -128,8 +142,10 @@ RunResult run_simulation_rb_gpu(Raster<double> initial, const RunConfig& cfg, co
                       std::to_string(cfg.height));
   StepSetup setup;
   setup.routing = cfg.routing;
+  setup.mfd_exponent = cfg.mfd_exponent;
   check_setup(setup);
   auto c = make_ctx(initial.width(), initial.height(), cfg.connectivity, cfg.params, device);
+  apply_routing(*c, setup);
   check(c->h, lemgpu_upload_elev(c->h, initial.storage().data()));  // rejects non-finite input
   RunResult res;
   res.elevation = std::move(initial);

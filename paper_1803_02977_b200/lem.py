@@ -387,6 +387,28 @@ class DeviceContext:
         out["nlevels"] = nl.value
         return out
 
+    def set_routing(self, routing, mfd_exponent: float = 1.0):
+        """StepSetup::routing / mfd_exponent (simulation.hpp:55-60): Routing.kMfd
+        feeds the erosion the multiple-flow drainage area (mfd.cpp:33-132)."""
+        self._check(self._L.lemgpu_set_routing(self._h, int(Routing(routing) == Routing.kMfd), float(mfd_exponent)))
+
+    def download_mfd(self, A=True, plan=True):
+        """The last step's MFD drainage area (ws.accum) and MFD plan (ws.mfd_plan)."""
+        n = self.n
+        a = np.empty(n, np.float64) if A else None
+        o = np.empty(n, np.uint32) if plan else None
+        lv = np.empty(n + 2, np.uint32) if plan else None
+        nl = C.c_uint32(0)
+        ptr = lambda x: x.ctypes.data if x is not None else None  # noqa: E731
+        self._check(self._L.lemgpu_download_mfd(self._h, ptr(a), ptr(o), ptr(lv), C.byref(nl)))
+        out = {"nlevels": nl.value}
+        if A:
+            out["A"] = a
+        if plan:
+            out["order"] = o
+            out["levels"] = lv[: nl.value + 1].copy()
+        return out
+
     def stream_ptr(self) -> int:
         return int(self._L.lemgpu_stream(self._h) or 0)
 
@@ -471,13 +493,18 @@ class SimWorkspace:
         self.gpu: Optional[DeviceContext] = None
         self._key = None
 
-    def ensure(self, grid: GridGraph, params: SimParams, device: int = 0) -> DeviceContext:
+    def ensure(self, grid: GridGraph, params: SimParams, device: int = 0, setup=None) -> DeviceContext:
         key = (grid.width, grid.height, grid.nbh.connectivity, device, tuple(vars(params).items()))
         if self.gpu is None or self._key != key:
             if self.gpu is not None:
                 self.gpu.close()
             self.gpu = DeviceContext(grid.width, grid.height, params, grid.nbh.connectivity, device)
             self._key = key
+            self._routing = (Routing.kD8, 1.0)
+        want = (setup.routing, setup.mfd_exponent) if setup is not None else (Routing.kD8, 1.0)
+        if want != self._routing:
+            self.gpu.set_routing(want[0], want[1])
+            self._routing = want
         return self.gpu
 
     def graph(self, **kw):
@@ -491,9 +518,8 @@ def _check_strategy(setup: StepSetup, strategy: Strategy):
         raise ConfigError(
             f"strategy {strategy.kind.value!r} is a CPU strategy of the reference library; "
             "this package provides only 'rb_gpu'")
-    # like rb_private_queues (scheduler.cpp:413-416): the device path is D8/D4 queue order only
-    if setup.routing == Routing.kMfd:
-        raise ConfigError("rb_gpu requires single-receiver (d8/d4) routing")
+    if setup.routing == Routing.kMfd and not setup.mfd_exponent > 0.0:
+        raise ConfigError("mfd_exponent must be > 0")
     if setup.order == OrderKind.kStack:
         raise ConfigError("rb_gpu uses the breadth-first queue order")
 
@@ -507,7 +533,7 @@ def strategy_step(elev: np.ndarray, grid: GridGraph, params: SimParams, setup: S
         raise ConfigError("StepInstrumentation is not supported by rb_gpu")
     if elev.shape != (grid.height, grid.width) or elev.dtype != np.float64 or not elev.flags.c_contiguous:
         raise ConfigError("elev must be a C-contiguous float64 array of shape (height, width)")
-    ctx = ws.ensure(grid, params, strategy.device)
+    ctx = ws.ensure(grid, params, strategy.device, setup)
     return ctx.step_host(elev)
 
 
@@ -555,6 +581,7 @@ class RunConfig:
     params: SimParams = field(default_factory=SimParams)
     connectivity: int = 8
     routing: Routing = Routing.kD8
+    mfd_exponent: float = 1.0
     fill: FillOptions = field(default_factory=FillOptions)
 
     def validate(self):
@@ -565,6 +592,8 @@ class RunConfig:
             raise ConfigError("grid exceeds 2^32-1 cells")
         self.params.validate()
         Neighborhood.make(self.connectivity)
+        if not self.mfd_exponent > 0.0:
+            raise ConfigError("mfd_exponent must be > 0")
         if self.fill.mode == FillMode.kEpsilonAscending and not self.fill.epsilon_increment > 0.0:
             raise ConfigError("fill_epsilon must be > 0 for epsilon_ascending fill")
 
@@ -601,9 +630,11 @@ def run_simulation(initial, cfg: Optional[RunConfig] = None,
     if cfg is None:
         cfg, initial = initial, None
     cfg.validate()
-    _check_strategy(StepSetup(routing=cfg.routing), cfg.strategy)
+    _check_strategy(StepSetup(routing=cfg.routing, mfd_exponent=cfg.mfd_exponent), cfg.strategy)
     ctx = DeviceContext(cfg.width, cfg.height, cfg.params, cfg.connectivity, cfg.strategy.device)
     try:
+        if cfg.routing == Routing.kMfd:
+            ctx.set_routing(cfg.routing, cfg.mfd_exponent)
         if initial is None:  # generate_terrain + optional depression fill (scheduler.cpp:503-506)
             ctx.generate_terrain([cfg.seed])
             ctx.fill(cfg.fill)

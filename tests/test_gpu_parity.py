@@ -712,3 +712,113 @@ def test_ensemble_shard_with_nccl_allreduce_in_graph(oracle):
         for i in range(M):
             assert np.array_equal(g[i].view(np.uint64), refs[i].view(np.uint64)), (s, i)
     ens.close()
+
+
+# ---- MFD routing: StepSetup::routing = kMfd -------------------------------
+
+def _mfd_ctx(w, h, ex, conn=8, members=1, **kw):
+    ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=members)
+    ctx.set_routing(lem.Routing.kMfd, ex)
+    return ctx
+
+
+def test_mfd_golden(oracle, golden_dir):
+    """Every mfd_*.npz fixture (made by the unmodified reference's simulate_step
+    with Routing::kMfd): h after the step, Newton iterations, the MFD drainage
+    area and the MFD plan, bit for bit."""
+    for path in sorted(golden_dir.glob("mfd_*.npz")):
+        g = np.load(path)
+        kw = json.loads(str(g["params"]))
+        ctx = _mfd_ctx(int(g["w"]), int(g["h"]), float(g["exponent"]), int(g["conn"]), **kw)
+        ctx.upload(g["h0"])
+        d = ctx.step(1)[0]
+        assert np.array_equal(ctx.download().view(np.uint64), g["h1"].view(np.uint64)), path.name
+        assert d.newton_iters == int(g["newton_iters"]), path.name
+        m = ctx.download_mfd()
+        assert np.array_equal(m["A"].view(np.uint64), g["A"].view(np.uint64)), path.name
+        assert np.array_equal(m["order"], g["mfd_order"]) and np.array_equal(m["levels"], g["mfd_levels"]), path.name
+        ctx.close()
+
+
+@pytest.mark.parametrize("w,h,seed,conn,ex,kw,terrain", [
+    (300, 200, 51, 8, 1.0, {}, "noise"), (257, 131, 52, 8, 1.3, {"m_exp": 0.4}, "noise"),
+    (130, 97, 53, 4, 1.0, {}, "noise"), (77, 65, 54, 8, 2.0, {"dx": 0.5, "dy": 2.0}, "noise"),
+    (120, 90, 55, 8, 1.0, {"n_exp": 2.0}, "noise"), (200, 150, 56, 8, 1.0, {}, "ramp"),
+    (400, 12, 57, 8, 0.7, {}, "ramp"), (3, 3, 58, 8, 1.0, {}, "noise"),
+])
+def test_mfd_steps_vs_oracle(oracle, w, h, seed, conn, ex, kw, terrain):
+    """4 MFD steps per shape (odd widths, D4, anisotropic spacing, exponents
+    0.7-2, n = 2, deep ramps): h, A and the MFD plan against the oracle each step."""
+    ctx = _mfd_ctx(w, h, ex, conn, **kw)
+    e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
+    ctx.upload(e)
+    p = make_params(**kw)
+    for s in range(4):
+        d = ctx.step(1)[0]
+        o = oracle.step_mfd(e, exponent=ex, conn=conn, params=p)
+        assert o["status"] == 0
+        assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), f"step {s}"
+        assert d.newton_iters == o["newton_iters"] and d.interior_noflow == o["interior_noflow"]
+        assert d.nlevels == o["nlevels"]  # the D8 plan's levels (the erosion's)
+        m = ctx.download_mfd()
+        assert np.array_equal(m["A"].view(np.uint64), o["A"].view(np.uint64)), f"step {s}"
+        assert np.array_equal(m["order"], o["mfd_order"]) and np.array_equal(m["levels"], o["mfd_levels"])
+
+
+def test_mfd_ensemble_members(oracle):
+    """A stacked ensemble under MFD routing: every member equals its own oracle run."""
+    M, w, h = 3, 90, 70
+    ctx = _mfd_ctx(w, h, 1.0, members=M)
+    seeds = [61, 62, 63]
+    ctx.generate_terrain(seeds)
+    es = [oracle.terrain(w, h, sd) for sd in seeds]
+    for s in range(3):
+        ctx.step(1)
+        g = ctx.download().reshape(M, h, w)
+        for m in range(M):
+            oracle.step_mfd(es[m])
+            assert np.array_equal(g[m].view(np.uint64), es[m].view(np.uint64)), (s, m)
+
+
+def test_mfd_1000_vs_reference():
+    """configs[0]'s 1000^2 DEM under MFD routing: one step against the reference's
+    simulate_step (A and the MFD plan too), then 5 more against its rb_par_all."""
+    from _oracle import RefLib
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref/liblemref.so not present")
+    ref = RefLib.get()
+    n = 1000
+    e = ref.terrain(n, n, 42)
+    ctx = _mfd_ctx(n, n, 1.0)
+    ctx.upload(e)
+    d = ctx.step(1)[0]
+    r = ref.step_mfd(e)
+    assert r["status"] == 0
+    assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
+    assert d.newton_iters == r["newton_iters"]
+    m = ctx.download_mfd()
+    assert np.array_equal(m["A"].view(np.uint64), r["A"].view(np.uint64))
+    assert np.array_equal(m["order"], r["mfd_order"]) and np.array_equal(m["levels"], r["mfd_levels"])
+    ds = ctx.step(5)
+    rc, newton, _ = ref.run(e, 5, strategy="rb_par_all", workers=ref.max_threads(), routing=1)
+    assert rc == 0
+    assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
+    assert sum(x.newton_iters for x in ds) == newton
+
+
+def test_mfd_routing_switch_and_dropin(oracle):
+    """strategy_step with StepSetup(routing=kMfd) through the Python drop-in,
+    then back to D8 on the same workspace: both against the oracle."""
+    w, h = 96, 80
+    e = oracle.terrain(w, h, 7)
+    ref_e = e.copy()
+    g = lem.GridGraph(w, h)
+    ws = lem.SimWorkspace()
+    for routing in (lem.Routing.kMfd, lem.Routing.kD8, lem.Routing.kMfd):
+        lem.strategy_step(e, g, lem.SimParams(), lem.StepSetup(routing=routing), lem.Strategy(), ws)
+        if routing == lem.Routing.kMfd:
+            oracle.step_mfd(ref_e)
+        else:
+            oracle.step(ref_e, want_donor=False)
+        assert np.array_equal(e.view(np.uint64), ref_e.view(np.uint64)), routing

@@ -36,8 +36,11 @@ def test_step_rejects_unsupported_setups():
     ws = lem.SimWorkspace()
     with pytest.raises(lem.ConfigError, match="CPU strategy"):
         lem.strategy_step(e, g, lem.SimParams(), lem.StepSetup(), lem.Strategy(lem.StrategyKind.kRbSerial), ws)
-    with pytest.raises(lem.ConfigError, match="single-receiver"):
-        lem.strategy_step(e, g, lem.SimParams(), lem.StepSetup(routing=lem.Routing.kMfd), lem.Strategy(), ws)
+    with pytest.raises(lem.ConfigError, match="mfd_exponent"):  # config.cpp:166
+        lem.strategy_step(e, g, lem.SimParams(), lem.StepSetup(routing=lem.Routing.kMfd, mfd_exponent=0.0),
+                          lem.Strategy(), ws)
+    with pytest.raises(lem.ConfigError, match="mfd_exponent"):
+        lem.RunConfig(routing=lem.Routing.kMfd, mfd_exponent=-1.0).validate()
     with pytest.raises(lem.ConfigError, match="queue"):
         lem.strategy_step(e, g, lem.SimParams(), lem.StepSetup(order=lem.OrderKind.kStack), lem.Strategy(), ws)
     with pytest.raises(lem.ConfigError, match="shape"):

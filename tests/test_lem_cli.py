@@ -76,7 +76,19 @@ def test_lem_bench_prints_rb_gpu_phases():
         assert sum(secs) > 0 and all(s >= 0 for s in secs)  # lem::Phase split of the device time
 
 
-def test_lem_rb_gpu_rejects_mfd_routing():
-    r = lem("run", "strategy=rb_gpu", "routing=mfd", "width=50", "height=40", "timesteps=2",
+@pytest.mark.parametrize("extra", [
+    ["width=200", "height=150", "timesteps=8", "seed=3"],
+    ["width=131", "height=97", "timesteps=5", "seed=4", "mfd_exponent=1.3", "connectivity=4"],
+    ["width=120", "height=90", "timesteps=5", "seed=6", "fill=epsilon_ascending", "n_exp=2"],
+], ids=["d8", "d4-e13", "filled-n2"])
+def test_lem_compare_rb_gpu_mfd_routing(extra):
+    # routing=mfd: rb_gpu against the reference's serial and level-parallel strategies
+    out = lem("compare", "strategies=rb_serial,rb_par_all,rb_gpu", "routing=mfd", "workers=4", *extra)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "3 strategies produced byte-identical rasters" in out.stdout
+
+
+def test_lem_rb_gpu_rejects_bad_mfd_exponent():
+    r = lem("run", "strategy=rb_gpu", "routing=mfd", "mfd_exponent=0", "width=50", "height=40", "timesteps=2",
             "output=/tmp/lem_mfd_reject.lem")
-    assert r.returncode != 0 and "single-receiver" in (r.stdout + r.stderr)
+    assert r.returncode != 0 and "mfd_exponent" in (r.stdout + r.stderr)
