@@ -2,7 +2,7 @@
 """Benchmark of the B200 D8 landscape-evolution step (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
-                    [--workload dem10000|dem1000|dem4000n2|dem1000fill|dem4000fill|ens64]
+                    [--workload dem10000|dem1000|dem4000n2|dem1000fill|dem4000fill|dem1000mfd|dem10000mfd|ens64]
 
 A "step" is one timestep (receivers, donors, level order, accumulation,
 uplift + erosion) over the whole workload.  Default workload at N=1: the
@@ -47,6 +47,10 @@ B_STEP = 87
 B_RECV = 17
 B_TILES = 70
 B_TILES_MIN = 18
+# MFD routing (not in SURVEY 8(d); same counting rule): graph 17 (read h 8, write lower mask 1 + weight
+# sum 8) + plan 9 (read mask 1, write order 4 + level 4) + accumulation 37 (read order 4, h 8, mask 1,
+# donors' weight sums 8 and A 8, write A 8) = 63 B/cell on top of the D8 step's 87
+B_MFD = 63
 WORKLOADS = {
     "dem10000": dict(w=10000, h=10000, members=1, n_exp=1.0,
                      desc="10000x10000 random-noise DEM, D8, m=0.5 n=1, fixed-perimeter base level, seed 42 (configs[1])"),
@@ -58,6 +62,12 @@ WORKLOADS = {
     "dem4000fill": dict(w=4000, h=4000, members=1, n_exp=1.0, fill=2,
                         desc="4000x4000 random-noise DEM, Priority-Flood epsilon-filled (1e-8), D8, n=1: "
                              "the deep-level regime (SURVEY 8(f) rank 1)"),
+    "dem1000mfd": dict(w=1000, h=1000, members=1, n_exp=1.0, routing=1,
+                       desc="1000x1000 random-noise DEM, D8 erosion fed by the MFD drainage area (routing=mfd, "
+                            "mfd_exponent 1), n=1 (SURVEY 8(f) rank 3)"),
+    "dem10000mfd": dict(w=10000, h=10000, members=1, n_exp=1.0, routing=1,
+                        desc="10000x10000 random-noise DEM, D8 erosion fed by the MFD drainage area (routing=mfd, "
+                             "mfd_exponent 1), n=1 (SURVEY 8(f) rank 3)"),
     "ens64": dict(w=2000, h=2000, members=64, n_exp=1.0,
                   desc="ensemble of 64 x 2000^2 DEMs, seeds 1000+i, K_i=1e-6(1+i%8), m_i=0.35+0.05*floor(i/8) (configs[4])"),
 }
@@ -70,6 +80,7 @@ def arm_config(workload, world):
     return {"workload": wl["desc"] + (" -- one independent replica per GPU" if (world > 1 and wl["members"] == 1) else ""),
             "grid": [wl["w"], wl["h"]], "members": wl["members"] * (world if wl["members"] == 1 else 1),
             "params": "K=2e-6 m=0.5 n=%g u=2e-3 dt=1000 eps=1e-6 D8" % wl["n_exp"]
+                      + (" routing=mfd mfd_exponent=1" if wl.get("routing") else "")
                       + (" (per-member K, m)" if wl["members"] > 1 else ""),
             "fill": "epsilon_ascending 1e-8" if wl.get("fill") else "off"}
 
@@ -179,6 +190,12 @@ def traffic_from_profiles(workload):
     return {}, None
 
 
+def ref_strategy(wl):
+    """The reference's fastest strategy for the workload: rb_private_queues, or
+    rb_par_all under MFD routing (private queues reject it, scheduler.cpp:413-416)."""
+    return "rb_par_all" if wl.get("routing") else "rb_private_queues"
+
+
 def cpu_baseline_reference(workload, budget_s=30.0):
     """The unmodified reference on this host's cores: lem::strategy_step with
     rb_private_queues (its fastest strategy), all OpenMP threads, a bounded
@@ -196,12 +213,13 @@ def cpu_baseline_reference(workload, budget_s=30.0):
     # bounded sample: ~budget_s of CPU work, at least 2 timed steps after 1 warm-up
     est = 3e-8 * w * h * 16 / max(threads, 1)  # ~3 s per 10000^2 step on 16 cores
     n = int(max(2, min(10, budget_s // max(est, 1e-3))))
-    samples, _ = ref.bench(w, h, n, warmup=1, strategy="rb_private_queues", workers=threads, params=p,
-                           fill=wl.get("fill", 0))
+    strat = ref_strategy(wl)
+    samples, _ = ref.bench(w, h, n, warmup=1, strategy=strat, workers=threads, params=p,
+                           fill=wl.get("fill", 0), routing=wl.get("routing", 0))
     per_step = float(np.median(samples))
     cells = w * h
     return {"value": cells / per_step, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{len(samples)} lem::strategy_step(rb_private_queues, {threads} threads) timesteps of the "
+            "sample": f"{len(samples)} lem::strategy_step({strat}, {threads} threads) timesteps of the "
                       f"{w}x{h} seed-42 DEM{' (priority_flood_fill first)' if wl.get('fill') else ''}, median wall time {per_step:.3f} s/step (oracle/_ref, -O2 -ffp-contract=off)"}
 
 
@@ -226,23 +244,25 @@ def run_reference_arm(args):
     # bounded sample (one member) scaled to the member count.
     t0 = time.time()
     fill = wl.get("fill", 0)
-    wsecs, _ = ref.bench(w, h, 1, warmup=0, strategy="rb_private_queues", workers=threads, params=p, fill=fill)
+    strat, routing = ref_strategy(wl), wl.get("routing", 0)
+    wsecs, _ = ref.bench(w, h, 1, warmup=0, strategy=strat, workers=threads, params=p, fill=fill, routing=routing)
     est = float(wsecs[0]) * members
     budget = 180.0
     k = args.steps
     warm = max(0, min(args.warmup - 1, int((budget / 4) // max(est, 1e-3))))
     k_run = int(max(1, min(k, (budget - (time.time() - t0)) // max(est, 1e-3) - warm)))
-    secs, _ = ref.bench(w, h, k_run, warmup=warm, strategy="rb_private_queues", workers=threads, params=p, fill=fill)
+    secs, _ = ref.bench(w, h, k_run, warmup=warm, strategy=strat, workers=threads, params=p, fill=fill,
+                        routing=routing)
     per_step = float(np.mean(secs)) * members
     value = w * h * members / per_step
-    sample = (f"{k_run} timed + {warm + 1} warm-up lem::strategy_step(rb_private_queues, {threads} threads) on "
+    sample = (f"{k_run} timed + {warm + 1} warm-up lem::strategy_step({strat}, {threads} threads) on "
               f"{w}x{h}" + (f" (one member, scaled x{members})" if members > 1 else "") +
               (f"; steps capped from {k} to fit the time budget" if k_run < k else ""))
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": k_run, "warmup": warm + 1,
            "ms_per_step": per_step * 1e3, "higher_is_better": True,
            "scaling": "weak" if wl["members"] == 1 else "strong", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic (splitmix64 random-noise DEM, lem::generate_terrain)", "config": cfg,
-           "details": {"impl": "reference CPU: lem::strategy_step(rb_private_queues) of the unmodified reference "
+           "details": {"impl": f"reference CPU: lem::strategy_step({strat}) of the unmodified reference "
                                "(oracle/_ref/liblemref.so)"},
            "impl": "reference",
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
@@ -316,6 +336,8 @@ def main():
     else:
         ctx = lem.DeviceContext(w, h, params, 8, device=local, members=M, options=opts or None)
         ctx.generate_terrain(seeds)
+        if wl.get("routing"):
+            ctx.set_routing(lem.Routing.kMfd, 1.0)
     fill_ms = None
     if wl.get("fill"):  # lem::priority_flood_fill on the device, once, before the timed steps
         torch.cuda.synchronize(local)
@@ -403,7 +425,12 @@ def main():
     # escape path 70 B/cell (order 9 + accumulation 21 + uplift/erosion 40) for
     # the cells each finishes.  The dominant one is the longest.
     cands = []
-    if pipelined:
+    if wl.get("routing"):
+        # MFD routing: the global level path (D8 plan, physics fed the MFD area)
+        # after the MFD kernels; their spans are not stamped separately: the step
+        cands.append(("step: k_mfd_graph + k_mfd_levels + global level path", step_ms_ev,
+                      (B_STEP + B_MFD) * cells, ()))
+    elif pipelined:
         # tall rasters: k_recv and k_tiles run in interleaved bands (receiver band
         # b+1 beside tile band b): one unit, the step minus the escape kernels
         cands.append(("k_recv+k_tiles (pipelined bands)", max(step_ms_ev - esc_ord_ms - esc_phys_ms, 1e-9),
@@ -413,10 +440,12 @@ def main():
         cands.append(("k_recv", k1_ms, B_RECV * cells, ("k_recv",)))
     cands.append(("escape path (k_esc_small | k_esc_bfs + k_chunks/k_deep_coop)", esc_ord_ms + esc_phys_ms,
                   B_TILES * esc_cells, ("k_esc_small", "k_esc_bfs", "k_chunks", "k_deep_coop")))
+    if wl.get("routing"):
+        cands = cands[:1]
     dom, dom_ms, dom_bytes, dom_kernels = max(cands, key=lambda c: c[1])
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     traffic = None
-    if traffic_tbl and all(k in traffic_tbl for k in dom_kernels[:2]):
+    if traffic_tbl and dom_kernels and all(k in traffic_tbl for k in dom_kernels[:2]):
         traffic = sum(traffic_tbl[k]["dram_bytes_per_launch"] for k in dom_kernels if k in traffic_tbl)
     per_gpu = value / world
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
