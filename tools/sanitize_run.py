@@ -38,6 +38,11 @@ CASES = [
     ("fp-area", {}, {"dx": 0.1, "dy": 0.3}, "noise", 100, 80),
     ("few-tile-ctas", {"tile_grid": 3}, {}, "noise", 200, 120),
     ("pipelined", {}, {}, "noise", 64, 8300),
+    ("forest", {"force_escape": 1, "no_esc_small": 1, "esc_forest": 1}, {}, "noise", 130, 97),
+    ("forest-half-n2", {"force_escape": 2, "no_esc_small": 1, "esc_forest": 1}, {"n_exp": 2.0}, "noise", 100, 80),
+    ("forest-ramp", {}, {}, "ramp", 200, 150),
+    ("mfd", {}, {}, "noise", 130, 97),
+    ("mfd-eager-e13", {"eager": 1}, {}, "noise", 100, 80),
 ]
 only = sys.argv[1:] or None
 if only == ["list"]:
@@ -47,12 +52,19 @@ for name, opts, kw, terrain, w, h in CASES:
     if only and name not in only:
         continue
     ctx = lem.DeviceContext(w, h, lem.SimParams(**kw), 8, options=opts)
+    mfd = name.startswith("mfd")
+    ex = 1.3 if name.endswith("e13") else 1.0
+    if mfd:
+        ctx.set_routing(lem.Routing.kMfd, ex)
     e = ora.terrain(w, h, 7) if terrain == "noise" else ramp(w, h, 7)
     ctx.upload(e)
     p = make_params(**kw)
     for s in range(2):
         d = ctx.step(1)[0]
-        ora.step(e, params=p, want_donor=False)
+        if mfd:
+            ora.step_mfd(e, exponent=ex, params=p)
+        else:
+            ora.step(e, params=p, want_donor=False)
         ok = np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
         assert ok, f"{name}: step {s} differs from the oracle"
     print(f"{name}: ok (nlevels {d.nlevels})", flush=True)
