@@ -139,6 +139,7 @@ int main() {
     CHECK(cfg, "non-finite input not rejected");
     StepSetup mfd;
     mfd.routing = Routing::kMfd;
+    mfd.mfd_exponent = 0.0;  // config.cpp:166
     bool mf = false;
     try {
       SimWorkspace ws;
@@ -147,8 +148,28 @@ int main() {
     } catch (const ConfigError&) {
       mf = true;
     }
-    CHECK(mf, "MFD routing accepted");
+    CHECK(mf, "mfd_exponent 0 accepted");
     std::printf("%s ConvergenceError(cell) / ConfigError behaviour\n", (got && cfg && mf) ? "ok  " : "FAIL");
+  }
+
+  // 4b. MFD routing (simulation.cpp:53-60): rb_gpu steps == rb_par_all steps,
+  // alternating with D8 steps on the same workspace (routing switched per step)
+  {
+    Raster<double> a = generate_terrain(150, 110, 21), b = a;
+    const GridGraph g(150, 110, Neighborhood::d8());
+    SimWorkspace wa, wb;
+    const Strategy par{StrategyKind::kRbParAll, 4};
+    bool ok = true;
+    for (int s = 0; s < 6; ++s) {
+      StepSetup st;
+      st.routing = (s % 3 == 2) ? Routing::kD8 : Routing::kMfd;
+      st.mfd_exponent = s < 3 ? 1.0 : 1.4;
+      strategy_step(a, g, SimParams{}, st, par, wa);
+      gpu::strategy_step_rb_gpu(b, g, SimParams{}, st, wb);
+      if (first_difference(a, b)) ok = false;
+    }
+    CHECK(ok, "MFD routing differs from rb_par_all");
+    std::printf("%s MFD routing (exponents 1, 1.4) interleaved with D8 == rb_par_all\n", ok ? "ok  " : "FAIL");
   }
 
   // 5. on_step callback sees every step's raster (scheduler.cpp:496)
