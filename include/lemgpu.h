@@ -102,7 +102,7 @@ typedef struct lemgpu_diag {
    * level expansion, [3] escape path's accumulation + uplift + erosion. */
   double kernel_s[4];
   uint32_t escaped_cells;   /* cells of the escaped trees */
-  uint32_t reserved;
+  uint32_t mfd_passes;      /* routing = kMfd: tile passes of the MFD accumulation (k_mfd_tiles); else 0 */
 } lemgpu_diag;
 
 /* Schedule / tuning / test knobs of a context (no reference counterpart).
@@ -131,7 +131,9 @@ typedef struct lemgpu_options {
   int32_t host_profile;    /* 1: banded host step prints its timing to stderr */
   int32_t esc_forest;      /* escaped trees by k_esc_forest (exact-area steps): 0 auto (>= 1/4 of the cells
                               escape), 1 always, -1 never (level path) */
-  int32_t reserved[2];
+  int32_t mfd_levels;      /* 1: routing = kMfd through the level-synchronous plan + accumulation and the
+                              global level path (default: MFD area by tile passes, D8 part on the tile path) */
+  int32_t reserved[1];
 } lemgpu_options;
 
 typedef struct lemgpu_ctx lemgpu_ctx;

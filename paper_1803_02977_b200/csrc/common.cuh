@@ -175,6 +175,9 @@ struct Ctl {
   uint32_t fr_flag[3], fr_maxd;          // k_esc_forest: pointer-jumping round flags, deepest escaped level
   uint32_t fr_rounds, fr_maxcells;       // ... rounds taken, most cells of one CTA
   uint32_t mfd_cnt[3], mfd_nlev;         // k_mfd_levels: per-level append counters, MFD plan levels
+  uint32_t mfd_pass, mfd_wl_n[2];        // k_mfd_tiles: pass id (monotonic), queued tiles per pass parity
+  uint32_t mfd_passes;                   // ... passes of this step
+  unsigned long long t_mfd_begin;        // ... first pass start (the step's device time starts there)
   unsigned long long fr_t[3];            // ... latest end over the CTAs of the counts, F and erosion sweeps
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;
   unsigned long long t_t_begin, t_t_end;  // k_tiles
@@ -200,6 +203,8 @@ struct StepArgs {
   uint32_t dist_one;  // bit k set when dist[k] == 1.0 (division is the identity)
   int unit_card;      // dx == dy == 1: cardinal slopes are the drops themselves
   double rinv_diag;   // RN(1 / dist_diag): pre-decides far-from-tie comparisons only
+  double rdist[8];    // RN(1 / dist[k]) (host): correctly rounded quotients by dist (div_rn_recip)
+  uint32_t dist_recip;  // bit k: 1 <= dist[k] < 2^500, the reciprocal path applies
   double dist[8];     // offset_length of direction k (neighborhood.hpp:17-23)
   double powdist_h, powdist_v, powdist_d;  // host-libm pow(dist, n) per offset class
   double du, w0, n_exp, eps;
@@ -263,11 +268,14 @@ struct StepArgs {
   uint32_t* mfd_lv;   // its level starts
   uint32_t* mfd_lev;  // cell-major level (for the export)
   double mfd_exp;     // StepSetup::mfd_exponent
+  uint32_t* mfd_wl;     // k_mfd_tiles: two work lists of tiles (pass parity), ntiles each
+  uint32_t* mfd_stamp;  // ... per tile: the pass it is queued for
+  int mfd_all;          // ... 1: this launch is pass 0 (every tile)
   uint8_t* dbg_level;  // debug capture (nullptr: off): level of every cell k_tiles finishes (escaped: untouched)
   double* dbg_A;       // ... and its drainage area
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
-  cudaGraphConditionalHandle h_expand, h_dacc, h_deros;
+  cudaGraphConditionalHandle h_expand, h_dacc, h_deros, h_mfd;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -405,13 +413,13 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total,
 }
 
 // Loop condition of the step graph (0: level expansion, 1: deep
-// accumulation, 2: deep erosion): a graph conditional when the step is a
+// accumulation, 2: deep erosion, 3: MFD tile passes): a graph conditional when the step is a
 // CUDA graph, a control-block word when it runs eagerly (profiling).
 __device__ __forceinline__ void set_cond(const StepArgs& a, int which, unsigned v) {
   if (a.eager) {
     a.ctl->cond[which] = v;
   } else {
-    const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : a.h_deros;
+    const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : which == 2 ? a.h_deros : a.h_mfd;
     cudaGraphSetConditional(h, v);
   }
 }

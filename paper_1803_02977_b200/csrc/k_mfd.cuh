@@ -24,6 +24,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "k_physics.cuh"
 
 namespace lemgpu {
 
@@ -35,10 +36,12 @@ __device__ __forceinline__ double mfd_weight(const StepArgs& a, double slope) {
   return a.mfd_exp == 1.0 ? slope : glibc_pow_dev(a.pow_fma, slope, a.mfd_exp);
 }
 
-// slope = (h[c] - h[nb]) / dist[k] (the division is exact for dist == 1).
+// slope = (h[c] - h[nb]) / dist[k]: exact for dist == 1, else the correctly
+// rounded quotient from the host reciprocal (div_rn_recip) or by IEEE division.
 __device__ __forceinline__ double mfd_slope(const StepArgs& a, double hc, double hn, int k) {
   const double d = __dsub_rn(hc, hn);
-  return ((a.dist_one >> k) & 1u) ? d : __ddiv_rn(d, a.dist[k]);
+  if ((a.dist_one >> k) & 1u) return d;
+  return ((a.dist_recip >> k) & 1u) ? div_rn_recip(d, a.dist[k], a.rdist[k]) : __ddiv_rn(d, a.dist[k]);
 }
 
 // compute_mfd per cell: the mask of strictly lower neighbours (stencil

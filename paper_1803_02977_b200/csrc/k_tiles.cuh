@@ -123,7 +123,7 @@ __device__ __forceinline__ int woff(uint32_t k) { return (int)(__byte_perm(kWOff
 __device__ __forceinline__ double tile_F(const StepArgs& a, uint32_t mem, uint32_t cls, double A,
                                          uint32_t& misses) {
   const double q = a.w0_is_one ? A : __ddiv_rn(A, a.w0);
-  if (a.lut_exact && q < (double)a.lut_entries && q == floor(q))
+  if (a.lut_exact && q < (double)a.lut_entries && q == floor(q) && (!a.mfd_A || a.w0_is_one))
     return __ldg(a.ftab + ((size_t)mem * 3 + cls) * a.lut_entries + (uint32_t)q);
   ++misses;
   const double pd = cls == 0 ? a.powdist_h : cls == 1 ? a.powdist_v : a.powdist_d;
@@ -496,6 +496,15 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         } while (code != kNoFlowCode);
       }
       __syncthreads();
+    } else if (a.mfd_A) {
+      // routing = kMfd: the erosion reads the MFD drainage area (simulation.cpp:55-60),
+      // final before this kernel (k_mfd_tiles)
+      if constexpr (!EX)
+        for (uint32_t i = tid; i < (nl ? s.lvs[nl] : 0u); i += kTTPB) {
+          const uint32_t q = s.list[i];
+          ACC(q) = __ldg(a.mfd_A + gcell(q));
+        }
+      __syncthreads();
     } else {
       // deepest level first: A = w + the children's A in slot order (the
       // reference's FP summation order, accumulation.hpp:21-28)
@@ -785,6 +794,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
         double A = a.w0;
         const uint32_t nk = l + 1 < (int)nl ? s.nk[i] : 0u, c0 = s.fc[i];
         for (uint32_t q = 0; q < nk; ++q) A = __dadd_rn(A, s.A[c0 + q]);
+        if (a.mfd_A) A = __ldg(a.mfd_A + s.cell[i]);  // routing = kMfd: the MFD area (k_mfd_tiles)
         s.A[i] = A;
       }
       __syncthreads();

@@ -35,6 +35,7 @@
 #include "k_tiles.cuh"
 #include "k_forest.cuh"
 #include "k_mfd.cuh"
+#include "k_mfd_tiles.cuh"
 #include "k_util.cuh"
 
 using namespace lemgpu;
@@ -46,6 +47,7 @@ struct lemgpu_ctx {
   lemgpu_params params{};
   std::vector<lemgpu_member> members;
   int scan_grid = 0, chunk_grid = 0, deep_grid = 0, tile_grid = 0;
+  int tile_grid_mfd = 0;  // CTAs of the FP-area k_tiles that MFD routing runs
   int esc_grid = 0;  // CTAs of the level expansion of the escaped trees (a small workload)
   int deep_coop_grid = 0;  // CTAs of k_deep_coop (kDeepTPB threads, co-resident)
   int forest_grid = 0;     // CTAs of k_esc_forest (kFTPB threads, co-resident)
@@ -53,6 +55,9 @@ struct lemgpu_ctx {
   int use_tiles = 1;  // k_tiles + escape path (else the global level path for every tree)
   bool opt_global = false;  // lemgpu_options::global_path (the tile path stays off after routing = d8 again)
   int routing = 0;          // 0 d8 / d4 (StepSetup::routing kD8), 1 kMfd (lemgpu_set_routing)
+  bool opt_mfd_levels = false;  // lemgpu_options::mfd_levels (MFD through the level-synchronous global path)
+  int mfd_tiles_grid = 0;       // CTAs of k_mfd_tiles (persistent)
+  uint32_t mfd_src = 0;         // buffer the last step read (the MFD plan export rebuilds from it)
   // ping-pong elevation buffers: a step reads hbuf[p] and writes hbuf[p ^ 1];
   // graph[p] / exec[p] is the step that reads hbuf[p]
   double* hbuf[2] = {nullptr, nullptr};
@@ -393,6 +398,7 @@ StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
   if (ctx->use_tiles) a.scan_grid = (uint32_t)ctx->esc_grid;
   if (!ctx->use_tiles) a.planes = nullptr;  // only k_tiles reads the code bit planes
   a.dmask_valid = ctx->use_tiles ? 0 : 1;   // the tile path derives donor masks from the codes where needed
+  if (a.mfd_A) a.esc_forest = 0;  // k_esc_forest carries integer counts; the MFD area is read by the other kernels
   return a;
 }
 
@@ -402,7 +408,7 @@ const void* tiles_fn_nk(int nk) {
                                                                 : (const void*)k_tiles<CONN, 0, EX>;
 }
 const void* tiles_fn(const StepArgs& a) {
-  if (a.lut_exact) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
+  if (a.lut_exact && !a.mfd_A) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
   return a.conn == 8 ? tiles_fn_nk<8, false>(a.nkind) : tiles_fn_nk<4, false>(a.nkind);
 }
 // the tile path's receiver pass (k_recv): division-free selection for D8 with unit cardinal spacing
@@ -413,7 +419,9 @@ const void* recv_fn(const StepArgs& a) {
 const void* forest_fn(int nk) {
   return nk == 1 ? (const void*)k_esc_forest<1> : nk == 2 ? (const void*)k_esc_forest<2> : (const void*)k_esc_forest<0>;
 }
-size_t tiles_smem(const StepArgs& a) { return a.lut_exact ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>(); }
+size_t tiles_smem(const StepArgs& a) {
+  return a.lut_exact && !a.mfd_A ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>();
+}
 
 // The step graph that reads hbuf[p]; with_stats: ending with the ensemble
 // statistics and their all-reduce.
@@ -438,7 +446,20 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
   cudaGraphNode_t prev = nullptr;
   int rc;
   const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
-  if (ctx->use_tiles && ctx->pipe > 1) {
+  if (ctx->use_tiles && a.mfd_A) {
+    // routing = kMfd: the MFD drainage area first (pass 0 over every tile,
+    // then the queued tiles until a pass queues none), then the D8 tile path
+    CU(ctx, cudaGraphConditionalHandleCreate(&a.h_mfd, g, 0, cudaGraphCondAssignDefault));
+    StepArgs a0 = a;
+    a0.mfd_all = 1;
+    a.mfd_all = 0;
+    if ((rc = add_kernel(ctx, g, &prev, (const void*)k_mfd_tiles, dim3(ctx->mfd_tiles_grid), dim3(kMTPB),
+                         kMfdTileSmemBytes, &a0, nullptr)) ||
+        (rc = add_while(ctx, g, &prev, a.h_mfd, (const void*)k_mfd_tiles, dim3(ctx->mfd_tiles_grid),
+                        kMfdTileSmemBytes, &a)))
+      return rc;
+  }
+  if (ctx->use_tiles && ctx->pipe > 1 && !a.mfd_A) {
     // pipelined: the receiver pass in bands of tile rows (a chain), k_tiles of
     // band b after the receivers of band b+1; k_tiles limited to 4 CTAs per
     // SM so the next receiver band's CTAs run beside it
@@ -485,7 +506,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
       return rc;
   } else if (ctx->use_tiles) {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
-        (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(ctx->tile_grid), dim3(kTTPB), tiles_smem(a), &a,
+        (rc = add_kernel(ctx, g, &prev, tiles_fn(a), dim3(a.mfd_A ? ctx->tile_grid_mfd : ctx->tile_grid), dim3(kTTPB),
+                         tiles_smem(a), &a,
                          &ctx->tmap[p])) ||
         (ctx->esc_small &&
          (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
@@ -618,6 +640,11 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   }
   a.unit_card = (a.dist[1] == 1.0 && a.dist[3] == 1.0) ? 1 : 0;
   a.rinv_diag = 1.0 / a.dist[0];
+  a.dist_recip = 0;
+  for (int k = 0; k < 8; ++k) {
+    a.rdist[k] = 1.0 / a.dist[k];
+    if (a.dist[k] >= 1.0 && a.dist[k] < 0x1p500) a.dist_recip |= 1u << k;
+  }
   a.powdist_h = std::pow(a.dist[3], p->n_exp);
   a.powdist_v = std::pow(a.dist[1], p->n_exp);
   a.powdist_d = std::pow(a.dist[0], p->n_exp);
@@ -709,6 +736,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   c0.t_k1_end = 0;
   c0.t_t_begin = ~0ull;
   c0.t_t_end = 0;
+  c0.t_mfd_begin = ~0ull;
   CUB(cudaMemcpy(a.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
 
   // launch geometry
@@ -722,6 +750,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   if (ctx->esc_grid < 1 || ctx->esc_grid > ctx->scan_grid) ctx->esc_grid = ctx->scan_grid;
   if (o.global_path) ctx->use_tiles = 0;
   ctx->opt_global = o.global_path != 0;
+  ctx->opt_mfd_levels = o.mfd_levels != 0;
   a.force_escape = 0;
   a.force_escape = o.force_escape;
   {
@@ -733,6 +762,14 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     if (o.tile_grid) tg = o.tile_grid;  // testing: few CTAs, many tiles each
     if (tg < 1) tg = 1;
     ctx->tile_grid = (int)(tg < ntiles ? tg : ntiles);
+    // MFD routing runs the FP-area instantiation (the MFD area is not a cell count)
+    StepArgs am = a;
+    am.mfd_A = reinterpret_cast<double*>(16);  // only selects the instantiation
+    const void* fm = tiles_fn(am);
+    CUB(cudaFuncSetAttribute(fm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiles_smem(am)));
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fm, kTTPB, tiles_smem(am)));
+    tg = o.tile_grid ? o.tile_grid : (uint32_t)(occ > 0 ? occ : 1) * (uint32_t)nsm;
+    ctx->tile_grid_mfd = (int)(tg < ntiles ? tg : ntiles);
   }
   a.eager = 0;
   a.force_deep = o.force_deep ? 1 : 0;
@@ -771,6 +808,10 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     ctx->forest_grid = (occf > 0 ? occf : 1) * nsm;
     CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_mfd_levels, kTPB, 0));
     ctx->mfd_grid = std::min(ctx->scan_grid, (occf > 0 ? occf : 1) * nsm);
+    CUB(cudaFuncSetAttribute((const void*)k_mfd_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMfdTileSmemBytes));
+    CUB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_mfd_tiles, kMTPB, kMfdTileSmemBytes));
+    ctx->mfd_tiles_grid = (occf > 0 ? occf : 1) * nsm;
   }
   {
     const void* fdc = a.nkind == 1 ? (const void*)k_deep_coop<1> : a.nkind == 2 ? (const void*)k_deep_coop<2>
@@ -903,6 +944,20 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
   cudaStream_t st = ctx->stream;
   set_eager_conds(a, st);
   enqueue_stats_pass(ctx, a, st);
+  if (ctx->use_tiles && a.mfd_A) {  // the MFD tile passes, the loop condition through the control block
+    StepArgs a0 = a;
+    a0.mfd_all = 1;
+    a.mfd_all = 0;
+    k_mfd_tiles<<<ctx->mfd_tiles_grid, kMTPB, kMfdTileSmemBytes, st>>>(a0);
+    unsigned cond[4];
+    const char* cbase = reinterpret_cast<const char*>(a.ctl) + offsetof(Ctl, cond);
+    for (;;) {
+      CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
+      CU(ctx, cudaStreamSynchronize(st));
+      if (!cond[3]) break;
+      k_mfd_tiles<<<ctx->mfd_tiles_grid, kMTPB, kMfdTileSmemBytes, st>>>(a);
+    }
+  }
   if (ctx->use_tiles) {
     const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
     {
@@ -910,7 +965,7 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
       CU(ctx, cudaLaunchKernel(recv_fn(a), g1, dim3(kTPB), rargs, 0, st));
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ctx->tile_grid);
+    cfg.gridDim = dim3(a.mfd_A ? ctx->tile_grid_mfd : ctx->tile_grid);
     cfg.blockDim = dim3(kTTPB);
     cfg.dynamicSmemBytes = tiles_smem(a);
     cfg.stream = st;
@@ -1069,6 +1124,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   k_finalize<<<1, 32, 0, st>>>(a);
   CU(ctx, cudaGetLastError());
   if (tev) CU(ctx, cudaEventRecord(tev[1], st));
+  ctx->mfd_src = p;
   ctx->cur = p ^ 1u;
   ++ctx->pending;
   ++ctx->st_steps;
@@ -1142,6 +1198,7 @@ int enqueue_step(lemgpu_ctx* ctx) {
   }
   ++ctx->st_steps;
   if (ev) CU(ctx, cudaEventRecord(ev[1], ctx->stream));
+  ctx->mfd_src = p;
   ctx->cur = p ^ 1u;
   ++ctx->pending;
   ctx->have_graph = true;
@@ -1183,7 +1240,7 @@ void lemgpu_destroy(lemgpu_ctx* ctx) {
   if (a.dbg_level) cudaFree(a.dbg_level);
   if (a.dbg_A) cudaFree(a.dbg_A);
   for (void* q : {(void*)a.mfd_A, (void*)a.mfd_wsum, (void*)a.mfd_lm, (void*)a.mfd_rem, (void*)a.mfd_ord,
-                  (void*)a.mfd_lv, (void*)a.mfd_lev})
+                  (void*)a.mfd_lv, (void*)a.mfd_lev, (void*)a.mfd_wl, (void*)a.mfd_stamp})
     if (q) cudaFree(q);
   if (ctx->st_local) cudaFree(ctx->st_local);
   if (ctx->st_part) cudaFree(ctx->st_part);
@@ -1393,6 +1450,7 @@ int lemgpu_sync(lemgpu_ctx* ctx, lemgpu_diag* out, uint32_t cap, uint32_t* count
       // input buffer (steps never write the buffer they read; later steps
       // of the batch did not run)
       ctx->cur = ctx->cur_synced = (c0buf + s) & 1u;
+      ctx->mfd_src = ctx->cur;  // the failed step read this buffer
       break;
     }
     ctx->last_nlevels = d[s].nlevels;
@@ -1463,7 +1521,7 @@ int lemgpu_step_host(lemgpu_ctx* ctx, double* elev_inout, lemgpu_diag* diag) {
   if (!ctx || !elev_inout) return fail(ctx, LEMGPU_ECONFIG, "null argument");
   CU(ctx, cudaSetDevice(ctx->device));
   const StepArgs& a = ctx->a;
-  if (ctx->use_tiles && ctx->bands > 1 && !a.eager) {
+  if (ctx->use_tiles && ctx->bands > 1 && !a.eager && !a.mfd_A) {
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, elev_inout) == cudaSuccess && pa.type == cudaMemoryTypeHost)
       return step_host_banded(ctx, elev_inout, diag);
@@ -1656,24 +1714,27 @@ int lemgpu_set_routing(lemgpu_ctx* ctx, int routing, double mfd_exponent) {
   }
   StepArgs& a = ctx->a;
   const size_t N = a.N;
+  const size_t ntm = (size_t)((a.W + kMX - 1) / kMX) * ((a.Htot + kMY - 1) / kMY);  // k_mfd_tiles tiles
   if (routing == 1 && !a.mfd_A) {
     if ((dmalloc(ctx, &a.mfd_A, N)) || (dmalloc(ctx, &a.mfd_wsum, N)) || (dmalloc(ctx, &a.mfd_lm, N)) ||
         (dmalloc(ctx, &a.mfd_rem, N)) || (dmalloc(ctx, &a.mfd_ord, N)) || (dmalloc(ctx, &a.mfd_lv, N + 2)) ||
-        (dmalloc(ctx, &a.mfd_lev, N)))
+        (dmalloc(ctx, &a.mfd_lev, N)) || (dmalloc(ctx, &a.mfd_wl, 2 * ntm)) || (dmalloc(ctx, &a.mfd_stamp, ntm)))
       return LEMGPU_ECUDA;
+    CU(ctx, cudaMemset(a.mfd_stamp, 0, ntm * sizeof(uint32_t)));
+    CU(ctx, cudaMemset(a.mfd_A, 0, N * sizeof(double)));
   } else if (routing == 0 && a.mfd_A) {
     for (void* q : {(void*)a.mfd_A, (void*)a.mfd_wsum, (void*)a.mfd_lm, (void*)a.mfd_rem, (void*)a.mfd_ord,
-                    (void*)a.mfd_lv, (void*)a.mfd_lev})
+                    (void*)a.mfd_lv, (void*)a.mfd_lev, (void*)a.mfd_wl, (void*)a.mfd_stamp})
       cudaFree(q);
     a.mfd_A = a.mfd_wsum = nullptr;
     a.mfd_lm = nullptr;
-    a.mfd_rem = a.mfd_ord = a.mfd_lv = a.mfd_lev = nullptr;
+    a.mfd_rem = a.mfd_ord = a.mfd_lv = a.mfd_lev = a.mfd_wl = a.mfd_stamp = nullptr;
   }
   a.mfd_exp = mfd_exponent;
   ctx->routing = routing;
-  // the MFD area feeds the global level path's physics (the tile kernels
-  // accumulate their own trees); d8 again: back to the configured path
-  ctx->use_tiles = routing == 1 || ctx->opt_global ? 0 : 1;
+  // MFD: the area by tile passes ahead of the D8 tile path (option
+  // mfd_levels: the level-synchronous plan + the global level path)
+  ctx->use_tiles = ctx->opt_global || (routing == 1 && ctx->opt_mfd_levels) ? 0 : 1;
   return rebuild_graphs(ctx);
 }
 
@@ -1688,6 +1749,18 @@ int lemgpu_download_mfd(lemgpu_ctx* ctx, double* A, uint32_t* order, uint32_t* l
   const StepArgs& a = ctx->a;
   const size_t N = a.N;
   if (A) CU(ctx, cudaMemcpy(A, a.mfd_A, N * sizeof(double), cudaMemcpyDeviceToHost));
+  if ((order || levels || nlevels) && ctx->use_tiles) {
+    // the tile passes need no plan: rebuild the step's (generate_mfd_order)
+    // from the elevation that step read -- k_mfd_levels also re-evaluates A
+    // level by level, to the same bits
+    StepArgs b = step_args(ctx, ctx->mfd_src);
+    b.eager = 1;
+    k_mfd_graph<<<ctx->deep_grid, kTPB, 0, ctx->stream>>>(b);
+    void* margs[] = {&b};
+    CU(ctx, cudaLaunchCooperativeKernel((const void*)k_mfd_levels, dim3(ctx->mfd_grid), dim3(kTPB), margs, 0,
+                                        ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   if (order || levels || nlevels) {
     // the reference's TraversalPlan (mfd.cpp:66-104): level-major, ascending
     // within a level -- a counting sort of the cell-major levels

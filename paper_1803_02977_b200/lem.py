@@ -224,12 +224,13 @@ class StepDiagnostics:
     escaped_trees: int = 0  # trees finished by the escape path (tile path), else source chunks
     kernel_seconds: List[float] = field(default_factory=lambda: [0.0] * 4)  # receiver, tile, escape-levels, escape-physics spans
     escaped_cells: int = 0
+    mfd_passes: int = 0  # routing = kMfd: tile passes of the MFD accumulation (k_mfd_tiles)
 
     @staticmethod
     def from_abi(d: _abi.lemgpu_diag) -> "StepDiagnostics":
         return StepDiagnostics(list(d.seconds), int(d.newton_iters), int(d.interior_noflow),
                                int(d.nlevels), int(d.lut_misses), int(d.escaped_trees), list(d.kernel_s),
-                               int(d.escaped_cells))
+                               int(d.escaped_cells), int(d.mfd_passes))
 
     @property
     def timings(self):
@@ -249,7 +250,7 @@ _KNOB_NAMES = {
     "LEMGPU_ESC_SMALL_GRID": ("esc_small_grid", int), "LEMGPU_PIPE_TILE_GRID": ("pipe_tile_grid", int),
     "LEMGPU_LUT_ENTRIES": ("lut_entries", int), "LEMGPU_HOST_BANDS": ("host_bands", int),
     "LEMGPU_PATCH_CAP": ("patch_cap", int), "LEMGPU_HOST_PROFILE": ("host_profile", int),
-    "LEMGPU_ESC_FOREST": ("esc_forest", int),
+    "LEMGPU_ESC_FOREST": ("esc_forest", int), "LEMGPU_MFD_LEVELS": ("mfd_levels", int),
 }
 
 

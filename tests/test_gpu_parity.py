@@ -716,20 +716,30 @@ def test_ensemble_shard_with_nccl_allreduce_in_graph(oracle):
 
 # ---- MFD routing: StepSetup::routing = kMfd -------------------------------
 
-def _mfd_ctx(w, h, ex, conn=8, members=1, **kw):
-    ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=members)
+# MFD schedules: the area by tile passes + the D8 tile path (default), with
+# every tree escaping to k_esc_small or to the cooperative escape kernels,
+# eagerly launched (the pass loop on the host), and the level-synchronous
+# plan + global level path (mfd_levels)
+MFD_PATHS = {"tiles": None, "tiles-escape": {"force_escape": 1}, "tiles-escape-coop": {"force_escape": 2, "no_esc_small": 1},
+             "tiles-eager": {"eager": 1}, "levels": {"mfd_levels": 1}}
+
+
+def _mfd_ctx(w, h, ex, conn=8, members=1, options=None, **kw):
+    ctx = lem.DeviceContext(w, h, sim_params(**kw), conn, members=members, options=options)
     ctx.set_routing(lem.Routing.kMfd, ex)
     return ctx
 
 
-def test_mfd_golden(oracle, golden_dir):
+@pytest.mark.parametrize("path", sorted(MFD_PATHS))
+def test_mfd_golden(oracle, golden_dir, path):
     """Every mfd_*.npz fixture (made by the unmodified reference's simulate_step
     with Routing::kMfd): h after the step, Newton iterations, the MFD drainage
-    area and the MFD plan, bit for bit."""
+    area and the MFD plan, bit for bit -- on every MFD schedule."""
+    opts = MFD_PATHS[path]
     for path in sorted(golden_dir.glob("mfd_*.npz")):
         g = np.load(path)
         kw = json.loads(str(g["params"]))
-        ctx = _mfd_ctx(int(g["w"]), int(g["h"]), float(g["exponent"]), int(g["conn"]), **kw)
+        ctx = _mfd_ctx(int(g["w"]), int(g["h"]), float(g["exponent"]), int(g["conn"]), options=opts, **kw)
         ctx.upload(g["h0"])
         d = ctx.step(1)[0]
         assert np.array_equal(ctx.download().view(np.uint64), g["h1"].view(np.uint64)), path.name
@@ -746,10 +756,12 @@ def test_mfd_golden(oracle, golden_dir):
     (120, 90, 55, 8, 1.0, {"n_exp": 2.0}, "noise"), (200, 150, 56, 8, 1.0, {}, "ramp"),
     (400, 12, 57, 8, 0.7, {}, "ramp"), (3, 3, 58, 8, 1.0, {}, "noise"),
 ])
-def test_mfd_steps_vs_oracle(oracle, w, h, seed, conn, ex, kw, terrain):
+@pytest.mark.parametrize("path", sorted(MFD_PATHS))
+def test_mfd_steps_vs_oracle(oracle, w, h, seed, conn, ex, kw, terrain, path):
     """4 MFD steps per shape (odd widths, D4, anisotropic spacing, exponents
-    0.7-2, n = 2, deep ramps): h, A and the MFD plan against the oracle each step."""
-    ctx = _mfd_ctx(w, h, ex, conn, **kw)
+    0.7-2, n = 2, deep ramps): h, A and the MFD plan against the oracle each
+    step, on every MFD schedule; the tile passes converge (mfd_passes > 0)."""
+    ctx = _mfd_ctx(w, h, ex, conn, options=MFD_PATHS[path], **kw)
     e = oracle.terrain(w, h, seed) if terrain == "noise" else _ramp(w, h, seed)
     ctx.upload(e)
     p = make_params(**kw)
@@ -760,15 +772,17 @@ def test_mfd_steps_vs_oracle(oracle, w, h, seed, conn, ex, kw, terrain):
         assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), f"step {s}"
         assert d.newton_iters == o["newton_iters"] and d.interior_noflow == o["interior_noflow"]
         assert d.nlevels == o["nlevels"]  # the D8 plan's levels (the erosion's)
+        assert (d.mfd_passes > 0) == (path != "levels")
         m = ctx.download_mfd()
         assert np.array_equal(m["A"].view(np.uint64), o["A"].view(np.uint64)), f"step {s}"
         assert np.array_equal(m["order"], o["mfd_order"]) and np.array_equal(m["levels"], o["mfd_levels"])
 
 
-def test_mfd_ensemble_members(oracle):
+@pytest.mark.parametrize("path", ["tiles", "levels"])
+def test_mfd_ensemble_members(oracle, path):
     """A stacked ensemble under MFD routing: every member equals its own oracle run."""
     M, w, h = 3, 90, 70
-    ctx = _mfd_ctx(w, h, 1.0, members=M)
+    ctx = _mfd_ctx(w, h, 1.0, members=M, options=MFD_PATHS[path])
     seeds = [61, 62, 63]
     ctx.generate_terrain(seeds)
     es = [oracle.terrain(w, h, sd) for sd in seeds]
@@ -822,3 +836,24 @@ def test_mfd_routing_switch_and_dropin(oracle):
         else:
             oracle.step(ref_e, want_donor=False)
         assert np.array_equal(e.view(np.uint64), ref_e.view(np.uint64)), routing
+
+
+@pytest.mark.parametrize("mode", [1, 2], ids=["exact", "epsilon"])
+def test_mfd_filled_dem_vs_oracle(oracle, mode):
+    """MFD routing on a Priority-Flood-filled DEM (flats / epsilon ramps: long
+    descending chains that cross many tile edges, many tile passes): h, A and
+    the MFD plan against the oracle for 3 steps."""
+    w, h = 160, 120
+    e = oracle.fill(oracle.terrain(w, h, 71), mode)
+    ctx = _mfd_ctx(w, h, 1.0)
+    ctx.upload(e)
+    for s in range(3):
+        d = ctx.step(1)[0]
+        o = oracle.step_mfd(e)
+        assert o["status"] == 0
+        assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64)), s
+        assert d.newton_iters == o["newton_iters"]
+        m = ctx.download_mfd()
+        assert np.array_equal(m["A"].view(np.uint64), o["A"].view(np.uint64)), s
+        assert np.array_equal(m["order"], o["mfd_order"]) and np.array_equal(m["levels"], o["mfd_levels"])
+    assert d.mfd_passes >= 2
