@@ -177,6 +177,7 @@ struct Ctl {
   uint32_t mfd_cnt[3], mfd_nlev;         // k_mfd_levels: per-level append counters, MFD plan levels
   uint32_t mfd_pass, mfd_wl_n[2];        // k_mfd_tiles: pass id (monotonic), queued tiles per pass parity
   uint32_t mfd_passes;                   // ... passes of this step
+  uint32_t mfd_g, mfd_done;              // ... grid of the next pass, cells finalised in the running pass
   unsigned long long t_mfd_begin;        // ... first pass start (the step's device time starts there)
   unsigned long long fr_t[3];            // ... latest end over the CTAs of the counts, F and erosion sweeps
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;

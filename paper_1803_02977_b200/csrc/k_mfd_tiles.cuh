@@ -6,26 +6,25 @@
 //   accumulate_mfd         proj/src/mfd.cpp:106-132, add_mfd_donor_flow mfd.hpp:66-73
 //
 // A[c] = w + sum over the donors n of c, in slot order, of alpha(n, c) * A[n]
-// (alpha = RN(pow(slope, e) / wsum[n])): every cell's value is one fixed
-// function of its donors' values, and the donors are strictly higher, so the
-// system has exactly one solution -- the reference's bits -- and any
-// evaluation order that reads final donor values reproduces them.  The
-// reference orders the whole raster by dependency levels (generate_mfd_order)
-// and sweeps them; a level-synchronous sweep on the device reads every
-// level's cells scattered over the raster (~1.4 KB of DRAM traffic per cell at
-// 10000^2).  Here a CTA owns a 64x32 tile: it stages the tile's elevations
-// with two rings, derives the lower masks and weight sums of the tile and its
-// first ring, orders the tile's cells by in-tile dependency counting (a cell
-// is ready when its donors inside the tile are done) and evaluates A level by
-// level in shared memory; donors in the ring contribute the values currently
-// in the global A.  A tile whose border cells changed the value that a
-// neighbouring tile reads (a cell with a receiver across the tile edge)
-// queues that neighbour for the next pass.  Pass 0 runs every tile; the
-// passes repeat (graph WHILE node) until a pass queues nothing.  Then every
-// tile was last evaluated on inputs equal to the current values: the global
-// A is the fixed point, i.e. exactly the reference's accumulation.  (The
-// number of passes is bounded by how often a dependency chain crosses tile
-// edges, ~12 at 1000^2 random noise; the late passes touch a few tiles.)
+// (alpha = RN(pow(slope, e) / wsum[n])): once every donor of c has its final
+// value, evaluating this expression gives c the reference's bits, whatever
+// order the cells are finalised in.  The reference orders the whole raster by
+// dependency levels (generate_mfd_order) and sweeps them; a level-synchronous
+// device sweep reads every level's cells scattered over the raster (~1.4 KB
+// of DRAM traffic per cell at 10000^2).  Here a CTA owns a 64x32 tile: it
+// stages the elevations of the tile and two rings, derives the lower masks
+// and weight sums of the tile and its first ring, and finalises the tile's
+// cells by in-tile dependency counting (a cell is ready when all its donors
+// are final), level by level in shared memory.  A cell stays unfinished while
+// a donor in another tile is unfinished; unfinished cells hold a NaN
+// sentinel in the global A, so a donor's 8-byte value is either its final
+// value or the sentinel.  Pass 0 runs every tile and reads no other tile;
+// each further pass runs the tiles (of a grid shifted by half a tile on
+// alternate passes, so chains that zig-zag along a tile edge land inside one
+// tile) that hold unfinished cells, reading the first ring from the global A.
+// Every pass finalises at least the highest unfinished cell; the passes
+// repeat (graph WHILE node) until none is left.  Each cell is evaluated once,
+// from final donors: A is exactly the reference's accumulation.
 //
 // The MFD plan itself (generate_mfd_order) is needed only by the export
 // (lemgpu_download_mfd), which rebuilds it with k_mfd_graph + k_mfd_levels
@@ -43,18 +42,27 @@ constexpr int kMWY = kMY + 4;           // window rows
 constexpr int kMN = kMP * kMWY;         // window cells
 constexpr int kMT = kMX * kMY;          // tile cells
 constexpr int kMTPB = 256;
-constexpr uint32_t kMfdMaxPasses = 1u << 20;  // safety bound (a DAG converges far earlier)
+constexpr unsigned long long kMfdUnset = 0x7FF4DEAD00000000ull;  // NaN payload: not final yet
+
+// Tiles of grid g (0: origin (0, 0); 1: shifted by (-kMX/2, -kMY/2)).
+__host__ __device__ __forceinline__ uint32_t mfd_ntx(uint32_t W, int g) { return (W + (g ? kMX / 2 : 0) + kMX - 1) / kMX; }
+__host__ __device__ __forceinline__ uint32_t mfd_nty(uint32_t H, int g) { return (H + (g ? kMY / 2 : 0) + kMY - 1) / kMY; }
+// work-list / stamp capacity per grid
+__host__ __device__ __forceinline__ uint32_t mfd_cap(uint32_t W, uint32_t H) {
+  const uint32_t a = mfd_ntx(W, 0) * mfd_nty(H, 0), b = mfd_ntx(W, 1) * mfd_nty(H, 1);
+  return a > b ? a : b;
+}
 
 struct MfdTileSmem {
   double h[kMN];        // window elevations (0 off the raster: never read for an existing neighbour)
   double ws[kMN];       // weight sums (tile + first ring; interior cells)
-  double A[kMN];        // drainage area: first ring from the global A, tile evaluated here
-  uint32_t rem[kMT];    // in-tile donors not yet evaluated
-  uint16_t list[kMT];   // the tile's cells, dependency-level-major
+  double A[kMN];        // drainage area (tile + first ring): final value or the kMfdUnset bits
+  uint32_t rem[kMT];    // unfinished donors of an unfinished tile cell
+  uint16_t list[kMT];   // cells finalised in this visit, level-major
   uint8_t lm[kMN];      // mask of strictly lower neighbours (0: boundary / off raster / outer ring)
   uint32_t cnt[3];      // per-level append counters (rotating)
-  uint32_t mark;        // neighbour tiles to queue: bit (dy+1)*3 + (dx+1)
-  uint32_t pass, n;     // pass id, work items of this pass
+  uint32_t mark;        // next-grid tiles to queue: bit dy*2 + dx
+  uint32_t pass, n, g;  // pass id, work items and grid of this pass
 };
 constexpr size_t kMfdTileSmemBytes = sizeof(MfdTileSmem);
 
@@ -63,44 +71,60 @@ __device__ __forceinline__ bool m_in_tile(int q) {
   const int y = q / kMP, x = q - y * kMP;
   return (unsigned)(x - 2) < (unsigned)kMX && (unsigned)(y - 2) < (unsigned)kMY;
 }
+__device__ __forceinline__ bool m_unset(double v) { return (unsigned long long)__double_as_longlong(v) == kMfdUnset; }
 
-// One pass over the queued tiles (a.mfd_all: every tile, pass 0 of the step).
+// One pass over the queued tiles (a.mfd_all: pass 0 of the step, every tile of grid 0).
 __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
   extern __shared__ __align__(16) unsigned char mraw[];
   MfdTileSmem& s = *reinterpret_cast<MfdTileSmem*>(mraw);
   Ctl* ctl = a.ctl;
   const int all = a.mfd_all;
   const uint32_t tid = threadIdx.x;
-  const uint32_t ntx = (a.W + kMX - 1) / kMX, nty = (a.Htot + kMY - 1) / kMY, ntiles = ntx * nty;
   PhWhole ph(ctl, LEMGPU_PHASE_ACCUM);
   if (tid == 0) {
     if (all) atomicMin(&ctl->t_mfd_begin, globaltimer());
     const uint32_t P = ld_volatile_u32(&ctl->mfd_pass);
+    const uint32_t g = all ? 0u : ld_volatile_u32(&ctl->mfd_g);
     s.pass = P;
-    s.n = ld_volatile_u32(&ctl->err_flag) ? 0u : all ? ntiles : ld_volatile_u32(&ctl->mfd_wl_n[P & 1u]);
+    s.g = g;
+    s.n = ld_volatile_u32(&ctl->err_flag) ? 0u
+          : all ? mfd_ntx(a.W, 0) * mfd_nty(a.Htot, 0) : ld_volatile_u32(&ctl->mfd_wl_n[P & 1u]);
   }
   __syncthreads();
   const uint32_t P = s.pass, nitems = s.n;
-  const uint32_t* wl = a.mfd_wl + (size_t)(P & 1u) * ntiles;
-  uint32_t* wl_next = a.mfd_wl + (size_t)((P + 1u) & 1u) * ntiles;
+  const int g = (int)s.g;
+  const uint32_t ntx = mfd_ntx(a.W, g);
+  const uint32_t ntx1 = mfd_ntx(a.W, g ^ 1), nty1 = mfd_nty(a.Htot, g ^ 1);
+  const uint32_t cap = mfd_cap(a.W, a.Htot);
+  const uint32_t* wl = a.mfd_wl + (size_t)(P & 1u) * cap;
+  uint32_t* wl_next = a.mfd_wl + (size_t)((P + 1u) & 1u) * cap;
   const int W = (int)a.W, Ht = (int)a.Htot;
+  const int sx = g ? kMX / 2 : 0, sy = g ? kMY / 2 : 0;          // this grid's shift
+  const int nsx = g ? 0 : kMX / 2, nsy = g ? 0 : kMY / 2;        // the next grid's
+  uint32_t done = 0;                                             // cells this CTA finalised
   for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
     const uint32_t t = all ? it : __ldcg(wl + it);
     const int tx = (int)(t % ntx), ty = (int)(t / ntx);
-    const int wx0 = tx * kMX - 2, wy0 = ty * kMY - 2;
+    const int x0 = tx * kMX - sx, y0 = ty * kMY - sy;  // first tile cell
+    const int wx0 = x0 - 2, wy0 = y0 - 2;
     __syncthreads();  // the previous tile is done with shared memory
-    // ---- stage: elevations of the window, the global A of the first ring
+    // ---- stage: window elevations; A of the tile and the first ring (pass 0:
+    // nothing is final yet -- other tiles' values may be a previous step's)
+    uint32_t unf = 0;
     for (int i = (int)tid; i < kMN; i += kMTPB) {
       const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
       const bool in = gx >= 0 && gx < W && gy >= 0 && gy < Ht;
-      const size_t g = (size_t)gy * a.W + gx;
-      s.h[i] = in ? __ldg(a.h + g) : 0.0;
-      const bool ring1 = x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1 && !m_in_tile(i);
-      if (ring1) s.A[i] = in ? __ldcg(a.mfd_A + g) : 0.0;
+      const size_t g0 = (size_t)gy * a.W + gx;
+      s.h[i] = in ? __ldg(a.h + g0) : 0.0;
+      if (x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1) {
+        const double v = in && !all ? __ldcg(a.mfd_A + g0) : __longlong_as_double((long long)kMfdUnset);
+        s.A[i] = v;
+        unf += in && m_in_tile(i) && m_unset(v) ? 1u : 0u;
+      }
     }
     if (tid < 3) s.cnt[tid] = 0;
     if (tid == 0) s.mark = 0;
-    __syncthreads();
+    if (__syncthreads_count(unf != 0) == 0) continue;  // every cell of this tile is final
     // ---- compute_mfd for the tile and its first ring: lower mask, weight sum
     for (int i = (int)tid; i < kMN; i += kMTPB) {
       const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
@@ -124,20 +148,22 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       s.ws[i] = wsum;
     }
     __syncthreads();
-    // ---- in-tile dependency counts; level 0 = cells without donors in the tile
+    // ---- unfinished tile cells: count their unfinished donors; level 0 = none
     for (int j = (int)tid; j < kMT; j += kMTPB) {
       const int q = (j / kMX + 2) * kMP + (j % kMX) + 2;
+      if (!m_unset(s.A[q]) || x0 + j % kMX >= W || y0 + j / kMX >= Ht || x0 + j % kMX < 0 || y0 + j / kMX < 0)
+        continue;
       uint32_t r = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int n = q + mwoff(k);
-        r += (m_in_tile(n) && ((s.lm[n] >> (7 - k)) & 1u)) ? 1u : 0u;
+        r += (((s.lm[n] >> (7 - k)) & 1u) && m_unset(s.A[n])) ? 1u : 0u;
       }
       s.rem[j] = r;
       if (r == 0) s.list[atomicAdd(&s.cnt[0], 1u)] = (uint16_t)q;
     }
     __syncthreads();
-    // ---- levels: evaluate A, release the in-tile receivers
+    // ---- levels: evaluate A (every donor final), release the in-tile receivers
     uint32_t qs = 0, qe = s.cnt[0];
     for (uint32_t l = 0; qs < qe; ++l) {
       uint32_t* nc = &s.cnt[(l + 1) % 3];
@@ -145,15 +171,25 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       for (uint32_t i = qs + tid; i < qe; i += kMTPB) {
         const int q = s.list[i];
         const double hc = s.h[q];
+        // the donors' terms first (independent), then their sum in slot order
+        // (ascending index = stencil order)
+        double tk[8];
+        uint32_t dm = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int n = q + mwoff(k);
+          tk[k] = 0.0;
+          if (dir_in(a.conn, k) && ((s.lm[n] >> (7 - k)) & 1u)) {
+            dm |= 1u << k;
+            // n's weight towards q: its slope in direction 7-k (same length as k)
+            const double w = mfd_weight(a, mfd_slope(a, s.h[n], hc, 7 - k));
+            tk[k] = __dmul_rn(__ddiv_rn(w, s.ws[n]), s.A[n]);
+          }
+        }
         double acc = a.w0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // donors in slot order (ascending index = stencil order)
-          const int n = q + mwoff(k);
-          if (!dir_in(a.conn, k) || !((s.lm[n] >> (7 - k)) & 1u)) continue;
-          // n's weight towards q: its slope in direction 7-k (same length as k)
-          const double w = mfd_weight(a, mfd_slope(a, s.h[n], hc, 7 - k));
-          acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(w, s.ws[n]), s.A[n]));
-        }
+        for (int k = 0; k < 8; ++k)
+          if ((dm >> k) & 1u) acc = __dadd_rn(acc, tk[k]);
         s.A[q] = acc;
         for (uint32_t m = s.lm[q]; m; m &= m - 1) {
           const int r = q + mwoff(__ffs(m) - 1);
@@ -166,46 +202,48 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       qs = qe;
       qe += *reinterpret_cast<volatile uint32_t*>(nc);
     }
-    // ---- write the tile; a changed value that a neighbouring tile reads
-    // (a receiver across the tile edge) queues that tile
+    done += tid == 0 ? qe : 0u;
+    // ---- write the finalised cells (pass 0: every tile cell, final or the
+    // sentinel); the next grid's tiles holding cells still unfinished are queued
     for (int j = (int)tid; j < kMT; j += kMTPB) {
-      const int y = j / kMX, x = j - y * kMX, gx = tx * kMX + x, gy = ty * kMY + y;
-      if (gx >= W || gy >= Ht) continue;
+      const int y = j / kMX, x = j - y * kMX, gx = x0 + x, gy = y0 + y;
+      if (gx < 0 || gx >= W || gy < 0 || gy >= Ht) continue;
       const int q = (y + 2) * kMP + x + 2;
-      const size_t g = (size_t)gy * a.W + gx;
       const double v = s.A[q];
-      uint32_t out = 0;  // receivers in other tiles
-      if (x == 0 || x == kMX - 1 || y == 0 || y == kMY - 1)
-        for (uint32_t m = s.lm[q]; m; m &= m - 1) {
-          const int k = __ffs(m) - 1;
-          const int rx = x + dir_ox(k), ry = y + dir_oy(k);
-          const int dx = rx < 0 ? -1 : rx >= kMX ? 1 : 0, dy = ry < 0 ? -1 : ry >= kMY ? 1 : 0;
-          if (dx || dy) out |= 1u << ((dy + 1) * 3 + dx + 1);
-        }
-      if (out && __double_as_longlong(__ldcg(a.mfd_A + g)) != __double_as_longlong(v)) atomicOr(&s.mark, out);
-      __stcg(a.mfd_A + g, v);
+      if (m_unset(v)) {
+        const int ix = (gx + nsx) / kMX - (x0 + nsx) / kMX, iy = (gy + nsy) / kMY - (y0 + nsy) / kMY;
+        atomicOr(&s.mark, 1u << (iy * 2 + ix));
+        if (all) __stcg(a.mfd_A + (size_t)gy * a.W + gx, v);
+      } else {
+        __stcg(a.mfd_A + (size_t)gy * a.W + gx, v);
+      }
     }
     __syncthreads();
-    if (tid < 9 && ((s.mark >> tid) & 1u)) {
-      const int nx = tx + (int)(tid % 3) - 1, ny = ty + (int)(tid / 3) - 1;
-      if (nx >= 0 && nx < (int)ntx && ny >= 0 && ny < (int)nty) {
-        const uint32_t tn = (uint32_t)ny * ntx + (uint32_t)nx;
-        __threadfence();  // the tile's new values before the queue entry
-        if (atomicExch(a.mfd_stamp + tn, P + 1u) != P + 1u)
+    if (tid < 4 && ((s.mark >> tid) & 1u)) {
+      const uint32_t nx = (uint32_t)((x0 + nsx) / kMX + (int)(tid & 1u));
+      const uint32_t ny = (uint32_t)((y0 + nsy) / kMY + (int)(tid >> 1));
+      if (nx < ntx1 && ny < nty1) {
+        const uint32_t tn = ny * ntx1 + nx;
+        if (atomicExch(a.mfd_stamp + (size_t)(g ^ 1) * cap + tn, P + 1u) != P + 1u)
           wl_next[atomicAdd(&ctl->mfd_wl_n[(P + 1u) & 1u], 1u)] = tn;
       }
     }
   }
-  // ---- the last CTA closes the pass: the next pass runs if it has work
+  if (tid == 0 && done) atomicAdd(&ctl->mfd_done, done);
+  // ---- the last CTA closes the pass: the next pass (other grid) runs if it has work
   if (last_block_done(ctl) && tid == 0) {
     const uint32_t nn = ld_volatile_u32(&ctl->mfd_wl_n[(P + 1u) & 1u]);
+    const uint32_t fin = ld_volatile_u32(&ctl->mfd_done);
+    ctl->mfd_done = 0;
     ctl->mfd_wl_n[P & 1u] = 0;
     ctl->mfd_pass = P + 1u;
+    ctl->mfd_g = (uint32_t)(g ^ 1);
     ctl->mfd_passes += 1u;
     bool more = nn != 0;
-    if (more && ctl->mfd_passes >= kMfdMaxPasses) {  // cannot happen on a DAG; reported, never looped forever
+    if (more && fin == 0 && nitems) {  // no progress: a cycle (impossible with strict descent), reported
       more = false;
       ctl->err_flag = LEMGPU_ESTRUCTURE;
+      ctl->err_cell = 0;
       ctl->err_slot = ctl->slot;
     }
     set_cond(a, 3, more ? 1u : 0u);

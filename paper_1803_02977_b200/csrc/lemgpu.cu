@@ -1714,11 +1714,11 @@ int lemgpu_set_routing(lemgpu_ctx* ctx, int routing, double mfd_exponent) {
   }
   StepArgs& a = ctx->a;
   const size_t N = a.N;
-  const size_t ntm = (size_t)((a.W + kMX - 1) / kMX) * ((a.Htot + kMY - 1) / kMY);  // k_mfd_tiles tiles
+  const size_t ntm = 2 * (size_t)mfd_cap(a.W, a.Htot);  // k_mfd_tiles: tiles of both grids
   if (routing == 1 && !a.mfd_A) {
     if ((dmalloc(ctx, &a.mfd_A, N)) || (dmalloc(ctx, &a.mfd_wsum, N)) || (dmalloc(ctx, &a.mfd_lm, N)) ||
         (dmalloc(ctx, &a.mfd_rem, N)) || (dmalloc(ctx, &a.mfd_ord, N)) || (dmalloc(ctx, &a.mfd_lv, N + 2)) ||
-        (dmalloc(ctx, &a.mfd_lev, N)) || (dmalloc(ctx, &a.mfd_wl, 2 * ntm)) || (dmalloc(ctx, &a.mfd_stamp, ntm)))
+        (dmalloc(ctx, &a.mfd_lev, N)) || (dmalloc(ctx, &a.mfd_wl, ntm)) || (dmalloc(ctx, &a.mfd_stamp, ntm)))
       return LEMGPU_ECUDA;
     CU(ctx, cudaMemset(a.mfd_stamp, 0, ntm * sizeof(uint32_t)));
     CU(ctx, cudaMemset(a.mfd_A, 0, N * sizeof(double)));
