@@ -177,7 +177,8 @@ struct Ctl {
   uint32_t mfd_cnt[3], mfd_nlev;         // k_mfd_levels: per-level append counters, MFD plan levels
   uint32_t mfd_pass, mfd_wl_n[2];        // k_mfd_tiles: pass id (monotonic), queued tiles per pass parity
   uint32_t mfd_passes;                   // ... passes of this step
-  uint32_t mfd_g, mfd_done;              // ... grid of the next pass, cells finalised in the running pass
+  uint32_t mfd_done;                     // ... cells finalised in the running pass / round
+  uint32_t mfd_tail_n[2], mfd_tail_cur;  // k_mfd_tail: listed cells per list, the list being read
   unsigned long long t_mfd_begin;        // ... first pass start (the step's device time starts there)
   unsigned long long fr_t[3];            // ... latest end over the CTAs of the counts, F and erosion sweeps
   unsigned long long t_k1_begin, t_k1_end, t_order_end, t_phys_end;

@@ -18,13 +18,15 @@
 // are final), level by level in shared memory.  A cell stays unfinished while
 // a donor in another tile is unfinished; unfinished cells hold a NaN
 // sentinel in the global A, so a donor's 8-byte value is either its final
-// value or the sentinel.  Pass 0 runs every tile and reads no other tile;
-// each further pass runs the tiles (of a grid shifted by half a tile on
-// alternate passes, so chains that zig-zag along a tile edge land inside one
-// tile) that hold unfinished cells, reading the first ring from the global A.
-// Every pass finalises at least the highest unfinished cell; the passes
-// repeat (graph WHILE node) until none is left.  Each cell is evaluated once,
-// from final donors: A is exactly the reference's accumulation.
+// value or the sentinel.  Pass 0 runs every tile, reads no other tile and
+// stores the lower masks and weight sums; pass 1 runs the tiles of a grid
+// shifted by half a tile (chains that zig-zag along a pass-0 tile edge land
+// inside one tile) that hold unfinished cells, reading the first ring from
+// the global A, and lists the cells still unfinished (~1 % of a random-noise
+// DEM).  Those are finished by k_mfd_tail rounds (graph WHILE node): a listed
+// cell whose donors are all final is evaluated, the others are listed again,
+// until the list is empty.  Each cell is evaluated once, from final donors: A
+// is exactly the reference's accumulation.
 //
 // The MFD plan itself (generate_mfd_order) is needed only by the export
 // (lemgpu_download_mfd), which rebuilds it with k_mfd_graph + k_mfd_levels
@@ -73,7 +75,7 @@ __device__ __forceinline__ bool m_in_tile(int q) {
 }
 __device__ __forceinline__ bool m_unset(double v) { return (unsigned long long)__double_as_longlong(v) == kMfdUnset; }
 
-// One pass over the queued tiles (a.mfd_all: pass 0 of the step, every tile of grid 0).
+// Pass 0 (a.mfd_all: every tile of grid 0) or pass 1 (the queued tiles of grid 1).
 __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
   extern __shared__ __align__(16) unsigned char mraw[];
   MfdTileSmem& s = *reinterpret_cast<MfdTileSmem*>(mraw);
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
   if (tid == 0) {
     if (all) atomicMin(&ctl->t_mfd_begin, globaltimer());
     const uint32_t P = ld_volatile_u32(&ctl->mfd_pass);
-    const uint32_t g = all ? 0u : ld_volatile_u32(&ctl->mfd_g);
+    const uint32_t g = all ? 0u : 1u;
     s.pass = P;
     s.g = g;
     s.n = ld_volatile_u32(&ctl->err_flag) ? 0u
@@ -126,6 +128,16 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
     if (tid == 0) s.mark = 0;
     if (__syncthreads_count(unf != 0) == 0) continue;  // every cell of this tile is final
     // ---- compute_mfd for the tile and its first ring: lower mask, weight sum
+    // (pass 1: as pass 0 stored them)
+    if (!all) {
+      for (int i = (int)tid; i < kMN; i += kMTPB) {
+        const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
+        const bool in = x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1 && gx >= 0 && gx < W && gy >= 0 && gy < Ht;
+        const size_t g0 = (size_t)gy * a.W + gx;
+        s.lm[i] = in ? __ldcg(a.mfd_lm + g0) : (uint8_t)0;
+        s.ws[i] = in ? __ldcg(a.mfd_wsum + g0) : 0.0;
+      }
+    } else
     for (int i = (int)tid; i < kMN; i += kMTPB) {
       const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
       uint32_t m = 0;
@@ -146,6 +158,11 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       }
       s.lm[i] = (uint8_t)m;
       s.ws[i] = wsum;
+      if (m_in_tile(i) && gx >= 0 && gx < W && gy >= 0 && gy < Ht) {  // for pass 1 and the tail rounds
+        const size_t g0 = (size_t)gy * a.W + gx;
+        __stcg(a.mfd_lm + g0, (uint8_t)m);
+        __stcg(a.mfd_wsum + g0, wsum);
+      }
     }
     __syncthreads();
     // ---- unfinished tile cells: count their unfinished donors; level 0 = none
@@ -211,9 +228,13 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       const int q = (y + 2) * kMP + x + 2;
       const double v = s.A[q];
       if (m_unset(v)) {
-        const int ix = (gx + nsx) / kMX - (x0 + nsx) / kMX, iy = (gy + nsy) / kMY - (y0 + nsy) / kMY;
-        atomicOr(&s.mark, 1u << (iy * 2 + ix));
-        if (all) __stcg(a.mfd_A + (size_t)gy * a.W + gx, v);
+        if (all) {  // pass 0: the pass-1 tile holding the cell is queued
+          const int ix = (gx + nsx) / kMX - (x0 + nsx) / kMX, iy = (gy + nsy) / kMY - (y0 + nsy) / kMY;
+          atomicOr(&s.mark, 1u << (iy * 2 + ix));
+          __stcg(a.mfd_A + (size_t)gy * a.W + gx, v);
+        } else {  // pass 1: listed for the tail rounds
+          a.mfd_ord[atomicAdd(&ctl->mfd_tail_n[0], 1u)] = (uint32_t)gy * a.W + (uint32_t)gx;
+        }
       } else {
         __stcg(a.mfd_A + (size_t)gy * a.W + gx, v);
       }
@@ -230,18 +251,92 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
     }
   }
   if (tid == 0 && done) atomicAdd(&ctl->mfd_done, done);
-  // ---- the last CTA closes the pass: the next pass (other grid) runs if it has work
+  // ---- the last CTA closes the pass; after pass 1 the tail rounds run if
+  // cells are left (list 0)
   if (last_block_done(ctl) && tid == 0) {
-    const uint32_t nn = ld_volatile_u32(&ctl->mfd_wl_n[(P + 1u) & 1u]);
-    const uint32_t fin = ld_volatile_u32(&ctl->mfd_done);
     ctl->mfd_done = 0;
     ctl->mfd_wl_n[P & 1u] = 0;
     ctl->mfd_pass = P + 1u;
-    ctl->mfd_g = (uint32_t)(g ^ 1);
+    ctl->mfd_passes += 1u;
+    if (!all) {
+      ctl->mfd_tail_cur = 0;
+      set_cond(a, 3, ld_volatile_u32(&ctl->mfd_tail_n[0]) ? 1u : 0u);
+    }
+  }
+}
+
+// One tail round: every listed cell whose donors are all final is evaluated
+// (add_mfd_donor_flow, mfd.hpp:66-73); the others are listed for the next
+// round.  A donor finalised by another thread during the round may or may not
+// be seen: either way a cell is only evaluated from final donors.
+__global__ void __launch_bounds__(kTPB) k_mfd_tail(StepArgs a) {
+  Ctl* ctl = a.ctl;
+  const uint32_t cur = ld_volatile_u32(&ctl->mfd_tail_cur), nxt = cur ^ 1u;
+  const uint32_t n = ld_volatile_u32(&ctl->err_flag) ? 0u : ld_volatile_u32(&ctl->mfd_tail_n[cur]);
+  const uint32_t* lst = cur ? a.mfd_lev : a.mfd_ord;
+  uint32_t* lnx = cur ? a.mfd_ord : a.mfd_lev;
+  const uint32_t lane = threadIdx.x & 31u;
+  const int W = (int)a.W;
+  uint32_t done = 0;
+  for (uint32_t i0 = blockIdx.x * kTPB; i0 < n; i0 += gridDim.x * kTPB) {  // warp-uniform trip count
+    const uint32_t i = i0 + threadIdx.x;
+    bool left = false;
+    if (i < n) {
+      const uint32_t c = __ldcg(lst + i);
+      const uint32_t y = c / a.W, x = c - y * a.W;
+      const double hc = __ldg(a.h + c);
+      double tk[8];
+      uint32_t dm = 0;
+      bool ready = true;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        tk[k] = 0.0;
+        const uint32_t nx = x + dir_ox(k), ny = y + dir_oy(k);
+        if (!dir_in(a.conn, k) || nx >= a.W || ny >= a.Htot) continue;
+        const uint32_t nb = (uint32_t)((int)c + dir_ox(k) + dir_oy(k) * W);
+        if (!((__ldcg(a.mfd_lm + nb) >> (7 - k)) & 1u)) continue;
+        const double An = __ldcg(a.mfd_A + nb);
+        if (m_unset(An)) {
+          ready = false;
+          continue;
+        }
+        dm |= 1u << k;
+        const double w = mfd_weight(a, mfd_slope(a, __ldg(a.h + nb), hc, 7 - k));
+        tk[k] = __dmul_rn(__ddiv_rn(w, __ldcg(a.mfd_wsum + nb)), An);
+      }
+      if (ready) {
+        double acc = a.w0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if ((dm >> k) & 1u) acc = __dadd_rn(acc, tk[k]);
+        __stcg(a.mfd_A + c, acc);
+        ++done;
+      } else {
+        left = true;
+      }
+      if (left) {
+        const uint32_t b = __activemask(), bl = __ballot_sync(b, true);  // lanes still unfinished
+        const int ld = __ffs(bl) - 1;
+        uint32_t p = 0;
+        if ((int)lane == ld) p = atomicAdd(&ctl->mfd_tail_n[nxt], (uint32_t)__popc(bl));
+        p = __shfl_sync(bl, p, ld);
+        lnx[p + __popc(bl & ((1u << lane) - 1u))] = c;
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) done += __shfl_xor_sync(0xffffffffu, done, o);
+  if (lane == 0 && done) atomicAdd(&ctl->mfd_done, done);
+  if (last_block_done(ctl) && threadIdx.x == 0) {
+    const uint32_t nn = ld_volatile_u32(&ctl->mfd_tail_n[nxt]);
+    const uint32_t fin = ld_volatile_u32(&ctl->mfd_done);
+    ctl->mfd_done = 0;
+    ctl->mfd_tail_n[cur] = 0;
+    ctl->mfd_tail_cur = nxt;
     ctl->mfd_passes += 1u;
     bool more = nn != 0;
-    if (more && fin == 0 && nitems) {  // no progress: a cycle (impossible with strict descent), reported
+    if (more && fin == 0 && n) {  // no progress: a cycle (impossible with strict descent), reported
       more = false;
+      ctl->mfd_tail_n[nxt] = 0;
       ctl->err_flag = LEMGPU_ESTRUCTURE;
       ctl->err_cell = 0;
       ctl->err_slot = ctl->slot;

@@ -455,8 +455,9 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
     a.mfd_all = 0;
     if ((rc = add_kernel(ctx, g, &prev, (const void*)k_mfd_tiles, dim3(ctx->mfd_tiles_grid), dim3(kMTPB),
                          kMfdTileSmemBytes, &a0, nullptr)) ||
-        (rc = add_while(ctx, g, &prev, a.h_mfd, (const void*)k_mfd_tiles, dim3(ctx->mfd_tiles_grid),
-                        kMfdTileSmemBytes, &a)))
+        (rc = add_kernel(ctx, g, &prev, (const void*)k_mfd_tiles, dim3(ctx->mfd_tiles_grid), dim3(kMTPB),
+                         kMfdTileSmemBytes, &a, nullptr)) ||
+        (rc = add_while(ctx, g, &prev, a.h_mfd, (const void*)k_mfd_tail, dim3(ctx->scan_grid), 0, &a)))
       return rc;
   }
   if (ctx->use_tiles && ctx->pipe > 1 && !a.mfd_A) {
@@ -949,13 +950,14 @@ int enqueue_step_eager(lemgpu_ctx* ctx, uint32_t p) {
     a0.mfd_all = 1;
     a.mfd_all = 0;
     k_mfd_tiles<<<ctx->mfd_tiles_grid, kMTPB, kMfdTileSmemBytes, st>>>(a0);
+    k_mfd_tiles<<<ctx->mfd_tiles_grid, kMTPB, kMfdTileSmemBytes, st>>>(a);
     unsigned cond[4];
     const char* cbase = reinterpret_cast<const char*>(a.ctl) + offsetof(Ctl, cond);
     for (;;) {
       CU(ctx, cudaMemcpyAsync(cond, cbase, sizeof cond, cudaMemcpyDeviceToHost, st));
       CU(ctx, cudaStreamSynchronize(st));
       if (!cond[3]) break;
-      k_mfd_tiles<<<ctx->mfd_tiles_grid, kMTPB, kMfdTileSmemBytes, st>>>(a);
+      k_mfd_tail<<<ctx->scan_grid, kTPB, 0, st>>>(a);
     }
   }
   if (ctx->use_tiles) {
