@@ -38,12 +38,18 @@
 
 namespace lemgpu {
 
-constexpr int kMX = 64, kMY = 32;       // tile
+#ifndef LEMGPU_MFD_TY
+#define LEMGPU_MFD_TY 32
+#endif
+#ifndef LEMGPU_MFD_TPB
+#define LEMGPU_MFD_TPB 256
+#endif
+constexpr int kMX = 64, kMY = LEMGPU_MFD_TY;  // tile
 constexpr int kMP = kMX + 4;            // window pitch: the tile and two rings
 constexpr int kMWY = kMY + 4;           // window rows
 constexpr int kMN = kMP * kMWY;         // window cells
 constexpr int kMT = kMX * kMY;          // tile cells
-constexpr int kMTPB = 256;
+constexpr int kMTPB = LEMGPU_MFD_TPB;
 constexpr unsigned long long kMfdUnset = 0x7FF4DEAD00000000ull;  // NaN payload: not final yet
 
 // Tiles of grid g (0: origin (0, 0); 1: shifted by (-kMX/2, -kMY/2)).

@@ -140,7 +140,9 @@ __device__ __forceinline__ double dbg_area(T v, double w0) {
     return (double)v;
 }
 
-template <int CONN, int NK, bool EX>
+// MF (routing = kMfd, with EX's layout): the erosion reads the MFD drainage
+// area from global memory (final before this kernel: k_mfd_tiles); no counts.
+template <int CONN, int NK, bool EX, bool MF = false>
 __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char smraw[];
   TileSmem<EX>& s = *reinterpret_cast<TileSmem<EX>*>(smraw);
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   const uint32_t ntx = (a.W + kTX - 1) / kTX, nty = (a.Htot + kTY - 1) / kTY;
   const uint32_t ntiles = ntx * nty;
   const uint32_t E = a.lut_entries;
-  const bool tab = EX && NK == 1 && a.tab_ok;
+  const bool tab = EX && NK == 1 && a.tab_ok && !MF;
   if (tid == 0) {
     atomicMin(&ctl->t_t_begin, globaltimer());
     if (a.use_tma) mbar_init(&s.bar, 1);
@@ -487,7 +489,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     phclk_mark(s_pc, LEMGPU_PHASE_ORDER);  // staging + the levels
     if (EX) {
       // cell counts: every cell adds 1 to each ancestor (integer adds commute)
-      for (uint32_t i = (nl > 1 ? s.lvs[1] : 0u) + tid; i < (nl > 1 ? s.lvs[nl] : 0u); i += kTTPB) {
+      // (MF: the erosion reads the MFD drainage area, simulation.cpp:55-60)
+      for (uint32_t i = (nl > 1 && !MF ? s.lvs[1] : 0u) + tid; i < (nl > 1 && !MF ? s.lvs[nl] : 0u); i += kTTPB) {
         uint32_t p = s.list[i], code = RC(p);
         do {
           p = (uint32_t)((int)p + woff(code));
@@ -495,15 +498,6 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           code = RC(p);
         } while (code != kNoFlowCode);
       }
-      __syncthreads();
-    } else if (a.mfd_A) {
-      // routing = kMfd: the erosion reads the MFD drainage area (simulation.cpp:55-60),
-      // final before this kernel (k_mfd_tiles)
-      if constexpr (!EX)
-        for (uint32_t i = tid; i < (nl ? s.lvs[nl] : 0u); i += kTTPB) {
-          const uint32_t q = s.list[i];
-          ACC(q) = __ldg(a.mfd_A + gcell(q));
-        }
       __syncthreads();
     } else {
       // deepest level first: A = w + the children's A in slot order (the
@@ -589,7 +583,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       } else {
         double F;
         if (EX)
-          F = __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)ACC(q));
+          F = MF ? tile_F(a, mem, cls, __ldg(a.mfd_A + gcell(q)), misses)
+                 : __ldg(a.ftab + (mem * 3 + cls) * E + (uint32_t)ACC(q));
         else
           F = tile_F(a, mem, cls, (double)ACC(q), misses);
         if (NK == 1)
@@ -633,7 +628,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           const uint32_t q = s.list[i];
           if (ESC_GET(q)) continue;
           a.dbg_level[gcell(q)] = (uint8_t)l;
-          a.dbg_A[gcell(q)] = dbg_area<EX>(ACC(q), a.w0);
+          a.dbg_A[gcell(q)] = MF ? a.mfd_A[gcell(q)] : dbg_area<EX>(ACC(q), a.w0);
         }
     }
     phclk_mark(s_pc, LEMGPU_PHASE_EROSION);

@@ -402,13 +402,16 @@ StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
   return a;
 }
 
-template <int CONN, bool EX>
+template <int CONN, bool EX, bool MF = false>
 const void* tiles_fn_nk(int nk) {
-  return nk == 1 ? (const void*)k_tiles<CONN, 1, EX> : nk == 2 ? (const void*)k_tiles<CONN, 2, EX>
-                                                                : (const void*)k_tiles<CONN, 0, EX>;
+  return nk == 1 ? (const void*)k_tiles<CONN, 1, EX, MF> : nk == 2 ? (const void*)k_tiles<CONN, 2, EX, MF>
+                                                                    : (const void*)k_tiles<CONN, 0, EX, MF>;
 }
+// (routing = kMfd: the MF instantiation reads the MFD area from global
+// memory; the count layout serves for its escape marks whatever the cell area)
 const void* tiles_fn(const StepArgs& a) {
-  if (a.lut_exact && !a.mfd_A) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
+  if (a.mfd_A) return a.conn == 8 ? tiles_fn_nk<8, true, true>(a.nkind) : tiles_fn_nk<4, true, true>(a.nkind);
+  if (a.lut_exact) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
   return a.conn == 8 ? tiles_fn_nk<8, false>(a.nkind) : tiles_fn_nk<4, false>(a.nkind);
 }
 // the tile path's receiver pass (k_recv): division-free selection for D8 with unit cardinal spacing
@@ -420,7 +423,7 @@ const void* forest_fn(int nk) {
   return nk == 1 ? (const void*)k_esc_forest<1> : nk == 2 ? (const void*)k_esc_forest<2> : (const void*)k_esc_forest<0>;
 }
 size_t tiles_smem(const StepArgs& a) {
-  return a.lut_exact && !a.mfd_A ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>();
+  return a.lut_exact || a.mfd_A ? tiles_smem_bytes<true>() : tiles_smem_bytes<false>();
 }
 
 // The step graph that reads hbuf[p]; with_stats: ending with the ensemble
@@ -763,7 +766,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
     if (o.tile_grid) tg = o.tile_grid;  // testing: few CTAs, many tiles each
     if (tg < 1) tg = 1;
     ctx->tile_grid = (int)(tg < ntiles ? tg : ntiles);
-    // MFD routing runs the FP-area instantiation (the MFD area is not a cell count)
+    // MFD routing: the instantiation may differ (tiles_fn)
     StepArgs am = a;
     am.mfd_A = reinterpret_cast<double*>(16);  // only selects the instantiation
     const void* fm = tiles_fn(am);

@@ -8,7 +8,7 @@ for n in [int(x) for x in (sys.argv[1:] or ["1000", "4000", "10000"])]:
     ctx = lem.DeviceContext(n, n, lem.SimParams(), 8)
     ctx.generate_terrain([42])
     ctx.set_routing(lem.Routing.kMfd, 1.0)
-    for s in range(6):
+    for s in range(int(__import__("os").environ.get("PROBE_STEPS", "6"))):
         t = time.time()
         d = ctx.step(1)[0]
         dt = time.time() - t
