@@ -47,9 +47,10 @@ B_STEP = 87
 B_RECV = 17
 B_TILES = 70
 B_TILES_MIN = 18
-# MFD routing (not in SURVEY 8(d); same counting rule): graph 17 (read h 8, write lower mask 1 + weight
-# sum 8) + plan 9 (read mask 1, write order 4 + level 4) + accumulation 37 (read order 4, h 8, mask 1,
-# donors' weight sums 8 and A 8, write A 8) = 63 B/cell on top of the D8 step's 87
+# MFD routing (not in SURVEY 8(d); same counting rule, the reference's MFD work): graph 17 (read h 8,
+# write lower mask 1 + weight sum 8) + plan 9 (read mask 1, write order 4 + level 4) + accumulation 37
+# (read order 4, h 8, mask 1, donors' weight sums 8 and A 8, write A 8) = 63 B/cell on top of the D8
+# step's 87 (the device builds no plan in the step: k_mfd_tiles finishes cells in dependency order)
 B_MFD = 63
 WORKLOADS = {
     "dem10000": dict(w=10000, h=10000, members=1, n_exp=1.0,
@@ -426,10 +427,13 @@ def main():
     # the cells each finishes.  The dominant one is the longest.
     cands = []
     if wl.get("routing"):
-        # MFD routing: the global level path (D8 plan, physics fed the MFD area)
-        # after the MFD kernels; their spans are not stamped separately: the step
-        cands.append(("step: k_mfd_graph + k_mfd_levels + global level path", step_ms_ev,
-                      (B_STEP + B_MFD) * cells, ()))
+        # MFD routing: the MFD area (k_mfd_tiles pass 0 + pass 1, k_mfd_tail rounds)
+        # runs first, then the D8 tile path reads it; the MFD kernels' span is the
+        # step minus the D8 kernels' spans
+        mfd_ms = max(step_ms_ev - k1_ms - tiles_ms - esc_ord_ms - esc_phys_ms, 1e-9)
+        cands.append(("k_mfd_tiles + k_mfd_tail (MFD area)", mfd_ms, B_MFD * cells, ("k_mfd_tiles", "k_mfd_tail")))
+        cands.append(("k_tiles", tiles_ms, B_TILES * tile_cells, ("k_tiles",)))
+        cands.append(("k_recv", k1_ms, B_RECV * cells, ("k_recv",)))
     elif pipelined:
         # tall rasters: k_recv and k_tiles run in interleaved bands (receiver band
         # b+1 beside tile band b): one unit, the step minus the escape kernels
@@ -440,8 +444,6 @@ def main():
         cands.append(("k_recv", k1_ms, B_RECV * cells, ("k_recv",)))
     cands.append(("escape path (k_esc_small | k_esc_bfs + k_chunks/k_deep_coop)", esc_ord_ms + esc_phys_ms,
                   B_TILES * esc_cells, ("k_esc_small", "k_esc_bfs", "k_chunks", "k_deep_coop")))
-    if wl.get("routing"):
-        cands = cands[:1]
     dom, dom_ms, dom_bytes, dom_kernels = max(cands, key=lambda c: c[1])
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     traffic = None
@@ -505,6 +507,9 @@ def main():
                    "lut_misses_last_step": last.lut_misses if last else None,
                    "escaped_trees_last_step": last.escaped_trees if last else None,
                    "newton_iters_last_step": last.newton_iters if last else None,
+                   **({"mfd_passes_last_step": last.mfd_passes if last else None,
+                       "mfd_path": "k_mfd_tiles pass 0 + pass 1 (shifted grid) + k_mfd_tail rounds, then the D8 "
+                                   "tile path reading the MFD area"} if wl.get("routing") else {}),
                    **({"fill": "lem::priority_flood_fill epsilon_ascending 1e-8 on the device (lemgpu_fill), once, "
                                "untimed", "fill_ms": fill_ms} if fill_ms is not None else {})},
         "clocks": clk.summary(),
