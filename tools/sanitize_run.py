@@ -43,6 +43,10 @@ CASES = [
     ("forest-ramp", {}, {}, "ramp", 200, 150),
     ("mfd", {}, {}, "noise", 130, 97),
     ("mfd-eager-e13", {"eager": 1}, {}, "noise", 100, 80),
+    ("mfd-escape", {"force_escape": 1}, {}, "noise", 130, 97),
+    ("mfd-escape-coop", {"force_escape": 2, "no_esc_small": 1}, {}, "noise", 100, 80),
+    ("mfd-ramp", {}, {}, "ramp", 200, 150),
+    ("mfd-levels", {"mfd_levels": 1}, {}, "noise", 100, 80),
 ]
 only = sys.argv[1:] or None
 if only == ["list"]:
@@ -51,6 +55,8 @@ if only == ["list"]:
 for name, opts, kw, terrain, w, h in CASES:
     if only and name not in only:
         continue
+    if __import__("os").environ.get("SAN_EAGER"):  # racecheck: eager launches (see profiles/sanitizer_r02)
+        opts = dict(opts, eager=1)
     ctx = lem.DeviceContext(w, h, lem.SimParams(**kw), 8, options=opts)
     mfd = name.startswith("mfd")
     ex = 1.3 if name.endswith("e13") else 1.0
@@ -62,7 +68,10 @@ for name, opts, kw, terrain, w, h in CASES:
     for s in range(2):
         d = ctx.step(1)[0]
         if mfd:
-            ora.step_mfd(e, exponent=ex, params=p)
+            o = ora.step_mfd(e, exponent=ex, params=p)
+            m = ctx.download_mfd()  # the area of the step and the plan rebuilt for the export
+            assert np.array_equal(m["A"].view(np.uint64), o["A"].view(np.uint64)), f"{name}: MFD area differs"
+            assert np.array_equal(m["order"], o["mfd_order"]), f"{name}: MFD plan differs"
         else:
             ora.step(e, params=p, want_donor=False)
         ok = np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
