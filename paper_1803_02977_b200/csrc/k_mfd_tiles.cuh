@@ -194,20 +194,25 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       for (uint32_t i = qs + tid; i < qe; i += kMTPB) {
         const int q = s.list[i];
         const double hc = s.h[q];
-        // the donors' terms first (independent), then their sum in slot order
-        // (ascending index = stencil order)
+        // the donors' terms first, then their sum in slot order (ascending
+        // index = stencil order).  All eight directions are evaluated without
+        // branches (a non-donor gets harmless operands and is masked out of the
+        // sum): the lanes of a warp stay converged and the eight division
+        // chains overlap.
         double tk[8];
         uint32_t dm = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int n = q + mwoff(k);
-          tk[k] = 0.0;
-          if (dir_in(a.conn, k) && ((s.lm[n] >> (7 - k)) & 1u)) {
-            dm |= 1u << k;
-            // n's weight towards q: its slope in direction 7-k (same length as k)
-            const double w = mfd_weight(a, mfd_slope(a, s.h[n], hc, 7 - k));
-            tk[k] = __dmul_rn(__ddiv_rn(w, s.ws[n]), s.A[n]);
-          }
+          const bool don = dir_in(a.conn, k) && ((s.lm[n] >> (7 - k)) & 1u);
+          dm |= don ? 1u << k : 0u;
+          // n's weight towards q: its slope in direction 7-k (same length as k)
+          const double d = don ? __dsub_rn(s.h[n], hc) : 1.0;
+          const double sl = ((a.dist_one >> k) & 1u) ? d
+                            : ((a.dist_recip >> k) & 1u) ? div_rn_recip(d, a.dist[k], a.rdist[k])
+                                                         : __ddiv_rn(d, a.dist[k]);
+          const double w = mfd_weight(a, sl);
+          tk[k] = __dmul_rn(__ddiv_rn(w, don ? s.ws[n] : 1.0), don ? s.A[n] : 0.0);
         }
         double acc = a.w0;
 #pragma unroll
