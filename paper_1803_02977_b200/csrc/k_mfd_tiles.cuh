@@ -21,7 +21,7 @@
 // value or the sentinel.  Pass 0 runs every tile, reads no other tile and
 // stores the lower masks and weight sums; pass 1 runs the tiles of a grid
 // shifted by half a tile (chains that zig-zag along a pass-0 tile edge land
-// inside one tile) that hold unfinished cells, reading the first ring from
+// inside one tile) that hold unfinished cells, reading the ring from
 // the global A, and lists the cells still unfinished (~1 % of a random-noise
 // DEM).  Those are finished by k_mfd_tail rounds (graph WHILE node): a listed
 // cell whose donors are all final is evaluated, the others are listed again,
@@ -39,14 +39,14 @@
 namespace lemgpu {
 
 #ifndef LEMGPU_MFD_TY
-#define LEMGPU_MFD_TY 32
+#define LEMGPU_MFD_TY 28  // 64x28: 55 KB of shared memory, 4 CTAs per SM (measured best of 16/24/28/32/48/64)
 #endif
 #ifndef LEMGPU_MFD_TPB
 #define LEMGPU_MFD_TPB 256
 #endif
 constexpr int kMX = 64, kMY = LEMGPU_MFD_TY;  // tile
-constexpr int kMP = kMX + 4;            // window pitch: the tile and two rings
-constexpr int kMWY = kMY + 4;           // window rows
+constexpr int kMP = kMX + 2;            // window pitch: the tile and one ring
+constexpr int kMWY = kMY + 2;           // window rows
 constexpr int kMN = kMP * kMWY;         // window cells
 constexpr int kMT = kMX * kMY;          // tile cells
 constexpr int kMTPB = LEMGPU_MFD_TPB;
@@ -63,11 +63,12 @@ __host__ __device__ __forceinline__ uint32_t mfd_cap(uint32_t W, uint32_t H) {
 
 struct MfdTileSmem {
   double h[kMN];        // window elevations (0 off the raster: never read for an existing neighbour)
-  double ws[kMN];       // weight sums (tile + first ring; interior cells)
-  double A[kMN];        // drainage area (tile + first ring): final value or the kMfdUnset bits
-  uint32_t rem[kMT];    // unfinished donors of an unfinished tile cell
+  double ws[kMN];       // weight sums (tile; pass 1: and ring)
+  double A[kMN];        // drainage area: final value or the kMfdUnset bits
+  alignas(4) uint8_t rem[kMT];  // unfinished donors of an unfinished tile cell (byte countdowns, word atomics)
   uint16_t list[kMT];   // cells finalised in this visit, level-major
-  uint8_t lm[kMN];      // mask of strictly lower neighbours (0: boundary / off raster / outer ring)
+  uint8_t lm[kMN];      // mask of strictly lower neighbours (0: boundary / off raster); ring cells in
+                        // pass 0: only the bits towards the window
   uint32_t cnt[3];      // per-level append counters (rotating)
   uint32_t mark;        // next-grid tiles to queue: bit dy*2 + dx
   uint32_t pass, n, g;  // pass id, work items and grid of this pass
@@ -77,7 +78,7 @@ constexpr size_t kMfdTileSmemBytes = sizeof(MfdTileSmem);
 __device__ __forceinline__ int mwoff(int k) { return dir_ox(k) + dir_oy(k) * kMP; }
 __device__ __forceinline__ bool m_in_tile(int q) {
   const int y = q / kMP, x = q - y * kMP;
-  return (unsigned)(x - 2) < (unsigned)kMX && (unsigned)(y - 2) < (unsigned)kMY;
+  return (unsigned)(x - 1) < (unsigned)kMX && (unsigned)(y - 1) < (unsigned)kMY;
 }
 __device__ __forceinline__ bool m_unset(double v) { return (unsigned long long)__double_as_longlong(v) == kMfdUnset; }
 
@@ -114,9 +115,9 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
     const uint32_t t = all ? it : __ldcg(wl + it);
     const int tx = (int)(t % ntx), ty = (int)(t / ntx);
     const int x0 = tx * kMX - sx, y0 = ty * kMY - sy;  // first tile cell
-    const int wx0 = x0 - 2, wy0 = y0 - 2;
+    const int wx0 = x0 - 1, wy0 = y0 - 1;
     __syncthreads();  // the previous tile is done with shared memory
-    // ---- stage: window elevations; A of the tile and the first ring (pass 0:
+    // ---- stage: window elevations; A of the tile and the ring (pass 0:
     // nothing is final yet -- other tiles' values may be a previous step's)
     uint32_t unf = 0;
     for (int i = (int)tid; i < kMN; i += kMTPB) {
@@ -124,21 +125,21 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       const bool in = gx >= 0 && gx < W && gy >= 0 && gy < Ht;
       const size_t g0 = (size_t)gy * a.W + gx;
       s.h[i] = in ? __ldg(a.h + g0) : 0.0;
-      if (x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1) {
-        const double v = in && !all ? __ldcg(a.mfd_A + g0) : __longlong_as_double((long long)kMfdUnset);
-        s.A[i] = v;
-        unf += in && m_in_tile(i) && m_unset(v) ? 1u : 0u;
-      }
+      const double v = in && !all ? __ldcg(a.mfd_A + g0) : __longlong_as_double((long long)kMfdUnset);
+      s.A[i] = v;
+      unf += in && m_in_tile(i) && m_unset(v) ? 1u : 0u;
     }
     if (tid < 3) s.cnt[tid] = 0;
     if (tid == 0) s.mark = 0;
     if (__syncthreads_count(unf != 0) == 0) continue;  // every cell of this tile is final
-    // ---- compute_mfd for the tile and its first ring: lower mask, weight sum
-    // (pass 1: as pass 0 stored them)
+    // ---- compute_mfd for the tile: lower mask, weight sum; for a ring cell
+    // only its lower mask towards the window (pass 0 reads no other tile's
+    // values, so a ring donor only blocks its receivers).  Pass 1: the tile
+    // and the ring as pass 0 stored them.
     if (!all) {
       for (int i = (int)tid; i < kMN; i += kMTPB) {
         const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
-        const bool in = x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1 && gx >= 0 && gx < W && gy >= 0 && gy < Ht;
+        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < Ht;
         const size_t g0 = (size_t)gy * a.W + gx;
         s.lm[i] = in ? __ldcg(a.mfd_lm + g0) : (uint8_t)0;
         s.ws[i] = in ? __ldcg(a.mfd_wsum + g0) : 0.0;
@@ -148,16 +149,19 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
       const int y = i / kMP, x = i - y * kMP, gx = wx0 + x, gy = wy0 + y;
       uint32_t m = 0;
       double wsum = 0.0;
-      if (x >= 1 && x < kMP - 1 && y >= 1 && y < kMWY - 1 && gx > 0 && gx < W - 1 && gy > 0 && gy < Ht) {
+      const bool tc = m_in_tile(i);
+      if (gx > 0 && gx < W - 1 && gy > 0 && gy < Ht) {
         const uint32_t yl = (uint32_t)gy % a.H;
         if (yl > 0 && yl < a.H - 1) {  // interior (boundary cells have no receivers, mfd.cpp:43)
           const double hc = s.h[i];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (!dir_in(a.conn, k)) continue;
+            if (!tc && (unsigned)(x + dir_ox(k)) >= (unsigned)kMP) continue;  // ring cell: in-window bits only
+            if (!tc && (unsigned)(y + dir_oy(k)) >= (unsigned)kMWY) continue;
             const double hn = s.h[i + mwoff(k)];
             if (hn >= hc) continue;  // receivers must be strictly lower (mfd.cpp:48)
-            wsum = __dadd_rn(wsum, mfd_weight(a, mfd_slope(a, hc, hn, k)));
+            if (tc) wsum = __dadd_rn(wsum, mfd_weight(a, mfd_slope(a, hc, hn, k)));
             m |= 1u << k;
           }
         }
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
     __syncthreads();
     // ---- unfinished tile cells: count their unfinished donors; level 0 = none
     for (int j = (int)tid; j < kMT; j += kMTPB) {
-      const int q = (j / kMX + 2) * kMP + (j % kMX) + 2;
+      const int q = (j / kMX + 1) * kMP + (j % kMX) + 1;
       if (!m_unset(s.A[q]) || x0 + j % kMX >= W || y0 + j / kMX >= Ht || x0 + j % kMX < 0 || y0 + j / kMX < 0)
         continue;
       uint32_t r = 0;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
         const int n = q + mwoff(k);
         r += (((s.lm[n] >> (7 - k)) & 1u) && m_unset(s.A[n])) ? 1u : 0u;
       }
-      s.rem[j] = r;
+      s.rem[j] = (uint8_t)r;
       if (r == 0) s.list[atomicAdd(&s.cnt[0], 1u)] = (uint16_t)q;
     }
     __syncthreads();
@@ -222,8 +226,10 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
         for (uint32_t m = s.lm[q]; m; m &= m - 1) {
           const int r = q + mwoff(__ffs(m) - 1);
           if (!m_in_tile(r)) continue;
-          const int j = (r / kMP - 2) * kMX + (r % kMP) - 2;
-          if (atomicSub(&s.rem[j], 1u) == 1u) s.list[qe + atomicAdd(nc, 1u)] = (uint16_t)r;
+          const int j = (r / kMP - 1) * kMX + (r % kMP) - 1;
+          const uint32_t sh = 8u * (uint32_t)(j & 3);
+          if (((atomicSub(reinterpret_cast<uint32_t*>(s.rem) + (j >> 2), 1u << sh) >> sh) & 0xFFu) == 1u)
+            s.list[qe + atomicAdd(nc, 1u)] = (uint16_t)r;
         }
       }
       __syncthreads();
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kMTPB) k_mfd_tiles(StepArgs a) {
     for (int j = (int)tid; j < kMT; j += kMTPB) {
       const int y = j / kMX, x = j - y * kMX, gx = x0 + x, gy = y0 + y;
       if (gx < 0 || gx >= W || gy < 0 || gy >= Ht) continue;
-      const int q = (y + 2) * kMP + x + 2;
+      const int q = (y + 1) * kMP + x + 1;
       const double v = s.A[q];
       if (m_unset(v)) {
         if (all) {  // pass 0: the pass-1 tile holding the cell is queued
