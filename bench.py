@@ -442,13 +442,15 @@ def main():
     else:
         cands.append(("k_tiles", tiles_ms, B_TILES * tile_cells, ("k_tiles",)))
         cands.append(("k_recv", k1_ms, B_RECV * cells, ("k_recv",)))
-    cands.append(("escape path (k_esc_small | k_esc_bfs + k_chunks/k_deep_coop)", esc_ord_ms + esc_phys_ms,
-                  B_TILES * esc_cells, ("k_esc_small", "k_esc_bfs", "k_chunks", "k_deep_coop")))
+    cands.append(("escape path (k_esc_small | k_esc_forest | k_esc_bfs + k_chunks/k_deep_coop)",
+                  esc_ord_ms + esc_phys_ms, B_TILES * esc_cells,
+                  ("k_esc_small", "k_esc_forest", "k_esc_bfs", "k_chunks", "k_deep_coop")))
     dom, dom_ms, dom_bytes, dom_kernels = max(cands, key=lambda c: c[1])
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     traffic = None
-    if traffic_tbl and dom_kernels and all(k in traffic_tbl for k in dom_kernels[:2]):
-        traffic = sum(traffic_tbl[k]["dram_bytes_per_launch"] for k in dom_kernels if k in traffic_tbl)
+    if traffic_tbl and dom_kernels and all(k in traffic_tbl for k in dom_kernels[:1]):
+        traffic = sum(traffic_tbl[k].get("dram_bytes_per_step", traffic_tbl[k]["dram_bytes_per_launch"])
+                      for k in dom_kernels if k in traffic_tbl)
     per_gpu = value / world
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
