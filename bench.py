@@ -484,7 +484,10 @@ def main():
     # k_esc_small, k_esc_bfs (cooperative, every escape level inside),
     # k_chunks, k_deep_coop (cooperative), [k_stats_reduce], k_finalize --
     # the kernel nodes of the step graph (the NCCL all-reduce is a library kernel)
-    launches = args.steps * ctx.kernels_per_step()
+    # the step graph's unconditional kernel nodes, plus the MFD tail rounds
+    # (a WHILE node: mfd_passes - 2 per step); the escape kernels behind the IF
+    # node after k_esc_small run only when it could not finish the escaped trees
+    launches = args.steps * ctx.kernels_per_step() + sum(max(d.mfd_passes - 2, 0) for d in diags[-args.steps:])
     last = diags[-1] if diags else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -517,6 +520,8 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
+        "gpu_launches_note": "graph kernel nodes executed every step + MFD tail rounds; the escape kernels inside "
+                             "the IF node (k_esc_forest, k_esc_bfs, k_chunks, k_deep_coop) are not counted",
         "roofline": roofline,
         "cpu_baseline": cpu,
     }

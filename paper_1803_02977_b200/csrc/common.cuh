@@ -157,7 +157,7 @@ struct Ctl {
   uint32_t err_cell;  // failing cell (any failing cell is acceptable)
   uint32_t err_slot;  // diagnostics slot of the step that failed
   uint32_t slot;      // diagnostics slot of the running step
-  uint32_t cond[4];   // loop conditions when the step runs eagerly (no graph)
+  uint32_t cond[5];   // loop conditions when the step runs eagerly (no graph)
   // per step (reset by k_finalize)
   uint32_t lvl;          // level being expanded
   uint32_t done;         // finished CTAs of the running kernel
@@ -277,7 +277,8 @@ struct StepArgs {
   double* dbg_A;       // ... and its drainage area
   Ctl* ctl;
   lemgpu_diag* diag;  // ring of per-step diagnostics (slot = ctl->slot)
-  cudaGraphConditionalHandle h_expand, h_dacc, h_deros, h_mfd;
+  cudaGraphConditionalHandle h_expand, h_dacc, h_deros, h_mfd, h_esc;
+  int esc_if;  // 1: the escape kernels after k_esc_small sit in a graph IF node on h_esc
 };
 
 // ---------------------------------------------------------------- helpers
@@ -415,13 +416,14 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total,
 }
 
 // Loop condition of the step graph (0: level expansion, 1: deep
-// accumulation, 2: deep erosion, 3: MFD tile passes): a graph conditional when the step is a
+// accumulation, 2: deep erosion, 3: MFD tail rounds, 4: escape kernels after k_esc_small): a graph conditional when the step is a
 // CUDA graph, a control-block word when it runs eagerly (profiling).
 __device__ __forceinline__ void set_cond(const StepArgs& a, int which, unsigned v) {
   if (a.eager) {
     a.ctl->cond[which] = v;
   } else {
-    const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : which == 2 ? a.h_deros : a.h_mfd;
+    const cudaGraphConditionalHandle h = which == 0 ? a.h_expand : which == 1 ? a.h_dacc : which == 2 ? a.h_deros
+                                         : which == 3 ? a.h_mfd : a.h_esc;
     cudaGraphSetConditional(h, v);
   }
 }

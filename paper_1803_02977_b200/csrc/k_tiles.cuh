@@ -858,6 +858,8 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   if (s_last && tid == 0) {
     __threadfence();
     ctl->esc_done = 0;
+    // the cooperative escape kernels run only when a CTA's share did not fit
+    if (a.esc_if) set_cond(a, 4, ld_volatile_u32(&ctl->esc_fail) ? 1u : 0u);
     if (ld_volatile_u32(&ctl->esc_fail) == 0) {
       ctl->nlev = ld_volatile_u32(&ctl->esc_nlev);
       ctl->n0 = n;

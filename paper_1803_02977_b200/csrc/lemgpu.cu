@@ -439,6 +439,11 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
     CU(ctx, cudaGraphConditionalHandleCreate(&a.h_dacc, g, 0, cudaGraphCondAssignDefault));
     CU(ctx, cudaGraphConditionalHandleCreate(&a.h_deros, g, 0, cudaGraphCondAssignDefault));
   }
+  // tile path with k_esc_small: the cooperative escape kernels behind an IF
+  // node that k_esc_small's last CTA clears when it finished every escaped tree
+  // (their launches are most of a small raster's step)
+  a.esc_if = ctx->use_tiles && ctx->esc_small ? 1 : 0;
+  if (a.esc_if) CU(ctx, cudaGraphConditionalHandleCreate(&a.h_esc, g, 1, cudaGraphCondAssignDefault));
   const int nk = a.nkind;
   const void* fdc = nk == 1 ? (const void*)k_deep_coop<1> : nk == 2 ? (const void*)k_deep_coop<2> : (const void*)k_deep_coop<0>;
   const void* fk1 = ctx->use_tiles ? recv_fn(a)
@@ -449,6 +454,32 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
   cudaGraphNode_t prev = nullptr;
   int rc;
   const dim3 g1((a.W + kBX - 1) / kBX, (a.Htot + kBY - 1) / kBY);
+  // the tile path's escape kernels after k_esc_small (in the IF node's body, or inline)
+  auto add_escape = [&](cudaGraph_t gg, cudaGraphNode_t* pv) -> int {
+    int r;
+    if ((a.esc_forest && (r = add_kernel(ctx, gg, pv, forest_fn(nk), dim3(ctx->forest_grid), dim3(kFTPB),
+                                         kForestSmemBytes, &a, nullptr, true))) ||
+        (r = add_kernel(ctx, gg, pv, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)) ||
+        (r = add_kernel(ctx, gg, pv, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
+        (r = add_kernel(ctx, gg, pv, fdc, dim3(ctx->deep_coop_grid), dim3(kDeepTPB), kDeepSmemBytes, &a, nullptr,
+                        true)))
+      return r;
+    return 0;
+  };
+  auto add_escape_path = [&]() -> int {
+    if (!a.esc_if) return add_escape(g, &prev);
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = a.h_esc;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t n;
+    CU(ctx, cudaGraphAddNode(&n, g, prev ? &prev : nullptr, prev ? 1 : 0, &cp));
+    cudaGraphNode_t inner = nullptr;
+    const int r = add_escape(cp.conditional.phGraph_out[0], &inner);
+    prev = n;
+    return r;
+  };
   if (ctx->use_tiles && a.mfd_A) {
     // routing = kMfd: the MFD drainage area first (pass 0 over every tile,
     // then the queued tiles until a pass queues none), then the D8 tile path
@@ -504,9 +535,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
     prev = join;
     if ((ctx->esc_small &&
          (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
-        (a.esc_forest && (rc = add_kernel(ctx, g, &prev, forest_fn(nk), dim3(ctx->forest_grid), dim3(kFTPB),
-                                          kForestSmemBytes, &a, nullptr, true))) ||
-        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
+        (rc = add_escape_path()))
       return rc;
   } else if (ctx->use_tiles) {
     if ((rc = add_kernel(ctx, g, &prev, fk1, g1, dim3(kTPB), 0, &a, &ctx->hmap[p])) ||
@@ -515,9 +544,7 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
                          &ctx->tmap[p])) ||
         (ctx->esc_small &&
          (rc = add_kernel(ctx, g, &prev, fes, dim3(ctx->esc_small_grid), dim3(kTPB), kEscSmallSmemBytes, &a, nullptr))) ||
-        (a.esc_forest && (rc = add_kernel(ctx, g, &prev, forest_fn(nk), dim3(ctx->forest_grid), dim3(kFTPB),
-                                          kForestSmemBytes, &a, nullptr, true))) ||
-        (rc = add_kernel(ctx, g, &prev, (const void*)k_esc_bfs, dim3(a.scan_grid), dim3(kTPB), 0, &a, nullptr, true)))
+        (rc = add_escape_path()))
       return rc;
   } else {
     if ((a.mfd_A &&  // routing = kMfd: the MFD graph, plan and drainage area first (they read only h)
@@ -530,10 +557,8 @@ int build_graph(lemgpu_ctx* ctx, uint32_t p, bool with_stats = false) {
       return rc;
   }
   if ((!ctx->use_tiles && (rc = add_while(ctx, g, &prev, a.h_expand, (const void*)k_expand, dim3(a.scan_grid), 0, &a))) ||
-      (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr)) ||
-      (ctx->use_tiles &&
-       (rc = add_kernel(ctx, g, &prev, fdc, dim3(ctx->deep_coop_grid), dim3(kDeepTPB), kDeepSmemBytes, &a, nullptr,
-                        true))) ||
+      (!ctx->use_tiles &&
+       (rc = add_kernel(ctx, g, &prev, fch, dim3(ctx->chunk_grid), dim3(kChunkTPB), kChunksSmemBytes, &a, nullptr))) ||
       (!ctx->use_tiles &&
        ((rc = add_kernel(ctx, g, &prev, (const void*)k_deep_prep, dim3(ctx->deep_grid), dim3(kTPB), 0, &a, nullptr)) ||
         (rc = add_while(ctx, g, &prev, a.h_dacc, (const void*)k_deep_accum, dim3(ctx->deep_grid), 0, &a)) ||

@@ -1,2 +1,5 @@
-timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "mfd" -p no:cacheprovider 2>&1 | tail -2
-PROBE_STEPS=3 timeout -s KILL 300 python tools/mfd_probe.py 1000 10000
+timeout -s KILL 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -2
+for wl in dem1000 dem10000 dem1000fill; do for i in 1 2; do for so in tools/var_base.so tools/var_new.so; do
+  LEMGPU_LIB=$so timeout -s KILL 200 python bench.py --workload $wl --no-cpu-baseline --e2e-steps 0 --steps 30 2>/dev/null \
+    | python -c "import json,sys; d=json.load(sys.stdin); print('$wl $so', round(d['ms_per_step'],4), d['gpu_launches'])"
+done; done; done
