@@ -695,8 +695,9 @@ constexpr int kEscSmallRoots = 1024;
 constexpr int kEscSmallCap = 6144;
 constexpr int kEscSmallLev = 64;  // deeper shares fail early (deep plans belong to the cooperative path)
 struct EscSmallSmem {
-  double h[kEscSmallCap];
-  double A[kEscSmallCap];
+  double h[kEscSmallCap];  // the step's input elevation (staged at discovery), then the new one
+  double A[kEscSmallCap];  // drainage area, then F
+  double y[kEscSmallCap];  // n = 1: RN(1 / RN(1 + F)) for newton_n1_tab
   uint32_t cell[kEscSmallCap];
   uint16_t par[kEscSmallCap];  // parent slot (roots: 0xFFFF)
   uint16_t fc[kEscSmallCap];   // first child slot
@@ -723,8 +724,11 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
   uint32_t nl = 0;
   if (ok && nr > 0) {
     for (uint32_t i = tid; i < nr; i += kTPB) {
-      s.cell[i] = a.order[r0 + i];
+      const uint32_t c = a.order[r0 + i];
+      s.cell[i] = c;
       s.par[i] = 0xFFFFu;
+      // the elevation the step reads, copied asynchronously (consumed by the erosion)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&s.h[i])), "l"(a.h + c) : "memory");
     }
     if (tid == 0) {
       s.lvl[0] = 0;
@@ -754,9 +758,12 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
           while (m) {
             const uint32_t k = __ffs(m) - 1;
             m &= m - 1;
-            s.cell[c] = (uint32_t)((int)cell + dir_off(k, (int)a.W));
+            const uint32_t cc = (uint32_t)((int)cell + dir_off(k, (int)a.W));
+            s.cell[c] = cc;
             s.par[c] = (uint16_t)i;
             s.kd[c] = (uint8_t)k;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&s.h[c])), "l"(a.h + cc)
+                         : "memory");  // off every level's dependent chain
             ++c;
           }
         }
@@ -779,6 +786,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
       __syncthreads();
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // no copy in flight past here (a failed CTA exits)
   if (!ok) {
     if (tid == 0) atomicAdd(&ctl->esc_fail, 1u);
   } else if (nr > 0) {
@@ -795,22 +803,32 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
       __syncthreads();
     }
     phclk_mark(s_pc, LEMGPU_PHASE_ACCUM);
-    // uplift (level 0: interior sources only), erosion level by level
+    // F of every cell below level 0 at once (its table lookup or pow off the
+    // level chain), in place of the area
     uint32_t iters = 0, misses = 0;
+    for (uint32_t i = s.lvl[1 < nl ? 1 : 0] + tid; i < (nl > 1 ? s.lvl[nl] : 0u); i += kTPB) {
+      const uint32_t mem = a.M > 1 ? s.cell[i] / a.MN : 0u;
+      const double F = tile_F(a, mem, dir_class(s.kd[i]), s.A[i], misses);  // class symmetric in k <-> 7-k
+      s.A[i] = F;
+      if (NK == 1) s.y[i] = F < 0x1p500 ? __ddiv_rn(1.0, __dadd_rn(1.0, F)) : 0.0;  // 0: IEEE Newton
+    }
+    __syncthreads();  // (the staged elevations landed before the accumulation)
+    // uplift (level 0: interior sources only), erosion level by level, from shared memory
     for (uint32_t l = 0; l < nl; ++l) {
       for (uint32_t i = s.lvl[l] + tid; i < s.lvl[l + 1]; i += kTPB) {
         const uint32_t c = s.cell[i];
-        double hv = a.h[c];
+        double hv = s.h[i];
         if (l == 0) {
           if (is_interior(a, c)) hv = __dadd_rn(hv, a.du);
         } else {
           const double h0 = __dadd_rn(hv, a.du);
           const double hn = s.h[s.par[i]];
-          const uint32_t mem = a.M > 1 ? c / a.MN : 0u;
-          const double F = tile_F(a, mem, dir_class(s.kd[i]), s.A[i], misses);  // class symmetric in k <-> 7-k
+          const double F = s.A[i];
           int itn;
           bool okn;
-          if (NK == 1)
+          if (NK == 1 && s.y[i] != 0.0)
+            hv = newton_n1_tab(h0, hn, F, s.y[i], a.eps, a.maxit, itn, okn);
+          else if (NK == 1)
             hv = newton_n1(h0, hn, F, a.eps, a.maxit, itn, okn);
           else
             hv = newton_gen<NK>(h0, hn, F, a.n_exp, a.eps, a.maxit, a.pow_fma, itn, okn);
