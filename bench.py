@@ -453,9 +453,41 @@ def main():
             dt = float(t.item())
         if reg:
             lem._abi.lib().lemgpu_host_unregister(host.ctypes.data)
+        # the PCIe floor of that contract: the raster up and a raster down,
+        # concurrently on two streams, nothing else (pinned, same sizes)
+        floor_ms = None
+        try:
+            dev_in = torch.empty(cells, dtype=torch.float64, device=f"cuda:{local}")
+            dev_out = torch.empty(cells, dtype=torch.float64, device=f"cuda:{local}")
+            host_out = torch.empty(cells, dtype=torch.float64).pin_memory()
+            s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+            best = None
+            for _ in range(3):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                s_up.wait_event(e0)
+                s_dn.wait_event(e0)
+                with torch.cuda.stream(s_up):
+                    dev_in.copy_(host_t, non_blocking=True)
+                with torch.cuda.stream(s_dn):
+                    host_out.copy_(dev_out, non_blocking=True)
+                torch.cuda.current_stream().wait_stream(s_up)
+                torch.cuda.current_stream().wait_stream(s_dn)
+                e1.record()
+                e1.synchronize()
+                t = e0.elapsed_time(e1)
+                best = t if best is None else min(best, t)
+            floor_ms = best
+            del dev_in, dev_out, host_out
+        except RuntimeError:
+            pass
         del host, host_t
         e2e = {"value": total_cells * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": cells * 8,
                "d2h_bytes_per_step": cells * 8, "steps": args.e2e_steps,
+               "ms_per_step": dt / args.e2e_steps * 1e3,
+               "pcie_copy_floor_ms": floor_ms,
+               "frac_of_copy_floor": (floor_ms / (dt / args.e2e_steps * 1e3)) if floor_ms else None,
                "path": "lemgpu_step_host (strategy_step on a host raster: the whole raster H2D and D2H per call, "
                        "in bands overlapped with the step; escaped trees patched in)",
                "pinned": True, "host_alloc": "cudaHostAlloc (torch pin_memory)"}
