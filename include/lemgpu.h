@@ -133,7 +133,9 @@ typedef struct lemgpu_options {
                               escape), 1 always, -1 never (level path) */
   int32_t mfd_levels;      /* 1: routing = kMfd through the level-synchronous plan + accumulation and the
                               global level path (default: MFD area by tile passes, D8 part on the tile path) */
-  int32_t reserved[1];
+  int32_t phase_clocks;    /* 1: lemgpu_diag.seconds holds lem::Phase seconds (per-CTA phase clocks in the
+                              tile pass, ~1.5 % of a 10000^2 step); 0: the seconds are 0 (kernel_s still
+                              holds the kernel spans).  The C++ shim and the Python drop-in turn it on. */
 } lemgpu_options;
 
 typedef struct lemgpu_ctx lemgpu_ctx;

@@ -66,7 +66,7 @@ class lemgpu_options(C.Structure):
                                          "no_esc_small", "pipe", "pipe_unchained")] + \
                [(n, C.c_uint32) for n in ("tile_grid", "esc_grid", "esc_small_grid", "pipe_tile_grid", "lut_entries",
                                           "host_bands", "patch_cap")] + \
-               [("host_profile", C.c_int32), ("esc_forest", C.c_int32), ("mfd_levels", C.c_int32), ("reserved", C.c_int32 * 1)]
+               [("host_profile", C.c_int32), ("esc_forest", C.c_int32), ("mfd_levels", C.c_int32), ("phase_clocks", C.c_int32)]
 
 
 # Every symbol include/lemgpu.h declares, with its ctypes signature.

@@ -258,6 +258,7 @@ struct StepArgs {
   uint32_t st_member0;
   // k_esc_forest (k_forest.cuh): 0 off, 1 when >= 1/4 of the cells escape, 2 always (EX only)
   int esc_forest;
+  int phclk;         // lemgpu_options::phase_clocks: lem::Phase seconds (the tile pass's phase clocks)
   uint32_t* fbins;   // [owner CTA][depth] counts / cursors (the global path's levels array, N + 2)
   uint32_t cb_cap;   // entries of cbound (k_esc_forest: level starts)
   double* hx;        // position-major elevations (k_esc_forest)

@@ -142,14 +142,16 @@ __device__ __forceinline__ double dbg_area(T v, double w0) {
 
 // MF (routing = kMfd, with EX's layout): the erosion reads the MFD drainage
 // area from global memory (final before this kernel: k_mfd_tiles); no counts.
-template <int CONN, int NK, bool EX, bool MF = false>
+// PH: lem::Phase clocks (lemgpu_options::phase_clocks); their marks sit on the
+// barrier-separated critical paths (measured 1.4 % of a 10000^2 step).
+template <int CONN, int NK, bool EX, bool MF = false, bool PH = true>
 __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(StepArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char smraw[];
   TileSmem<EX>& s = *reinterpret_cast<TileSmem<EX>*>(smraw);
   __shared__ PhClk s_pc;
   Ctl* ctl = a.ctl;
   if (ld_volatile_u32(&ctl->err_flag)) return;  // an earlier step failed (uniform)
-  phclk_begin(s_pc);
+  if constexpr (PH) phclk_begin(s_pc);
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const int W = (int)a.W, Ht = (int)a.Htot;
   const uint32_t ntx = (a.W + kTX - 1) / kTX, nty = (a.Htot + kTY - 1) / kTY;
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       __syncthreads();
     }
     // ---- 6. drainage area
-    phclk_mark(s_pc, LEMGPU_PHASE_ORDER);  // staging + the levels
+    if constexpr (PH) phclk_mark(s_pc, LEMGPU_PHASE_ORDER);  // staging + the levels
     if (EX) {
       // cell counts: every cell adds 1 to each ancestor (integer adds commute)
       // (MF: the erosion reads the MFD drainage area, simulation.cpp:55-60)
@@ -523,7 +525,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         __syncthreads();
       }
     }
-    phclk_mark(s_pc, LEMGPU_PHASE_ACCUM);
+    if constexpr (PH) phclk_mark(s_pc, LEMGPU_PHASE_ACCUM);
     // ---- 7. level 0: uplift interior sources (never eroded)
     // escaped roots -> the global level path (level 0 of its queue)
     for (uint32_t i0 = 0; i0 < (nl ? s.lvs[1] : 0u); i0 += kTTPB) {
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
       }
     }
     __syncthreads();
-    phclk_mark(s_pc, LEMGPU_PHASE_UPLIFT);
+    if constexpr (PH) phclk_mark(s_pc, LEMGPU_PHASE_UPLIFT);
     // erosion, downstream -> upstream, with the receiver's updated elevation
     auto erode = [&](uint32_t i) -> bool {
       const uint32_t q = s.list[i];
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
           a.dbg_A[gcell(q)] = MF ? a.mfd_A[gcell(q)] : dbg_area<EX>(ACC(q), a.w0);
         }
     }
-    phclk_mark(s_pc, LEMGPU_PHASE_EROSION);
+    if constexpr (PH) phclk_mark(s_pc, LEMGPU_PHASE_EROSION);
   }
 
   // ---- counters: one atomic per warp for the whole kernel
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
   }
   if (tid == 0) atomicMax(&ctl->tile_nlev, maxl);
   __syncthreads();
-  phclk_end(s_pc, LEMGPU_PHASE_EROSION, ctl);
+  if constexpr (PH) phclk_end(s_pc, LEMGPU_PHASE_EROSION, ctl);
   if (tid == 0) atomicMax(&ctl->t_t_end, globaltimer());
 }
 

@@ -402,15 +402,17 @@ StepArgs step_args(const lemgpu_ctx* ctx, uint32_t p) {
   return a;
 }
 
-template <int CONN, bool EX, bool MF = false>
+template <int CONN, bool EX, bool MF = false, bool PH = true>
 const void* tiles_fn_nk(int nk) {
-  return nk == 1 ? (const void*)k_tiles<CONN, 1, EX, MF> : nk == 2 ? (const void*)k_tiles<CONN, 2, EX, MF>
-                                                                    : (const void*)k_tiles<CONN, 0, EX, MF>;
+  return nk == 1 ? (const void*)k_tiles<CONN, 1, EX, MF, PH> : nk == 2 ? (const void*)k_tiles<CONN, 2, EX, MF, PH>
+                                                                        : (const void*)k_tiles<CONN, 0, EX, MF, PH>;
 }
 // (routing = kMfd: the MF instantiation reads the MFD area from global
 // memory; the count layout serves for its escape marks whatever the cell area)
 const void* tiles_fn(const StepArgs& a) {
   if (a.mfd_A) return a.conn == 8 ? tiles_fn_nk<8, true, true>(a.nkind) : tiles_fn_nk<4, true, true>(a.nkind);
+  if (a.lut_exact && !a.phclk)  // the production instantiation: no phase clocks
+    return a.conn == 8 ? tiles_fn_nk<8, true, false, false>(a.nkind) : tiles_fn_nk<4, true, false, false>(a.nkind);
   if (a.lut_exact) return a.conn == 8 ? tiles_fn_nk<8, true>(a.nkind) : tiles_fn_nk<4, true>(a.nkind);
   return a.conn == 8 ? tiles_fn_nk<8, false>(a.nkind) : tiles_fn_nk<4, false>(a.nkind);
 }
@@ -782,6 +784,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   ctx->opt_mfd_levels = o.mfd_levels != 0;
   a.force_escape = 0;
   a.force_escape = o.force_escape;
+  a.phclk = o.phase_clocks ? 1 : 0;
   {
     const void* ft = tiles_fn(a);
     CUB(cudaFuncSetAttribute(ft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiles_smem(a)));

@@ -74,7 +74,10 @@ bool same(const SimParams& a, const SimParams& b) {
 std::unique_ptr<Ctx> make_ctx(int w, int h, int conn, const SimParams& p, int device) {
   auto c = std::make_unique<Ctx>();
   const lemgpu_params q = to_abi(p, conn);
-  const int rc = lemgpu_create(device, static_cast<std::uint32_t>(w), static_cast<std::uint32_t>(h), &q, &c->h);
+  lemgpu_options o{};
+  o.phase_clocks = 1;  // StepDiagnostics::timings / RunResult::phase_totals
+  const int rc = lemgpu_create_ex(device, static_cast<std::uint32_t>(w), static_cast<std::uint32_t>(h), 1, &q, nullptr,
+                                  &o, &c->h);
   if (rc != LEMGPU_OK) raise(rc, lemgpu_error_message(nullptr), kNoFlow);
   c->w = w;
   c->hgt = h;

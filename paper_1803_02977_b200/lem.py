@@ -251,6 +251,7 @@ _KNOB_NAMES = {
     "LEMGPU_LUT_ENTRIES": ("lut_entries", int), "LEMGPU_HOST_BANDS": ("host_bands", int),
     "LEMGPU_PATCH_CAP": ("patch_cap", int), "LEMGPU_HOST_PROFILE": ("host_profile", int),
     "LEMGPU_ESC_FOREST": ("esc_forest", int), "LEMGPU_MFD_LEVELS": ("mfd_levels", int),
+    "LEMGPU_PHASE_CLOCKS": ("phase_clocks", int),
 }
 
 
@@ -499,7 +500,8 @@ class SimWorkspace:
         if self.gpu is None or self._key != key:
             if self.gpu is not None:
                 self.gpu.close()
-            self.gpu = DeviceContext(grid.width, grid.height, params, grid.nbh.connectivity, device)
+            self.gpu = DeviceContext(grid.width, grid.height, params, grid.nbh.connectivity, device,
+                                     options={"phase_clocks": 1})  # StepDiagnostics::timings
             self._key = key
             self._routing = (Routing.kD8, 1.0)
         want = (setup.routing, setup.mfd_exponent) if setup is not None else (Routing.kD8, 1.0)
@@ -632,7 +634,8 @@ def run_simulation(initial, cfg: Optional[RunConfig] = None,
         cfg, initial = initial, None
     cfg.validate()
     _check_strategy(StepSetup(routing=cfg.routing, mfd_exponent=cfg.mfd_exponent), cfg.strategy)
-    ctx = DeviceContext(cfg.width, cfg.height, cfg.params, cfg.connectivity, cfg.strategy.device)
+    ctx = DeviceContext(cfg.width, cfg.height, cfg.params, cfg.connectivity, cfg.strategy.device,
+                        options={"phase_clocks": 1})  # RunResult::phase_totals
     try:
         if cfg.routing == Routing.kMfd:
             ctx.set_routing(cfg.routing, cfg.mfd_exponent)

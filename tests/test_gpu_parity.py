@@ -857,3 +857,24 @@ def test_mfd_filled_dem_vs_oracle(oracle, mode):
         assert np.array_equal(m["A"].view(np.uint64), o["A"].view(np.uint64)), s
         assert np.array_equal(m["order"], o["mfd_order"]) and np.array_equal(m["levels"], o["mfd_levels"])
     assert d.mfd_passes >= 2
+
+
+@pytest.mark.parametrize("clocks", [0, 1], ids=["off", "on"])
+def test_phase_clock_option(oracle, clocks):
+    """lemgpu_options::phase_clocks: on, lemgpu_diag.seconds holds lem::Phase
+    seconds that add up to the step's device time (every phase of a tile-path
+    step charged); off (the production default), they are 0 -- and the
+    elevations are the oracle's either way."""
+    w, h = 300, 200
+    ctx = device_ctx(w, h, options={"phase_clocks": clocks})
+    e = oracle.terrain(w, h, 81)
+    ctx.upload(e)
+    for _ in range(2):
+        d = ctx.step(1)[0]
+        oracle.step(e, want_donor=False)
+    assert np.array_equal(ctx.download().view(np.uint64), e.view(np.uint64))
+    if clocks:
+        assert all(x >= 0.0 for x in d.seconds) and sum(d.seconds) > 0.0
+        assert d.seconds[0] > 0.0 and d.seconds[2] > 0.0 and d.seconds[5] > 0.0  # receivers, order, erosion
+    else:
+        assert all(x == 0.0 for x in d.seconds)
