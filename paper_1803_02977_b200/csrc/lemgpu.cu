@@ -1064,7 +1064,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   constexpr uint32_t kRq = (uint32_t)(kBY / std::gcd(kBY, kTY));  // lcm(kBY, kTY) / kTY
   const uint32_t R = ((nty + (uint32_t)ctx->bands - 1) / (uint32_t)ctx->bands + kRq - 1) / kRq * kRq;
   const uint32_t nb = (nty + R - 1) / R;
-  while (ctx->band_ev.size() < 2 * (size_t)nb + 1) {
+  while (ctx->band_ev.size() < 3 * (size_t)nb + 2) {
     cudaEvent_t e;
     CU(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->band_ev.push_back(e);
@@ -1072,6 +1072,8 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   cudaEvent_t* eh = ctx->band_ev.data();  // band b uploaded
   cudaEvent_t* et = eh + nb;              // band b's tiles done
   cudaEvent_t e0 = eh[2 * nb];
+  cudaEvent_t* ed = eh + 2 * nb + 1;      // band b's copies down done
+  cudaEvent_t eg = eh[3 * nb + 1];        // the escaped cells' values gathered
   cudaEvent_t* tev = nullptr;
   if (ctx->timing) {  // step events as enqueue_step records them
     while (ctx->ev.size() < 2) {
@@ -1143,6 +1145,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     }
     const uint32_t body_end = b + 1 < nb ? r1 - std::min<uint32_t>(kHalo, r1 - r0) : r1;
     if ((rc = down(r0, body_end))) return rc;
+    CU(ctx, cudaEventRecord(ed[b], ctx->s_d2h));
   }
   if ((rc = enqueue_escape_eager(ctx, a, st))) return rc;
   {
@@ -1151,6 +1154,7 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     k_esc_gather<<<ctx->scan_grid, kTPB, 0, st>>>(a, reinterpret_cast<uint32_t*>(hp + 16),
                                                  reinterpret_cast<double*>(hp + 16 + (size_t)ctx->patch_cap * 4),
                                                  reinterpret_cast<uint32_t*>(hp), ctx->patch_cap);
+    CU(ctx, cudaEventRecord(eg, st));
   }
   enqueue_stats_pass(ctx, a, st);  // the input buffer is complete and unchanged by now
   if ((rc = enqueue_stats(ctx, a, st))) return rc;
@@ -1164,6 +1168,43 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   ctx->have_graph = true;
   using clk = std::chrono::steady_clock;
   const auto tq0 = clk::now();
+  // the escaped cells' values are gathered while the last bands are still on
+  // their way down: patch the cells of the bands already down now (rows above
+  // the first band whose copies are pending, less its predecessor's last
+  // kHalo rows, which travel with it), the rest after the copies
+  const uint32_t* pcells = ctx->h_patch + 4;
+  const double* pvals = reinterpret_cast<const double*>(reinterpret_cast<const char*>(ctx->h_patch) + 16 +
+                                                        (size_t)ctx->patch_cap * 4);
+  auto patch = [&](uint32_t n, uint32_t row_lo, uint32_t row_hi) {
+    // random writes into the raster: latency-bound, spread over a few threads
+    const uint32_t nt = n < 65536u ? 1u : std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
+    const uint64_t lo = (uint64_t)row_lo * W, hi = (uint64_t)row_hi * W;
+    auto part = [&](uint32_t t) {
+      const uint32_t i0 = (uint32_t)((uint64_t)n * t / nt), i1 = (uint32_t)((uint64_t)n * (t + 1) / nt);
+      for (uint32_t i = i0; i < i1; ++i)
+        if (pcells[i] >= lo && pcells[i] < hi) elev[pcells[i]] = pvals[i];
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(part, t);
+    part(0);
+    for (auto& th : pool) th.join();
+  };
+  uint32_t early_rows = 0;
+  CU(ctx, cudaEventSynchronize(eg));
+  const uint32_t n_early = *reinterpret_cast<volatile uint32_t*>(ctx->h_patch);
+  if (n_early <= ctx->patch_cap) {
+    uint32_t bd = 0;  // first band whose copies down are pending
+    while (bd < nb && cudaEventQuery(ed[bd]) == cudaSuccess) ++bd;
+    if (bd == nb) {
+      early_rows = Ht;
+    } else if (bd > 0) {
+      uint32_t r0, r1;
+      rows(bd, r0, r1);
+      early_rows = r0 > kHalo ? r0 - kHalo : 0u;
+    }
+    if (early_rows) patch(n_early, 0, early_rows);
+  }
+  const auto tqe = clk::now();
   CU(ctx, cudaStreamSynchronize(ctx->s_d2h));
   const auto tq1 = clk::now();
   lemgpu_diag d{};
@@ -1176,30 +1217,20 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
       cudaMemcpy(elev, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost);
     return rc;
   }
-  // patch the cells of the escaped trees
+  // patch the cells of the escaped trees (those of the bands that were still
+  // on their way down)
   const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctx->h_patch);
   if (n > ctx->patch_cap) {
     CU(ctx, cudaMemcpy(elev, ctx->hbuf[ctx->cur], (size_t)a.N * sizeof(double), cudaMemcpyDeviceToHost));
-  } else {
-    const uint32_t* cells = ctx->h_patch + 4;
-    const double* vals = reinterpret_cast<const double*>(reinterpret_cast<const char*>(ctx->h_patch) + 16 +
-                                                         (size_t)ctx->patch_cap * 4);
-    // random writes into the raster: latency-bound, spread over a few threads
-    const uint32_t nt = n < 65536u ? 1u : std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
-    auto part = [&](uint32_t t) {
-      const uint32_t i0 = (uint32_t)((uint64_t)n * t / nt), i1 = (uint32_t)((uint64_t)n * (t + 1) / nt);
-      for (uint32_t i = i0; i < i1; ++i) elev[cells[i]] = vals[i];
-    };
-    std::vector<std::thread> pool;
-    for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(part, t);
-    part(0);
-    for (auto& th : pool) th.join();
+  } else if (early_rows < Ht) {
+    patch(n, early_rows, Ht);
   }
   if (ctx->host_profile) {
     const auto tq3 = clk::now();
     auto ms = [](clk::duration x) { return std::chrono::duration<double, std::milli>(x).count(); };
-    std::fprintf(stderr, "step_host_banded: enqueue %.3f ms, then d2h done %.3f ms, sync %.3f ms, patch of %u cells %.3f ms\n",
-                 ms(tq0 - tb0), ms(tq1 - tq0), ms(tq2 - tq1), n, ms(tq3 - tq2));
+    std::fprintf(stderr, "step_host_banded: enqueue %.3f ms, gather + early patch (rows < %u) %.3f ms, then d2h done "
+                 "%.3f ms, sync %.3f ms, patch of %u cells %.3f ms\n",
+                 ms(tq0 - tb0), early_rows, ms(tqe - tq0), ms(tq1 - tqe), ms(tq2 - tq1), n, ms(tq3 - tq2));
   }
   return LEMGPU_OK;
 }
