@@ -1091,17 +1091,28 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     r0 = b * R * (uint32_t)kTY;
     r1 = std::min((b + 1) * R * (uint32_t)kTY, Ht);
   };
+  // band b goes up with the first two rows of band b+1, which k_recv of band b
+  // reads: k_recv(b) waits only for its own upload (k_tiles of band b reads
+  // codes kLY+1 rows into band b+1, i.e. waits for k_recv(b+1))
+  constexpr uint32_t kHead = 2;
+  auto up = [&](uint32_t r0, uint32_t r1) -> int {
+    if (r1 > r0)
+      CU(ctx, cudaMemcpyAsync(ctx->hbuf[p] + (size_t)r0 * W, elev + (size_t)r0 * W, (size_t)(r1 - r0) * W * sizeof(double),
+                              cudaMemcpyHostToDevice, ctx->s_h2d));
+    return LEMGPU_OK;
+  };
+  uint32_t up_to = 0;  // rows [0, up_to) are on their way up
   for (uint32_t b = 0; b < nb; ++b) {
     uint32_t r0, r1;
     rows(b, r0, r1);
-    CU(ctx, cudaMemcpyAsync(ctx->hbuf[p] + (size_t)r0 * W, elev + (size_t)r0 * W, (size_t)(r1 - r0) * W * sizeof(double),
-                            cudaMemcpyHostToDevice, ctx->s_h2d));
+    const uint32_t want = b + 1 < nb ? std::min(r1 + kHead, Ht) : Ht;
+    int rcu;
+    if ((rcu = up(std::max(up_to, r0), want))) return rcu;
+    up_to = std::max(up_to, want);
     CU(ctx, cudaEventRecord(eh[b], ctx->s_h2d));
   }
-  // k_recv of band b reads h two rows into band b+1; k_tiles of band b reads
-  // codes kLY+1 rows into band b+1
   auto recv = [&](uint32_t b) -> int {
-    CU(ctx, cudaStreamWaitEvent(st, eh[std::min(b + 1, nb - 1)], 0));
+    CU(ctx, cudaStreamWaitEvent(st, eh[b], 0));
     uint32_t r0, r1;
     rows(b, r0, r1);
     StepArgs ab = a;
