@@ -1091,10 +1091,11 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     r0 = b * R * (uint32_t)kTY;
     r1 = std::min((b + 1) * R * (uint32_t)kTY, Ht);
   };
-  // band b goes up with the first two rows of band b+1, which k_recv of band b
-  // reads: k_recv(b) waits only for its own upload (k_tiles of band b reads
-  // codes kLY+1 rows into band b+1, i.e. waits for k_recv(b+1))
-  constexpr uint32_t kHead = 2;
+  // band b goes up with the first kBY + 2 rows of band b+1: k_recv of band b
+  // also computes the codes of band b+1's first row block (k_tiles of band b
+  // reads them, kLY + 1 rows deep), so k_recv(b) and k_tiles(b) wait only for
+  // band b's own upload, and band b's copy down trails its upload by one band
+  constexpr uint32_t kHead = kBY + 2;
   auto up = [&](uint32_t r0, uint32_t r1) -> int {
     if (r1 > r0)
       CU(ctx, cudaMemcpyAsync(ctx->hbuf[p] + (size_t)r0 * W, elev + (size_t)r0 * W, (size_t)(r1 - r0) * W * sizeof(double),
@@ -1111,21 +1112,22 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     up_to = std::max(up_to, want);
     CU(ctx, cudaEventRecord(eh[b], ctx->s_h2d));
   }
-  auto recv = [&](uint32_t b) -> int {
+  auto recv = [&](uint32_t b) -> int {  // row blocks [r0 (+ kBY after band 0), r1 + kBY)
     CU(ctx, cudaStreamWaitEvent(st, eh[b], 0));
     uint32_t r0, r1;
     rows(b, r0, r1);
+    const uint32_t q0 = b ? r0 + (uint32_t)kBY : r0, q1 = std::min(r1 + (uint32_t)kBY, Ht);
+    if (q1 <= q0) return LEMGPU_OK;
     StepArgs ab = a;
-    ab.by0 = r0 / kBY;
-    const dim3 g((W + kBX - 1) / kBX, (r1 - r0 + kBY - 1) / kBY);
+    ab.by0 = q0 / kBY;
+    const dim3 g((W + kBX - 1) / kBX, (q1 - q0 + kBY - 1) / kBY);
     void* rargs[] = {&ab, &ctx->hmap[p]};
     CU(ctx, cudaLaunchKernel(recv_fn(a), g, dim3(kTPB), rargs, 0, st));
     return LEMGPU_OK;
   };
-  int rc = recv(0);
-  if (rc) return rc;
+  int rc;
   for (uint32_t b = 0; b < nb; ++b) {
-    if (b + 1 < nb && (rc = recv(b + 1))) return rc;
+    if ((rc = recv(b))) return rc;
     StepArgs ab = a;
     ab.t_lo = b * R * ntx;
     ab.t_hi = std::min((b + 1) * R, nty) * ntx;
