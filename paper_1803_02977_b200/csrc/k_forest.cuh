@@ -333,11 +333,12 @@ __global__ void __launch_bounds__(kFTPB, 1) k_esc_forest(StepArgs a) {
   Dl = 0;
   for (uint32_t j = 0; j < kFNW; ++j) Dl = max(Dl, s.red[j]);
   __syncthreads();
-  // the warps that sweep the counts: about two cells per thread of an average
-  // level (every idle warp would still pay the per-level bookkeeping and the
-  // barrier); the others skip the sweep
+  // the warps that sweep the counts: about half a cell per thread of an
+  // average level (measured: one warp per 16 cells of an average level beats
+  // one per 64 -- dem1000fill's counts 0.69 -> 0.56 ms -- and one per 8 or 32);
+  // the others skip the sweep
   const uint32_t avgw = (P1 - P0) / max(Dl, 1u);
-  uint32_t nact = 32u * min(kFNW, max(2u, (avgw + 63u) / 64u));
+  uint32_t nact = 32u * min(kFNW, max(2u, (avgw + 15u) / 16u));
   bool act = tid < nact;
   // ---- 6. drainage counts, deepest level first: each cell adds its final
   // count to its receiver's slot (shared-memory ring; global for wide levels).
