@@ -1065,8 +1065,8 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
   const uint32_t R = ((nty + (uint32_t)ctx->bands - 1) / (uint32_t)ctx->bands + kRq - 1) / kRq * kRq;
   const uint32_t nb = (nty + R - 1) / R;
   while (ctx->band_ev.size() < 3 * (size_t)nb + 2) {
-    cudaEvent_t e;
-    CU(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t e;  // timed only for host_profile's band timeline
+    CU(ctx, cudaEventCreateWithFlags(&e, ctx->host_profile ? cudaEventDefault : cudaEventDisableTiming));
     ctx->band_ev.push_back(e);
   }
   cudaEvent_t* eh = ctx->band_ev.data();  // band b uploaded
@@ -1244,6 +1244,15 @@ int step_host_banded(lemgpu_ctx* ctx, double* elev, lemgpu_diag* diag) {
     std::fprintf(stderr, "step_host_banded: enqueue %.3f ms, gather + early patch (rows < %u) %.3f ms, then d2h done "
                  "%.3f ms, sync %.3f ms, patch of %u cells %.3f ms\n",
                  ms(tq0 - tb0), early_rows, ms(tqe - tq0), ms(tq1 - tqe), ms(tq2 - tq1), n, ms(tq3 - tq2));
+    // device timeline from e0 (ms): band uploaded / tiles done / copies down done, and the gather
+    auto el = [&](cudaEvent_t e) {
+      float t = -1.f;
+      cudaEventElapsedTime(&t, e0, e);
+      return t;
+    };
+    std::fprintf(stderr, "  bands %u:", nb);
+    for (uint32_t b = 0; b < nb; ++b) std::fprintf(stderr, " [%.2f %.2f %.2f]", el(eh[b]), el(et[b]), el(ed[b]));
+    std::fprintf(stderr, " gather %.2f\n", el(eg));
   }
   return LEMGPU_OK;
 }
