@@ -398,8 +398,24 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
         break;
       }
     }
+    // EX: the cell counts of the levels listed so far need only the receiver
+    // codes, so while warp 0 lists the deep levels alone the other warps
+    // already walk those cells' ancestors (cnt_from: where the counts go on)
+    uint32_t cnt_from = 0;
     if (warp_mode) {
       __syncthreads();  // the last block level is listed
+      if (EX && !MF && tid >= 32) {
+        const uint32_t lv1 = nl > 1 ? s.lvs[1] : qpos;
+        for (uint32_t i = lv1 + tid - 32; i < qpos; i += kTTPB - 32) {
+          uint32_t p = s.list[i], code = RC(p);
+          do {
+            p = (uint32_t)((int)p + woff(code));
+            atomicAdd(reinterpret_cast<uint32_t*>(&ACC(p)), 1u);
+            code = RC(p);
+          } while (code != kNoFlowCode);
+        }
+      }
+      cnt_from = qpos;
       if (tid < 32) {
         uint32_t fs = s.lvs[nl - 1];  // frontier: level nl-1
         for (;;) {
@@ -439,7 +455,10 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
                   r = (uint32_t)((int)r + woff(code));
                   code = RC(r);
                 }
-                ESC_SET(r);
+                if (EX)  // atomically: the other warps' count adds may hit the same word
+                  atomicOr(reinterpret_cast<uint32_t*>(s.acc) + (r - kQ0), 0x80000000u);
+                else
+                  ESC_SET(r);
               }
             }
             run += __shfl_sync(0xffffffffu, inc, 31);
@@ -492,7 +511,8 @@ __global__ void __launch_bounds__(kTTPB, EX ? LEMGPU_TILE_MINB : 2) k_tiles(Step
     if (EX) {
       // cell counts: every cell adds 1 to each ancestor (integer adds commute)
       // (MF: the erosion reads the MFD drainage area, simulation.cpp:55-60)
-      for (uint32_t i = (nl > 1 && !MF ? s.lvs[1] : 0u) + tid; i < (nl > 1 && !MF ? s.lvs[nl] : 0u); i += kTTPB) {
+      const uint32_t c0 = cnt_from ? cnt_from : s.lvs[1];
+      for (uint32_t i = (nl > 1 && !MF ? c0 : 0u) + tid; i < (nl > 1 && !MF ? s.lvs[nl] : 0u); i += kTTPB) {
         uint32_t p = s.list[i], code = RC(p);
         do {
           p = (uint32_t)((int)p + woff(code));

@@ -1,0 +1,8 @@
+# A/B of two builds (tools/var_base.so, tools/var_new.so) on the default workload and dem1000 / dem4000n2
+LEMGPU_LIB=tools/var_new.so timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider 2>&1 | tail -1
+for i in 1 2 3; do for so in tools/var_base.so tools/var_new.so; do
+  LEMGPU_LIB=$so timeout -s KILL 200 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$so', round(d['ms_per_step'],4))"
+done; done
+for wl in dem1000 dem4000n2; do for so in tools/var_base.so tools/var_new.so tools/var_base.so tools/var_new.so; do
+  LEMGPU_LIB=$so timeout -s KILL 200 python bench.py --workload $wl --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$wl $so', round(d['ms_per_step'],4))"
+done; done
