@@ -124,16 +124,17 @@ __device__ __noinline__ double glibc_pow_dev(int pow_fma, double x, double y) {
 }
 
 // pow(x, 2) bit-identical with the host glibc: RN(x*x) unless x^2 is within
-// 1/32 ulp of a rounding midpoint (glibc_pow_sq), else the full restatement.
+// 1/64 ulp of a rounding midpoint or outside [2^-128, 2^128) (glibc_pow_sq),
+// else the full restatement.
 __device__ __forceinline__ double glibc_pow_sq_dev(int pow_fma, double x) {
   if (x == 0.0) return 0.0;
   const double hi = __dmul_rn(x, x);
   const double lo = __fma_rn(x, x, -hi);
   const unsigned long long b = (unsigned long long)__double_as_longlong(hi);
   const uint32_t e = (uint32_t)(b >> 52) & 0x7ffu;
-  if (e > 100u && e < 2000u) {
+  if (e - (1023u - 128u) < 256u) {  // x^2 in [2^-128, 2^128): the 1/64-ulp bound of glibc_pow_sq holds
     const double ulp = __longlong_as_double((long long)(e - 52u) << 52);
-    const double lim = (b & 0x000fffffffffffffull) ? __dmul_rn(ulp, 0.46875) : __dmul_rn(ulp, 0.21875);
+    const double lim = (b & 0x000fffffffffffffull) ? __dmul_rn(ulp, 0.484375) : __dmul_rn(ulp, 0.234375);
     if (fabs(lo) < lim) return hi;
   }
   return glibc_pow_dev(pow_fma, x, 2.0);

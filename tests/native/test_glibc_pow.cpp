@@ -116,10 +116,22 @@ int main(int argc, char** argv) {
   // the n = 2 fast path: glibc_pow_sq(x) == pow(x, 2), on random x and on x
   // whose square sits near a rounding midpoint (x = sqrt of a midpoint, nudged)
   uint64_t bad_sq = 0, nsq = 0;
+  uint64_t nband = 0;
   for (uint64_t i = 0; i < count / 2; ++i) {
     double x;
-    if (i & 1) {
+    if (i % 4 == 1) {
       x = std::ldexp(u01() + 0.5, (int)(next_u64() % 120) - 80);
+    } else if (i % 4 == 3) {
+      // x^2 between 1/64 and 1/16 ulp away from a rounding midpoint: the band
+      // the fast path newly decides (it answered only beyond 1/32 before)
+      for (;;) {
+        x = std::ldexp(u01() + 0.5, (int)(next_u64() % 136) - 68);
+        const double hi = x * x, lo = std::fma(x, x, -hi);
+        const double ulp = std::ldexp(1.0, std::ilogb(hi) - 52);
+        const double d = ulp / 2 - std::fabs(lo);
+        if (d >= ulp / 64 && d < ulp / 16) break;
+      }
+      ++nband;
     } else {
       const double m = std::ldexp(1.0 + u01(), (int)(next_u64() % 100) - 70);  // a square
       const double mid = m + std::ldexp(1.0, std::ilogb(m) - 53);            // the midpoint above it
@@ -135,7 +147,8 @@ int main(int argc, char** argv) {
       ++bad_sq;
     }
   }
-  std::printf("glibc_pow_sq: %llu inputs, %llu mismatches\n", (unsigned long long)nsq, (unsigned long long)bad_sq);
+  std::printf("glibc_pow_sq: %llu inputs (%llu within 1/16 ulp of a midpoint), %llu mismatches\n",
+              (unsigned long long)nsq, (unsigned long long)nband, (unsigned long long)bad_sq);
   bad += bad_sq;
   // identities the n = 1 and n = 2 Newton paths rely on (k_physics.cuh):
   // pow(x, 1) == x and pow(x, 0) == 1 for every positive finite x (normal or not)
