@@ -69,11 +69,14 @@ constexpr int kDN = kDH * kWP;           // per-cell arrays: the domain rows
 constexpr int kRN = (kDH + 2) * kWP;     // receiver codes: the domain rows and the ring rows
 constexpr int kCap = kDW * kDH;          // queue: every domain cell at most once
 constexpr int kTMaxLev = 64;             // deeper trees escape
+// measured (round 2, after the counts overlap; 10000^2 ms/step): BFS 32 / 48 /
+// 64 with ERO 0: 2.032 / 2.026 / 2.028; ERO 8 / 16 / 32 with BFS 32: 2.044 /
+// 2.046 / 2.048 -- the one-warp erosion tail no longer pays
 #ifndef LEMGPU_SMALL_BFS
-#define LEMGPU_SMALL_BFS 32
+#define LEMGPU_SMALL_BFS 48
 #endif
 #ifndef LEMGPU_SMALL_ERO
-#define LEMGPU_SMALL_ERO 32
+#define LEMGPU_SMALL_ERO 0
 #endif
 constexpr int kSmallLevel = LEMGPU_SMALL_BFS;  // levels this small are expanded by one warp
 constexpr int kSmallEro = LEMGPU_SMALL_ERO;    // erosion levels this small (in total) run on one warp
