@@ -335,8 +335,9 @@ int lemgpu_debug_tile_capture(lemgpu_ctx* ctx, int enable);
  * bit-identical with the reference on this host).  ctx may be NULL. */
 int lemgpu_pow_variant(const lemgpu_ctx* ctx);
 /* Test hook (no reference counterpart): out[i] = pow(x[i], y[i]) computed by
- * the device restatement of glibc pow (variant as above) on `device`; host
- * arrays of n doubles.  Lets the tests compare it with the host libm. */
+ * the device restatement of glibc pow (variant as above) on `device` -- for
+ * y = 2 through the n = 2 Newton fast path; host arrays of n doubles.  Lets
+ * the tests compare it with the host libm. */
 int lemgpu_debug_pow(int device, int variant, const double* x, const double* y, double* out, uint64_t n);
 
 /* Pin / unpin caller host memory (cudaHostRegister) for fast H2D/D2H. */
