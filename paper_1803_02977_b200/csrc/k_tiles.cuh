@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_gather(StepArgs a, uint32_t* cells
 
 // ---------------------------------------------------------------------------
 // The escaped trees in shared memory: the roots are split evenly over the
-// CTAs (one per SM) and each CTA finishes its share of trees alone -- the
+// CTAs (kEscSmallPerSM per SM) and each CTA finishes its share of trees alone -- the
 // same breadth-first levels (donor masks from the receiver codes), the
 // reference's FP accumulation in slot order, uplift and erosion level by level
 // -- with block barriers only, instead of the cooperative global path whose
@@ -717,7 +717,19 @@ __global__ void __launch_bounds__(kTPB) k_esc_gather(StepArgs a, uint32_t* cells
 // trees already written get the same bits again) and this kernel's counters
 // are dropped.  Otherwise the last CTA marks the escape work done.
 constexpr int kEscSmallRoots = 1024;
-constexpr int kEscSmallCap = 6144;
+// cells per CTA share, CTAs per SM: measured (round 2) 6144 x 1 / 2048 x 3 /
+// 1536 x 4 / 1024 x 6: 10000^2 2.033 / 2.020 / 2.020 / 2.037 ms/step, ens64
+// 5.617 / 5.587 / 5.586 / 5.60 (a share beyond the capacity fails over to the
+// cooperative path, exactly as before)
+#ifndef LEMGPU_ESC_SMALL_CAP
+#define LEMGPU_ESC_SMALL_CAP 2048
+#define LEMGPU_ESC_SMALL_PER_SM 3
+#endif
+#ifndef LEMGPU_ESC_SMALL_PER_SM
+#define LEMGPU_ESC_SMALL_PER_SM 1
+#endif
+constexpr int kEscSmallCap = LEMGPU_ESC_SMALL_CAP;
+constexpr int kEscSmallPerSM = LEMGPU_ESC_SMALL_PER_SM;
 constexpr int kEscSmallLev = 64;  // deeper shares fail early (deep plans belong to the cooperative path)
 struct EscSmallSmem {
   double h[kEscSmallCap];  // the step's input elevation (staged at discovery), then the new one

@@ -69,7 +69,7 @@ struct lemgpu_ctx {
   CUtensorMap tmap[2]{};  // ... k_tiles box
   uint32_t* d_levels_esc = nullptr;
   bool esc_small = true;  // k_esc_small ahead of the cooperative escape path
-  int esc_small_grid = 1;  // its CTAs (one per SM)
+  int esc_small_grid = 1;  // its CTAs (kEscSmallPerSM per SM)
   int pipe = 0, pipe_tile_grid = 0;  // pipelined receivers / tiles (bands), k_tiles CTAs per band
   int pipe_chain = 1;                // receiver bands chained (else independent)
   int pow_variant = -1;              // host_pow_variant(): the glibc pow the device reproduces
@@ -806,7 +806,7 @@ int create_impl(int device, uint32_t W, uint32_t H, uint32_t M, const lemgpu_par
   a.eager = 0;
   a.force_deep = o.force_deep ? 1 : 0;
   if (o.no_esc_small) ctx->esc_small = false;
-  ctx->esc_small_grid = nsm;
+  ctx->esc_small_grid = kEscSmallPerSM * nsm;
   {  // pipelined receivers / tiles for tall rasters: 24 bands (measured best at 10000^2: 2.127 -> 2.061 ms)
     const uint32_t nty = (H * M + kTY - 1) / kTY;
     ctx->pipe = nty >= 256 ? 24 : 0;  // (5000^2: 157 tile rows, banding costs more than it overlaps)
