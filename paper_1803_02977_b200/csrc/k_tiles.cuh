@@ -777,6 +777,9 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
     for (;;) {
       const uint32_t ls = s.lvl[nl - 1], le = s.lvl[nl];
       uint32_t carry = le;
+      // the other CTAs' failure flag, loaded now so that its L2 round trip
+      // overlaps this level's donor masks (published to the block below)
+      const uint32_t fail_seen = tid == 0 ? ld_volatile_u32(&ctl->esc_fail) : 0u;
       for (uint32_t b0 = ls; b0 < le; b0 += kTPB) {
         const uint32_t i = b0 + tid;
         uint32_t m = 0;
@@ -807,7 +810,7 @@ __global__ void __launch_bounds__(kTPB) k_esc_small(StepArgs a) {
         carry += tot;
       }
       if (!ok) break;
-      if (tid == 0) s.flag = ld_volatile_u32(&ctl->esc_fail);
+      if (tid == 0) s.flag = fail_seen;
       __syncthreads();
       if (carry == le) break;  // the next level is empty
       if (s.flag) {  // another CTA already failed: the cooperative path will run (uniform: read after the barrier)
