@@ -404,7 +404,10 @@ def main():
     for _ in range(args.warmup):
         one_step()
     ctx.sync()
-    ctx.kernel_timing(True)
+    # no per-step timing events inside the timed region (an event pair around
+    # every graph launch costs ~15 us a step, tools/probe_events.py): the step
+    # time is the timed region's own events / K, the kernel spans come from the
+    # steps' diagnostics (device %globaltimer stamps, lemgpu_diag::kernel_s)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -422,8 +425,12 @@ def main():
         diags = ctx.sync()  # raises on any failing step
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
-    kt = ctx.kernel_times()
-    ctx.kernel_timing(False)
+    timed = diags[-args.steps:]
+    kt = {"launches": len(timed), "step": ms / args.steps * len(timed),
+          "recv_donor": sum(d.kernel_seconds[0] for d in timed) * 1e3,
+          "tiles": sum(d.kernel_seconds[1] for d in timed) * 1e3,
+          "order": sum(d.kernel_seconds[2] for d in timed) * 1e3,
+          "physics": sum(d.kernel_seconds[3] for d in timed) * 1e3}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -549,8 +556,9 @@ def main():
                 "escaped_cells_per_step": esc_cells,
                 "kernel_ms": {"step(events)": step_ms_ev, "k_recv": k1_ms, "k_tiles": tiles_ms,
                               "escape:levels": esc_ord_ms, "escape:physics": esc_phys_ms},
-                "timing_source": "CUDA events around each step's graph launch on the context stream; "
-                                 "kernel spans from device %globaltimer stamps taken by the kernels",
+                "timing_source": "step: CUDA events around the K timed graph launches on the context stream / K "
+                                 "(no per-step events inside the timed region); kernel spans: device %globaltimer "
+                                 "stamps taken by the kernels in those steps (lemgpu_diag::kernel_s)",
                 "step": {"alg_bytes_per_cell": B_STEP, "achieved": per_gpu * B_STEP / 1e9,
                          "frac": per_gpu * B_STEP / 1e9 / peak},
                 "traffic_source": traffic_src}
